@@ -1,0 +1,168 @@
+/*
+ * mpk_b200.h -- C ABI of the B200 (sm_100a) mpkrylov hot path.
+ *
+ * Drop-in boundary for the reference package mpkrylov
+ * (/root/reference/pkg/src/mpkrylov).  The reference is pure Python+numba
+ * with no FFI of its own; each entry point below replaces one Python
+ * function on the hot path (cited per function), takes plain pointers and
+ * sizes, and uses the reference's array layouts: CSR row_ptr/col_idx int64
+ * (sparse.py:192-233), values float64; MC vectors C-contiguous (n, k)
+ * float64 with the most significant component first, complex vectors as a
+ * (re, im) pair of such arrays (sparse.py:341-404, _kernels.py:8-10).
+ * All pointers are HOST pointers unless the name says _dev.
+ *
+ * Status codes: 0 ok, 1 singular pivot, 2 numeric breakdown, 3 invalid
+ * argument, 4 CUDA error.  mpk_last_error() returns a thread-local message.
+ * The Python binding (paper_2504_14498_b200/_lib.py) maps them to the
+ * reference exceptions (ValueError, SingularPivotError,
+ * NumericBreakdownError) and breakdown strings (solvers.py:207-407).
+ */
+#ifndef MPK_B200_H
+#define MPK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPK_OK 0
+#define MPK_SINGULAR_PIVOT 1
+#define MPK_NUMERIC_BREAKDOWN 2
+#define MPK_INVALID 3
+#define MPK_CUDA_ERROR 4
+
+/* methods: solvers.py:57 METHODS order is bicg, cgs, bicgstab, gpbicg */
+#define MPK_BICG 0
+#define MPK_CGS 1
+#define MPK_BICGSTAB 2
+#define MPK_GPBICG 3
+
+/* breakdown codes (solvers.py string in comment) */
+#define MPK_BD_NONE 0              /* None */
+#define MPK_BD_SIGMA_ZERO 1        /* "sigma_zero" */
+#define MPK_BD_RHO_ZERO 2          /* "rho_zero" */
+#define MPK_BD_OMEGA_ZERO 3        /* "omega_zero" */
+#define MPK_BD_NONFINITE 4         /* "nonfinite_residual" */
+#define MPK_BD_BREAKDOWN_LS 5      /* "breakdown_ls" */
+#define MPK_BD_ZETA_ZERO 6         /* "zeta_zero" */
+#define MPK_BD_SINGULAR_PIVOT 7    /* SingularPivotError (ilu.py:60-66) */
+#define MPK_BD_NUMERIC_FACTOR 8    /* NumericBreakdownError, factors */
+#define MPK_BD_NUMERIC_SWEEP 9     /* NumericBreakdownError, sweep */
+
+typedef struct mpk_ctx mpk_ctx;
+typedef struct mpk_matrix mpk_matrix;
+
+typedef struct {
+  int64_t iterations;
+  int32_t converged;
+  int32_t breakdown;      /* MPK_BD_* */
+  int64_t bad_row;        /* SingularPivotError.k */
+  int32_t structural;     /* SingularPivotError(structural=True) */
+  int32_t has_x;
+  double final_recursive_relres; /* SolveReport, solvers.py:88-102 */
+  double true_relres;
+  int64_t hist_len;       /* number of norm2 calls in the method */
+  double factor_ms;       /* device time of the ILU(0) factorization */
+  double solve_ms;        /* device time of the Krylov loop */
+  double total_ms;        /* host wall time of the whole call */
+} mpk_report;
+
+const char *mpk_last_error(void);
+int mpk_version(void);
+
+/* One CUDA device + stream.  Reentrant per context. */
+int mpk_ctx_create(int device, mpk_ctx **out);
+void mpk_ctx_destroy(mpk_ctx *ctx);
+int mpk_ctx_synchronize(mpk_ctx *ctx);
+
+/* CsrMatrix.demoted() upload (sparse.py:192-249): binary64 values, val_im
+ * NULL for the real field.  Columns must be strictly increasing per row. */
+int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
+                   const int64_t *row_ptr, const int64_t *col_idx,
+                   const double *val_re, const double *val_im,
+                   mpk_matrix **out);
+void mpk_csr_free(mpk_matrix *m);
+
+/* ilu0_factorize_demoted (ilu.py:284-286 -> _factorize_tuples :178-276).
+ * Returns MPK_SINGULAR_PIVOT with *bad_row / *structural, or
+ * MPK_NUMERIC_BREAKDOWN for non-finite factors. */
+int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural);
+/* IluFactors.val_re / val_im as (nnz,) arrays (bitwise parity tests) */
+int mpk_ilu0_download(mpk_matrix *m, double *lu_re, double *lu_im);
+/* ilu0_apply on binary64 vectors (ilu.py:410-433): z = U^-1 L^-1 r, or the
+ * adjoint (LU)^-H r.  Complex: separate re/im arrays of length n. */
+int mpk_ilu0_apply_f64(mpk_matrix *m, const double *r_re, const double *r_im,
+                       double *z_re, double *z_im, int adjoint);
+/* ilu0_apply_mixed / _adjoint_mixed (ilu.py:448-470) on (n,k) MC vectors */
+int mpk_ilu0_apply_mixed(mpk_matrix *m, int k, const double *r_re,
+                         const double *r_im, double *z_re, double *z_im,
+                         int adjoint);
+
+/* spmv_mixed / spmv_adjoint_mixed (sparse.py:465-496) on (n,k) vectors */
+int mpk_spmv_mixed(mpk_matrix *m, int k, const double *x_re,
+                   const double *x_im, double *y_re, double *y_im,
+                   int adjoint);
+
+/* hdot (sparse.py:509-517): out_re/out_im k doubles.  norm2 (:532-539).
+ * Device reduction order is a fixed tree. */
+int mpk_hdot(mpk_ctx *ctx, int64_t n, int k, const double *x_re,
+             const double *x_im, const double *y_re, const double *y_im,
+             double *out_re, double *out_im);
+int mpk_norm2(mpk_ctx *ctx, int64_t n, int k, const double *x_re,
+              const double *x_im, double *out);
+/* axpy (sparse.py:542-560): out = y + alpha*x; alpha_im NULL for real */
+int mpk_axpy(mpk_ctx *ctx, int64_t n, int k, const double *alpha_re,
+             const double *alpha_im, const double *x_re, const double *x_im,
+             const double *y_re, const double *y_im, double *out_re,
+             double *out_im);
+
+/* Element-wise MC scalar arithmetic on the device (twin tests of
+ * _mccore.py): op 0 add, 1 sub, 2 mul, 3 div, 4 sqrt(a), 5 complex mul,
+ * 6 complex div, 7 renorm of 7 terms (a is (n,7)), 8 mul((a0,0..), b),
+ * 9 mul(a, (b0,0..)), 10 mul((a0,0..),(b0,0..)).  Arrays (n,k). */
+int mpk_mc_elementwise(mpk_ctx *ctx, int op, int k, int64_t n,
+                       const double *a_re, const double *a_im,
+                       const double *b_re, const double *b_im, double *o_re,
+                       double *o_im);
+/* Host-side MC scalar arithmetic (MCFloat/MCComplex operators,
+ * multicomponent.py:184-231): same op codes, one element, no GPU. */
+int mpk_mc_host(int op, int k, const double *a_re, const double *a_im,
+                const double *b_re, const double *b_im, double *o_re,
+                double *o_im);
+
+/* solve() (solvers.py:418-453) with precond ILU0_MIXED and spmv_mode
+ * "mixed": factorization + method + true residual.  x_re/x_im receive the
+ * solution (n,k); hist receives the norm2 sequence (k doubles per entry,
+ * at most hist_cap entries; rep->hist_len counts all).  max_iter < 0 means
+ * the reference default 3n. */
+int mpk_solve(mpk_matrix *m, int method, int k, double eps_rel,
+              double eps_abs, int64_t max_iter, const double *b_re,
+              const double *b_im, double *x_re, double *x_im, double *hist,
+              int64_t hist_cap, mpk_report *rep);
+
+/* Same, with b and x already resident in HBM in the device PLANAR layout
+ * (component c of element i at p[c*ld + i], ld = mpk_plane_ld(n); complex:
+ * k real planes then k imaginary planes).  hist_dev is device memory. */
+int64_t mpk_plane_ld(int64_t n);
+int mpk_solve_dev(mpk_matrix *m, int method, int k, double eps_rel,
+                  double eps_abs, int64_t max_iter, const double *b_dev,
+                  double *x_dev, double *hist_dev, int64_t hist_cap,
+                  mpk_report *rep);
+/* (n,k) host <-> planar device conversion helpers */
+int mpk_to_planar(mpk_ctx *ctx, int64_t n, int k, const double *re,
+                  const double *im, double *dev);
+int mpk_from_planar(mpk_ctx *ctx, int64_t n, int k, const double *dev,
+                    double *re, double *im, int cx);
+
+/* Independent systems (cfg5 batch): matrices[i] already uploaded, each
+ * solved on its own stream of the context's device.  b/x host (n_i,k). */
+int mpk_solve_batch(int nsys, mpk_matrix **ms, int method, int k,
+                    double eps_rel, double eps_abs, int64_t max_iter,
+                    const double *const *b_re, double *const *x_re,
+                    mpk_report *reps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,141 @@
+"""ctypes binding of the B200 hot-path library (include/mpk_b200.h).
+
+The product path has NO CPU fallback: if libmpkb200.so is missing, or no
+CUDA device is present, the device entry points raise.  Only the host-side
+MC scalar arithmetic (mpk_mc_host, used by MCFloat/MCComplex) works without
+a GPU, exactly like the reference's scalar types run on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import threading
+
+import numpy as np
+
+_SO = pathlib.Path(__file__).resolve().parent / "_lib" / "libmpkb200.so"
+_lib = None
+_lock = threading.Lock()
+_ctx = {}
+
+MPK_OK = 0
+MPK_SINGULAR_PIVOT = 1
+MPK_NUMERIC_BREAKDOWN = 2
+MPK_INVALID = 3
+MPK_CUDA_ERROR = 4
+
+METHOD_CODE = {"bicg": 0, "cgs": 1, "bicgstab": 2, "gpbicg": 3}
+BREAKDOWN = {
+    0: None,
+    1: "sigma_zero",
+    2: "rho_zero",
+    3: "omega_zero",
+    4: "nonfinite_residual",
+    5: "breakdown_ls",
+    6: "zeta_zero",
+    7: "SingularPivotError",
+    8: "NumericBreakdownError",
+    9: "NumericBreakdownError",
+}
+
+# every symbol include/mpk_b200.h declares (checked by tests/test_host.py)
+EXPORTS = (
+    "mpk_last_error", "mpk_version", "mpk_ctx_create", "mpk_ctx_destroy",
+    "mpk_ctx_synchronize", "mpk_csr_upload", "mpk_csr_free", "mpk_ilu0_factor",
+    "mpk_ilu0_download", "mpk_ilu0_apply_f64", "mpk_ilu0_apply_mixed",
+    "mpk_spmv_mixed", "mpk_hdot", "mpk_norm2", "mpk_axpy", "mpk_mc_elementwise",
+    "mpk_mc_host", "mpk_solve", "mpk_plane_ld", "mpk_solve_dev", "mpk_to_planar",
+    "mpk_from_planar", "mpk_solve_batch",
+)
+
+
+class MpkReport(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int64),
+        ("converged", ctypes.c_int32),
+        ("breakdown", ctypes.c_int32),
+        ("bad_row", ctypes.c_int64),
+        ("structural", ctypes.c_int32),
+        ("has_x", ctypes.c_int32),
+        ("final_recursive_relres", ctypes.c_double),
+        ("true_relres", ctypes.c_double),
+        ("hist_len", ctypes.c_int64),
+        ("factor_ms", ctypes.c_double),
+        ("solve_ms", ctypes.c_double),
+        ("total_ms", ctypes.c_double),
+    ]
+
+
+class ExtensionMissing(RuntimeError):
+    pass
+
+
+def lib():
+    """Load libmpkb200.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not _SO.exists():
+                    raise ExtensionMissing(
+                        f"{_SO} not built: run `python -c 'import __graft_entry__ as g;"
+                        f" g.build()'` (nvcc, sm_100a)")
+                L = ctypes.CDLL(str(_SO))
+                L.mpk_last_error.restype = ctypes.c_char_p
+                L.mpk_plane_ld.restype = ctypes.c_int64
+                L.mpk_plane_ld.argtypes = [ctypes.c_int64]
+                _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().mpk_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == MPK_OK:
+        return
+    msg = last_error()
+    if rc == MPK_INVALID:
+        raise ValueError(msg)
+    if rc == MPK_NUMERIC_BREAKDOWN:
+        from .ilu import NumericBreakdownError
+
+        raise NumericBreakdownError(msg)
+    if rc == MPK_SINGULAR_PIVOT:
+        raise RuntimeError(msg)  # callers translate with the row index
+    raise RuntimeError(f"CUDA error in {what}: {msg}")
+
+
+def context(device: int = 0):
+    """Per-device context (one CUDA stream), created on first use."""
+    c = _ctx.get(device)
+    if c is None:
+        with _lock:
+            c = _ctx.get(device)
+            if c is None:
+                p = ctypes.c_void_p()
+                check(lib().mpk_ctx_create(ctypes.c_int(device), ctypes.byref(p)),
+                      "mpk_ctx_create")
+                c = p
+                _ctx[device] = c
+    return c
+
+
+def dptr(a):
+    if a is None:
+        return None
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def plane_ld(n: int) -> int:
+    return int(lib().mpk_plane_ld(ctypes.c_int64(n)))

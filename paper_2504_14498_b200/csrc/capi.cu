@@ -1,0 +1,777 @@
+// capi.cu -- C ABI (include/mpk_b200.h) over the device hot path.
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/mpk_b200.h"
+#include "krylov.cuh"
+
+namespace mpk {
+int host_mc(int op, int k, const double *a_re, const double *a_im,
+            const double *b_re, const double *b_im, double *o_re,
+            double *o_im);
+void launch_to_planar(long long n, int k, const double *re, const double *im,
+                      double *dev, cudaStream_t st);
+void launch_from_planar(long long n, int k, const double *dev, double *re,
+                        double *im, cudaStream_t st);
+}  // namespace mpk
+
+using namespace mpk;
+
+struct mpk_ctx {
+  int device;
+  cudaStream_t stream;
+};
+
+struct mpk_matrix {
+  mpk_ctx *ctx;
+  DMat A;
+  int *rowflag = nullptr;
+  int *fscratch = nullptr;  // [0..1] ticket, [2] bad_row, [3] nonfinite
+  float factor_ms = 0.f;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CKR(x)                                                            \
+  do {                                                                    \
+    cudaError_t e_ = (x);                                                 \
+    if (e_ != cudaSuccess)                                                \
+      return fail(MPK_CUDA_ERROR, std::string(#x) + ": " +                \
+                                      cudaGetErrorString(e_));            \
+  } while (0)
+
+namespace {
+
+__global__ void gather_kernel(const double *src, const int *perm, double *dst,
+                              long long m, int cx) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  if (cx)
+    reinterpret_cast<double2 *>(dst)[q] =
+        reinterpret_cast<const double2 *>(src)[perm[q]];
+  else
+    dst[q] = src[perm[q]];
+}
+
+template <class T>
+int upload(T **dst, const std::vector<T> &v, cudaStream_t st) {
+  if (cudaMalloc(dst, sizeof(T) * (v.size() ? v.size() : 1)) != cudaSuccess)
+    return 4;
+  if (!v.empty())
+    cudaMemcpyAsync(*dst, v.data(), sizeof(T) * v.size(),
+                    cudaMemcpyHostToDevice, st);
+  return 0;
+}
+
+void gather(const double *src, const int *perm, double *dst, long long m,
+            bool cx, cudaStream_t st) {
+  if (m <= 0) return;
+  gather_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(src, perm, dst,
+                                                              m, cx ? 1 : 0);
+}
+
+}  // namespace
+
+namespace mpk {
+
+// Transposed gather structures for spmv_adjoint (ascending source row,
+// _kernels.py:281-297) and the adjoint sweeps (U^T ascending rows,
+// L^T descending rows; ilu.py:346-371).
+void ensure_adjoint(DMat &A, cudaStream_t st) {
+  const int n = A.n;
+  const bool cx = A.cx;
+  if (!A.at_rp) {
+    const auto &rp = A.h_rp, &ci = A.h_ci, &dp = A.h_dp;
+    std::vector<int> cnt(n + 1, 0), ucnt(n + 1, 0), lcnt(n + 1, 0);
+    for (int i = 0; i < n; ++i)
+      for (int p = rp[i]; p < rp[i + 1]; ++p) {
+        cnt[ci[p] + 1]++;
+        if (p > dp[i]) ucnt[ci[p] + 1]++;
+        if (p < dp[i]) lcnt[ci[p] + 1]++;
+      }
+    for (int i = 0; i < n; ++i) {
+      cnt[i + 1] += cnt[i];
+      ucnt[i + 1] += ucnt[i];
+      lcnt[i + 1] += lcnt[i];
+    }
+    std::vector<int> at_ci(cnt[n]), at_perm(cnt[n]), ut_ci(ucnt[n]),
+        ut_perm(ucnt[n]), lt_ci(lcnt[n]), lt_perm(lcnt[n]);
+    std::vector<int> f(cnt.begin(), cnt.end() - 1), uf(ucnt.begin(), ucnt.end() - 1),
+        lf(lcnt.begin(), lcnt.end() - 1);
+    for (int i = 0; i < n; ++i)
+      for (int p = rp[i]; p < rp[i + 1]; ++p) {
+        const int c = ci[p];
+        at_ci[f[c]] = i;
+        at_perm[f[c]++] = p;
+        if (p > dp[i]) {
+          ut_ci[uf[c]] = i;
+          ut_perm[uf[c]++] = p;
+        }
+      }
+    for (int j = n - 1; j >= 0; --j)
+      for (int p = rp[j]; p < dp[j]; ++p) {
+        const int c = ci[p];
+        lt_ci[lf[c]] = j;
+        lt_perm[lf[c]++] = p;
+      }
+    upload(&A.at_rp, cnt, st);
+    upload(&A.at_ci, at_ci, st);
+    upload(&A.at_perm, at_perm, st);
+    upload(&A.ut_rp, ucnt, st);
+    upload(&A.ut_ci, ut_ci, st);
+    upload(&A.ut_perm, ut_perm, st);
+    upload(&A.lt_rp, lcnt, st);
+    upload(&A.lt_ci, lt_ci, st);
+    upload(&A.lt_perm, lt_perm, st);
+    const size_t w = cx ? 2 : 1;
+    cudaMalloc(&A.at_val, sizeof(double) * w * (A.nnz ? A.nnz : 1));
+    cudaMalloc(&A.ut_val, sizeof(double) * w * (ut_ci.size() + 1));
+    cudaMalloc(&A.lt_val, sizeof(double) * w * (lt_ci.size() + 1));
+    gather(A.val, A.at_perm, A.at_val, (long long)at_ci.size(), cx, st);
+    A.h_adj_sizes[0] = (long long)ut_ci.size();
+    A.h_adj_sizes[1] = (long long)lt_ci.size();
+  }
+  if (A.factored && !A.adj_ready) {
+    gather(A.lu, A.ut_perm, A.ut_val, A.h_adj_sizes[0], cx, st);
+    gather(A.lu, A.lt_perm, A.lt_val, A.h_adj_sizes[1], cx, st);
+    A.adj_ready = true;
+  }
+}
+
+}  // namespace mpk
+
+extern "C" {
+
+const char *mpk_last_error(void) { return g_err.c_str(); }
+int mpk_version(void) { return 1; }
+
+int mpk_ctx_create(int device, mpk_ctx **out) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(MPK_CUDA_ERROR, "no CUDA device available");
+  if (device < 0 || device >= ndev)
+    return fail(MPK_INVALID, "device index out of range");
+  CKR(cudaSetDevice(device));
+  mpk_ctx *c = new mpk_ctx;
+  c->device = device;
+  CKR(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  *out = c;
+  return MPK_OK;
+}
+
+void mpk_ctx_destroy(mpk_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int mpk_ctx_synchronize(mpk_ctx *ctx) {
+  CKR(cudaStreamSynchronize(ctx->stream));
+  return MPK_OK;
+}
+
+int64_t mpk_plane_ld(int64_t n) { return plane_ld(n); }
+
+int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
+                   const int64_t *row_ptr, const int64_t *col_idx,
+                   const double *val_re, const double *val_im,
+                   mpk_matrix **out) {
+  // CsrMatrix._validate sparse.py:217-233
+  if (n < 0 || nnz < 0) return fail(MPK_INVALID, "negative size");
+  if (n > INT_MAX - 1 || nnz > INT_MAX)
+    return fail(MPK_INVALID, "matrix too large for int32 indices");
+  if (row_ptr[0] != 0 || row_ptr[n] != nnz)
+    return fail(MPK_INVALID, "inconsistent CSR row_ptr");
+  for (int64_t i = 0; i < n; ++i) {
+    if (row_ptr[i + 1] < row_ptr[i])
+      return fail(MPK_INVALID, "row_ptr must be non-decreasing");
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      const int64_t c = col_idx[p];
+      if (c < 0 || c >= n || (p > row_ptr[i] && c <= col_idx[p - 1]))
+        return fail(MPK_INVALID,
+                    "row " + std::to_string(i) +
+                        ": columns must be strictly increasing and in range");
+    }
+  }
+  CKR(cudaSetDevice(ctx->device));
+  mpk_matrix *m = new mpk_matrix;
+  m->ctx = ctx;
+  DMat &A = m->A;
+  A.n = (int)n;
+  A.nnz = nnz;
+  A.cx = val_im != nullptr;
+  A.h_rp.resize(n + 1);
+  A.h_ci.resize(nnz);
+  A.h_dp.assign(n, -1);
+  for (int64_t i = 0; i <= n; ++i) A.h_rp[i] = (int)row_ptr[i];
+  for (int64_t p = 0; p < nnz; ++p) A.h_ci[p] = (int)col_idx[p];
+  // CsrMatrix._find_diagonals sparse.py:235-243
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+      if (col_idx[p] == i) A.h_dp[i] = (int)p;
+  cudaStream_t st = ctx->stream;
+  if (upload(&A.rp, A.h_rp, st) || upload(&A.ci, A.h_ci, st) ||
+      upload(&A.dp, A.h_dp, st)) {
+    delete m;
+    return fail(MPK_CUDA_ERROR, "allocation failed");
+  }
+  const size_t w = A.cx ? 2 : 1;
+  std::vector<double> vals(w * nnz);
+  for (int64_t p = 0; p < nnz; ++p) {
+    if (A.cx) {
+      vals[2 * p] = val_re[p];
+      vals[2 * p + 1] = val_im[p];
+    } else {
+      vals[p] = val_re[p];
+    }
+  }
+  if (upload(&A.val, vals, st)) {
+    delete m;
+    return fail(MPK_CUDA_ERROR, "allocation failed");
+  }
+  const long long L = plane_ld(n);
+  CKR(cudaMalloc(&A.sw_y, sizeof(double) * w * L));
+  CKR(cudaMalloc(&A.sw_y2, sizeof(double) * w * L));
+  CKR(cudaMalloc(&A.tick, sizeof(int) * 8));
+  CKR(cudaMemsetAsync(A.tick, 0, sizeof(int) * 8, st));
+  CKR(cudaMalloc(&A.err, sizeof(int) * 2));
+  CKR(cudaMemsetAsync(A.err, 0, sizeof(int) * 2, st));
+  CKR(cudaMalloc(&m->rowflag, sizeof(int) * (n + 1)));
+  CKR(cudaMalloc(&m->fscratch, sizeof(int) * 4));
+  CKR(cudaStreamSynchronize(st));
+  *out = m;
+  return MPK_OK;
+}
+
+void mpk_csr_free(mpk_matrix *m) {
+  if (!m) return;
+  cudaSetDevice(m->ctx->device);
+  cudaStreamSynchronize(m->ctx->stream);
+  DMat &A = m->A;
+  void *ptrs[] = {A.rp,     A.ci,     A.dp,      A.val,    A.lu,
+                  A.at_rp,  A.at_ci,  A.at_perm, A.at_val, A.ut_rp,
+                  A.ut_ci,  A.ut_perm, A.lt_rp,  A.lt_ci,  A.lt_perm,
+                  A.ut_val, A.lt_val, A.sw_y,    A.sw_y2,  A.tick,
+                  A.err,    m->rowflag, m->fscratch};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  delete m;
+}
+
+int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
+  DMat &A = m->A;
+  cudaStream_t st = m->ctx->stream;
+  CKR(cudaSetDevice(m->ctx->device));
+  // _structural_check ilu.py:172-175
+  for (int i = 0; i < A.n; ++i) {
+    if (A.h_dp[i] < 0) {
+      if (bad_row) *bad_row = i;
+      if (structural) *structural = 1;
+      return fail(MPK_SINGULAR_PIVOT,
+                  "ILU(0): structurally missing pivot U[" + std::to_string(i) +
+                      "," + std::to_string(i) + "]");
+    }
+  }
+  const size_t w = A.cx ? 2 : 1;
+  if (!A.lu) CKR(cudaMalloc(&A.lu, sizeof(double) * w * (A.nnz ? A.nnz : 1)));
+  CKR(cudaMemcpyAsync(A.lu, A.val, sizeof(double) * w * A.nnz,
+                      cudaMemcpyDeviceToDevice, st));
+  CKR(cudaMemsetAsync(m->rowflag, 0, sizeof(int) * (A.n + 1), st));
+  int init[4] = {0, 0, INT_MAX, 0};
+  CKR(cudaMemcpyAsync(m->fscratch, init, sizeof(init), cudaMemcpyHostToDevice,
+                      st));
+  FactorArgs fa{};
+  fa.n = A.n;
+  fa.rp = A.rp;
+  fa.ci = A.ci;
+  fa.dp = A.dp;
+  fa.lu = A.lu;
+  fa.rowflag = m->rowflag;
+  fa.tick = m->fscratch;
+  fa.bad_row = m->fscratch + 2;
+  fa.nonfinite = m->fscratch + 3;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  if (A.n > 0) launch_factor(fa, A.cx, st);
+  cudaEventRecord(e1, st);
+  int res[4];
+  CKR(cudaMemcpyAsync(res, m->fscratch, sizeof(res), cudaMemcpyDeviceToHost,
+                      st));
+  CKR(cudaStreamSynchronize(st));
+  CKR(cudaGetLastError());
+  cudaEventElapsedTime(&m->factor_ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  A.factored = false;
+  A.adj_ready = false;
+  if (res[2] != INT_MAX) {
+    if (bad_row) *bad_row = res[2];
+    if (structural) *structural = 0;
+    return fail(MPK_SINGULAR_PIVOT, "ILU(0): zero pivot U[" +
+                                        std::to_string(res[2]) + "," +
+                                        std::to_string(res[2]) + "]");
+  }
+  if (res[3]) return fail(MPK_NUMERIC_BREAKDOWN, "non-finite value in ILU(0) factors");
+  A.factored = true;
+  return MPK_OK;
+}
+
+int mpk_ilu0_download(mpk_matrix *m, double *lu_re, double *lu_im) {
+  DMat &A = m->A;
+  if (!A.factored) return fail(MPK_INVALID, "matrix is not factored");
+  CKR(cudaSetDevice(m->ctx->device));
+  const size_t w = A.cx ? 2 : 1;
+  std::vector<double> h(w * A.nnz);
+  CKR(cudaMemcpy(h.data(), A.lu, sizeof(double) * h.size(),
+                 cudaMemcpyDeviceToHost));
+  for (long long p = 0; p < A.nnz; ++p) {
+    if (A.cx) {
+      lu_re[p] = h[2 * p];
+      lu_im[p] = h[2 * p + 1];
+    } else {
+      lu_re[p] = h[p];
+    }
+  }
+  return MPK_OK;
+}
+
+// apply on a device planar-MC input; output F vector in `fz`
+static int apply_dev(mpk_matrix *m, int k, const double *in_mc, double *fz,
+                     int adjoint) {
+  DMat &A = m->A;
+  cudaStream_t st = m->ctx->stream;
+  if (adjoint) ensure_adjoint(A, st);
+  const long long L = plane_ld(A.n);
+  CKR(cudaMemsetAsync(A.err, 0, sizeof(int), st));
+  launch_sweep_reset(A.sw_y, fz, A.n, A.cx, nullptr, st);
+  SweepArgs a{};
+  a.n = A.n;
+  a.rp = A.rp;
+  a.ci = A.ci;
+  a.dp = A.dp;
+  a.lu = A.lu;
+  a.ut_rp = A.ut_rp;
+  a.ut_ci = A.ut_ci;
+  a.ut_val = A.ut_val;
+  a.lt_rp = A.lt_rp;
+  a.lt_ci = A.lt_ci;
+  a.lt_val = A.lt_val;
+  a.in_re = in_mc;
+  a.in_im = A.cx ? in_mc + (long long)k * L : nullptr;
+  a.y = A.sw_y;
+  a.z = fz;
+  a.tick = A.tick;
+  a.err = A.err;
+  a.done = nullptr;
+  if (A.n > 0) launch_sweep(a, A.cx, adjoint != 0, st);
+  int err = 0;
+  CKR(cudaMemcpyAsync(&err, A.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  CKR(cudaGetLastError());
+  if (err)
+    return fail(MPK_NUMERIC_BREAKDOWN, "non-finite value in triangular sweep");
+  return MPK_OK;
+}
+
+int mpk_ilu0_apply_f64(mpk_matrix *m, const double *r_re, const double *r_im,
+                       double *z_re, double *z_im, int adjoint) {
+  DMat &A = m->A;
+  if (!A.factored) return fail(MPK_INVALID, "matrix is not factored");
+  if (A.cx != (r_im != nullptr))
+    return fail(MPK_INVALID, "field mismatch: factors/vector");
+  CKR(cudaSetDevice(m->ctx->device));
+  cudaStream_t st = m->ctx->stream;
+  const long long L = plane_ld(A.n);
+  double *din = nullptr, *dz = nullptr, *hin = nullptr;
+  // binary64 input as a k=1 "MC" vector: planes re[, im]
+  CKR(cudaMalloc(&din, sizeof(double) * 2 * L));
+  CKR(cudaMalloc(&dz, sizeof(double) * 2 * L));
+  CKR(cudaMemcpyAsync(din, r_re, sizeof(double) * A.n, cudaMemcpyHostToDevice, st));
+  if (A.cx)
+    CKR(cudaMemcpyAsync(din + L, r_im, sizeof(double) * A.n,
+                        cudaMemcpyHostToDevice, st));
+  (void)hin;
+  // for a k=1 input the "demotion" of the complex value must be the
+  // identity (complex(re, im) in ilu.py:301): the device applies the numpy
+  // re + 1j*im rounding, which only normalises signed zeros.
+  int rc = apply_dev(m, 1, din, dz, adjoint);
+  if (rc == MPK_OK) {
+    if (A.cx) {
+      std::vector<double> h(2 * A.n);
+      CKR(cudaMemcpy(h.data(), dz, sizeof(double) * 2 * A.n, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < A.n; ++i) {
+        z_re[i] = h[2 * i];
+        z_im[i] = h[2 * i + 1];
+      }
+    } else {
+      CKR(cudaMemcpy(z_re, dz, sizeof(double) * A.n, cudaMemcpyDeviceToHost));
+    }
+  }
+  cudaFree(din);
+  cudaFree(dz);
+  return rc;
+}
+
+static int to_dev_planar(mpk_ctx *ctx, int64_t n, int k, const double *re,
+                         const double *im, double **dev) {
+  cudaStream_t st = ctx->stream;
+  const long long L = plane_ld(n);
+  const int planes = k * (im ? 2 : 1);
+  double *tmp = nullptr;
+  CKR(cudaMalloc(dev, sizeof(double) * planes * L + 16));
+  CKR(cudaMemsetAsync(*dev, 0, sizeof(double) * planes * L + 16, st));
+  if (n == 0) return MPK_OK;
+  CKR(cudaMalloc(&tmp, sizeof(double) * n * k * (im ? 2 : 1)));
+  CKR(cudaMemcpyAsync(tmp, re, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
+  if (im)
+    CKR(cudaMemcpyAsync(tmp + n * k, im, sizeof(double) * n * k,
+                        cudaMemcpyHostToDevice, st));
+  launch_to_planar(n, k, tmp, im ? tmp + n * k : nullptr, *dev, st);
+  CKR(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  return MPK_OK;
+}
+
+static int from_dev_planar(mpk_ctx *ctx, int64_t n, int k, const double *dev,
+                           double *re, double *im) {
+  cudaStream_t st = ctx->stream;
+  if (n == 0) return MPK_OK;
+  double *tmp = nullptr;
+  CKR(cudaMalloc(&tmp, sizeof(double) * n * k * (im ? 2 : 1)));
+  launch_from_planar(n, k, dev, tmp, im ? tmp + n * k : nullptr, st);
+  CKR(cudaMemcpyAsync(re, tmp, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
+  if (im)
+    CKR(cudaMemcpyAsync(im, tmp + n * k, sizeof(double) * n * k,
+                        cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  return MPK_OK;
+}
+
+int mpk_to_planar(mpk_ctx *ctx, int64_t n, int k, const double *re,
+                  const double *im, double *dev) {
+  CKR(cudaSetDevice(ctx->device));
+  double *d = nullptr;
+  int rc = to_dev_planar(ctx, n, k, re, im, &d);
+  if (rc) return rc;
+  const long long L = plane_ld(n);
+  CKR(cudaMemcpy(dev, d, sizeof(double) * k * (im ? 2 : 1) * L,
+                 cudaMemcpyDeviceToDevice));
+  cudaFree(d);
+  return MPK_OK;
+}
+
+int mpk_from_planar(mpk_ctx *ctx, int64_t n, int k, const double *dev,
+                    double *re, double *im, int cx) {
+  CKR(cudaSetDevice(ctx->device));
+  return from_dev_planar(ctx, n, k, dev, re, cx ? im : nullptr);
+}
+
+int mpk_ilu0_apply_mixed(mpk_matrix *m, int k, const double *r_re,
+                         const double *r_im, double *z_re, double *z_im,
+                         int adjoint) {
+  DMat &A = m->A;
+  if (!A.factored) return fail(MPK_INVALID, "matrix is not factored");
+  if (k < 2) return fail(MPK_INVALID, "mixed apply expects a working precision above binary64");
+  if (A.cx != (r_im != nullptr)) return fail(MPK_INVALID, "factors/vector mismatch");
+  CKR(cudaSetDevice(m->ctx->device));
+  double *din = nullptr, *dz = nullptr;
+  int rc = to_dev_planar(m->ctx, A.n, k, r_re, r_im, &din);
+  if (rc) return rc;
+  const long long L = plane_ld(A.n);
+  CKR(cudaMalloc(&dz, sizeof(double) * 2 * L));
+  rc = apply_dev(m, k, din, dz, adjoint);
+  if (rc == MPK_OK) {
+    // _promote_exact ilu.py:436-445 after numpy demotion of z (sparse.py:392)
+    const int w = A.cx ? 2 : 1;
+    std::vector<double> h(w * A.n);
+    CKR(cudaMemcpy(h.data(), dz, sizeof(double) * w * A.n, cudaMemcpyDeviceToHost));
+    std::memset(z_re, 0, sizeof(double) * A.n * k);
+    if (A.cx) std::memset(z_im, 0, sizeof(double) * A.n * k);
+    for (int i = 0; i < A.n; ++i) {
+      if (A.cx) {
+        const double re0 = h[2 * i], im0 = h[2 * i + 1];
+        z_re[(size_t)i * k] = mpk::dadd(re0, mpk::dsub(mpk::dmul(0.0, im0), 0.0));
+        z_im[(size_t)i * k] = mpk::dadd(0.0, im0);
+      } else {
+        z_re[(size_t)i * k] = h[i];
+      }
+    }
+  }
+  cudaFree(din);
+  cudaFree(dz);
+  return rc;
+}
+
+int mpk_spmv_mixed(mpk_matrix *m, int k, const double *x_re,
+                   const double *x_im, double *y_re, double *y_im,
+                   int adjoint) {
+  DMat &A = m->A;
+  if (k < 2) return fail(MPK_INVALID, "mixed SpMV requires a working precision above binary64");
+  if (A.cx != (x_im != nullptr))
+    return fail(MPK_INVALID, std::string("field mismatch: matrix ") +
+                                 (A.cx ? "complex" : "real") + ", vector " +
+                                 (x_im ? "complex" : "real"));
+  CKR(cudaSetDevice(m->ctx->device));
+  cudaStream_t st = m->ctx->stream;
+  double *dx = nullptr, *dy = nullptr;
+  int rc = to_dev_planar(m->ctx, A.n, k, x_re, x_im, &dx);
+  if (rc) return rc;
+  const long long L = plane_ld(A.n);
+  CKR(cudaMalloc(&dy, sizeof(double) * k * 2 * L + 16));
+  rc = unit_spmv(A, k, adjoint != 0, false, dx, dy, st);
+  if (rc) return fail(rc, "unsupported k");
+  CKR(cudaGetLastError());
+  rc = from_dev_planar(m->ctx, A.n, k, dy, y_re, A.cx ? y_im : nullptr);
+  cudaFree(dx);
+  cudaFree(dy);
+  return rc;
+}
+
+int mpk_hdot(mpk_ctx *ctx, int64_t n, int k, const double *x_re,
+             const double *x_im, const double *y_re, const double *y_im,
+             double *out_re, double *out_im) {
+  if (k < 2 || k > 4) return fail(MPK_INVALID, "k must be 2..4");
+  CKR(cudaSetDevice(ctx->device));
+  double *dx = nullptr, *dy = nullptr;
+  int rc = to_dev_planar(ctx, n, k, x_re, x_im, &dx);
+  if (rc) return rc;
+  rc = to_dev_planar(ctx, n, k, y_re, y_im, &dy);
+  if (rc) return rc;
+  double out[8];
+  rc = unit_reduce(k, x_im != nullptr, 0, n, dx, dy, out, ctx->stream);
+  for (int c = 0; c < k; ++c) {
+    out_re[c] = out[c];
+    if (out_im) out_im[c] = out[4 + c];
+  }
+  cudaFree(dx);
+  cudaFree(dy);
+  return rc ? fail(rc, "hdot failed") : MPK_OK;
+}
+
+int mpk_norm2(mpk_ctx *ctx, int64_t n, int k, const double *x_re,
+              const double *x_im, double *out) {
+  if (k < 2 || k > 4) return fail(MPK_INVALID, "k must be 2..4");
+  CKR(cudaSetDevice(ctx->device));
+  double *dx = nullptr;
+  int rc = to_dev_planar(ctx, n, k, x_re, x_im, &dx);
+  if (rc) return rc;
+  double o[8];
+  rc = unit_reduce(k, x_im != nullptr, 1, n, dx, dx, o, ctx->stream);
+  for (int c = 0; c < k; ++c) out[c] = o[c];
+  cudaFree(dx);
+  return rc ? fail(rc, "norm2 failed") : MPK_OK;
+}
+
+int mpk_axpy(mpk_ctx *ctx, int64_t n, int k, const double *alpha_re,
+             const double *alpha_im, const double *x_re, const double *x_im,
+             const double *y_re, const double *y_im, double *out_re,
+             double *out_im) {
+  if (k < 2 || k > 4) return fail(MPK_INVALID, "k must be 2..4");
+  CKR(cudaSetDevice(ctx->device));
+  double *dx = nullptr, *dy = nullptr, *dout = nullptr;
+  int rc = to_dev_planar(ctx, n, k, x_re, x_im, &dx);
+  if (rc) return rc;
+  rc = to_dev_planar(ctx, n, k, y_re, y_im, &dy);
+  if (rc) return rc;
+  const long long L = plane_ld(n);
+  CKR(cudaMalloc(&dout, sizeof(double) * k * 2 * L + 16));
+  rc = unit_axpy(k, x_im != nullptr, n, alpha_re, alpha_im, dx, dy, dout,
+                 ctx->stream);
+  if (rc) return fail(rc, "axpy failed");
+  rc = from_dev_planar(ctx, n, k, dout, out_re, x_im ? out_im : nullptr);
+  cudaFree(dx);
+  cudaFree(dy);
+  cudaFree(dout);
+  return rc;
+}
+
+int mpk_mc_elementwise(mpk_ctx *ctx, int op, int k, int64_t n,
+                       const double *a_re, const double *a_im,
+                       const double *b_re, const double *b_im, double *o_re,
+                       double *o_im) {
+  if (k < 2 || k > 4) return fail(MPK_INVALID, "k must be 2..4");
+  CKR(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int sa = (op == 7) ? 7 : k;
+  double *d[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  const double *src[4] = {a_re, a_im, b_re, b_im};
+  const size_t sz[4] = {(size_t)sa, (size_t)k, (size_t)k, (size_t)k};
+  for (int q = 0; q < 4; ++q) {
+    if (!src[q]) continue;
+    CKR(cudaMalloc(&d[q], sizeof(double) * n * sz[q] + 8));
+    CKR(cudaMemcpyAsync(d[q], src[q], sizeof(double) * n * sz[q],
+                        cudaMemcpyHostToDevice, st));
+  }
+  CKR(cudaMalloc(&d[4], sizeof(double) * n * k + 8));
+  if (o_im) CKR(cudaMalloc(&d[5], sizeof(double) * n * k + 8));
+  int rc = unit_mc(op, k, d[0], d[1], d[2], d[3], d[4], d[5], (int)n, st);
+  if (rc) return fail(rc, "bad op");
+  CKR(cudaGetLastError());
+  CKR(cudaMemcpyAsync(o_re, d[4], sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
+  if (o_im)
+    CKR(cudaMemcpyAsync(o_im, d[5], sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  for (int q = 0; q < 6; ++q)
+    if (d[q]) cudaFree(d[q]);
+  return MPK_OK;
+}
+
+int mpk_mc_host(int op, int k, const double *a_re, const double *a_im,
+                const double *b_re, const double *b_im, double *o_re,
+                double *o_im) {
+  int rc = host_mc(op, k, a_re, a_im, b_re, b_im, o_re, o_im);
+  return rc ? fail(rc, "unsupported op/k") : MPK_OK;
+}
+
+static void fill_report(mpk_report *rep, const SolveOut &o, float factor_ms) {
+  rep->iterations = o.iterations;
+  rep->converged = o.converged;
+  rep->breakdown = o.breakdown;
+  rep->has_x = o.breakdown != kBdNumericSweep;
+  rep->final_recursive_relres = o.relres;
+  rep->true_relres = o.true_relres;
+  rep->hist_len = o.hist_len;
+  rep->factor_ms = factor_ms;
+  rep->solve_ms = o.loop_ms;
+}
+
+static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
+                      double eps_abs, int64_t max_iter, const double *d_b,
+                      double *d_x, double *d_hist, int64_t hist_cap,
+                      mpk_report *rep) {
+  std::memset(rep, 0, sizeof(*rep));
+  rep->final_recursive_relres = NAN;
+  rep->true_relres = NAN;
+  if (method < 0 || method > 3) return fail(MPK_INVALID, "unknown method");
+  if (k < 2 || k > 4)
+    return fail(MPK_INVALID, "mixed SpMV needs a working precision above binary64");
+  if (!(eps_rel > 0) || !(eps_abs > 0))
+    return fail(MPK_INVALID, "eps_rel and eps_abs must be positive");
+  // build_preconditioner (ilu.py:514-522) inside the timed solve, as the
+  // reference's total_seconds includes the factorization (solvers.py:426)
+  int64_t bad = -1;
+  int32_t structural = 0;
+  int rc = mpk_ilu0_factor(m, &bad, &structural);
+  if (rc == MPK_SINGULAR_PIVOT || rc == MPK_NUMERIC_BREAKDOWN) {
+    rep->iterations = 0;
+    rep->converged = 0;
+    rep->breakdown = rc == MPK_SINGULAR_PIVOT ? MPK_BD_SINGULAR_PIVOT
+                                              : MPK_BD_NUMERIC_FACTOR;
+    rep->bad_row = bad;
+    rep->structural = structural;
+    rep->has_x = 0;
+    rep->factor_ms = m->factor_ms;
+    return MPK_OK;
+  }
+  if (rc) return rc;
+  SolveParams p{};
+  p.method = method;
+  p.k = k;
+  p.eps_rel = eps_rel;
+  p.eps_abs = eps_abs;
+  p.max_iter = max_iter < 0 ? 3LL * m->A.n : max_iter;
+  p.precond_ilu = 1;
+  p.hist_cap = hist_cap;
+  SolveOut o{};
+  char eb[256] = {0};
+  rc = run_solve(m->A, p, d_b, d_x, d_hist, &o, m->ctx->stream, eb);
+  if (rc) return fail(rc, eb);
+  fill_report(rep, o, m->factor_ms);
+  return MPK_OK;
+}
+
+int mpk_solve_dev(mpk_matrix *m, int method, int k, double eps_rel,
+                  double eps_abs, int64_t max_iter, const double *b_dev,
+                  double *x_dev, double *hist_dev, int64_t hist_cap,
+                  mpk_report *rep) {
+  const auto t0 = std::chrono::steady_clock::now();
+  CKR(cudaSetDevice(m->ctx->device));
+  int rc = solve_core(m, method, k, eps_rel, eps_abs, max_iter, b_dev, x_dev,
+                      hist_dev, hist_cap, rep);
+  rep->total_ms = std::chrono::duration<double, std::milli>(
+                      std::chrono::steady_clock::now() - t0)
+                      .count();
+  return rc;
+}
+
+int mpk_solve(mpk_matrix *m, int method, int k, double eps_rel,
+              double eps_abs, int64_t max_iter, const double *b_re,
+              const double *b_im, double *x_re, double *x_im, double *hist,
+              int64_t hist_cap, mpk_report *rep) {
+  const auto t0 = std::chrono::steady_clock::now();
+  DMat &A = m->A;
+  if (A.cx != (b_im != nullptr))
+    return fail(MPK_INVALID, "matrix/vector field mismatch");
+  CKR(cudaSetDevice(m->ctx->device));
+  cudaStream_t st = m->ctx->stream;
+  double *db = nullptr, *dx = nullptr, *dh = nullptr;
+  int rc = to_dev_planar(m->ctx, A.n, k, b_re, b_im, &db);
+  if (rc) return rc;
+  const long long L = plane_ld(A.n);
+  CKR(cudaMalloc(&dx, sizeof(double) * k * (A.cx ? 2 : 1) * L + 16));
+  CKR(cudaMemsetAsync(dx, 0, sizeof(double) * k * (A.cx ? 2 : 1) * L + 16, st));
+  const int64_t hc = hist && hist_cap > 0 ? hist_cap : 0;
+  CKR(cudaMalloc(&dh, sizeof(double) * k * (hc ? hc : 1)));
+  rc = solve_core(m, method, k, eps_rel, eps_abs, max_iter, db, dx, dh, hc, rep);
+  if (rc == MPK_OK && rep->has_x)
+    rc = from_dev_planar(m->ctx, A.n, k, dx, x_re, A.cx ? x_im : nullptr);
+  if (rc == MPK_OK && hc) {
+    const int64_t cnt = rep->hist_len < hc ? rep->hist_len : hc;
+    if (cnt > 0)
+      CKR(cudaMemcpy(hist, dh, sizeof(double) * k * cnt, cudaMemcpyDeviceToHost));
+  }
+  cudaFree(db);
+  cudaFree(dx);
+  cudaFree(dh);
+  rep->total_ms = std::chrono::duration<double, std::milli>(
+                      std::chrono::steady_clock::now() - t0)
+                      .count();
+  return rc;
+}
+
+int mpk_solve_batch(int nsys, mpk_matrix **ms, int method, int k,
+                    double eps_rel, double eps_abs, int64_t max_iter,
+                    const double *const *b_re, double *const *x_re,
+                    mpk_report *reps) {
+  if (nsys <= 0) return MPK_OK;
+  // one host thread + stream per lane; systems dealt round-robin
+  const int lanes = nsys < 8 ? nsys : 8;
+  std::vector<int> rcs(lanes, 0);
+  std::vector<std::string> errs(lanes);
+  std::vector<std::thread> th;
+  for (int l = 0; l < lanes; ++l) {
+    th.emplace_back([&, l]() {
+      for (int s = l; s < nsys; s += lanes) {
+        int rc = mpk_solve(ms[s], method, k, eps_rel, eps_abs, max_iter,
+                           b_re[s], nullptr, x_re[s], nullptr, nullptr, 0,
+                           &reps[s]);
+        if (rc) {
+          rcs[l] = rc;
+          errs[l] = g_err;
+        }
+      }
+    });
+  }
+  for (auto &t : th) t.join();
+  for (int l = 0; l < lanes; ++l)
+    if (rcs[l]) return fail(rcs[l], errs[l]);
+  return MPK_OK;
+}
+
+}  // extern "C"

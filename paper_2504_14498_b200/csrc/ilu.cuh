@@ -1,0 +1,56 @@
+// ilu.cuh -- binary64 ILU(0) factorization and triangular sweeps on sm_100a.
+//
+// Reference: ilu.py:178-276 (_factorize_tuples, k=1), :322-343 (sweeps),
+// :346-371 (adjoint sweeps), :448-470 (mixed apply = promote . f64 . demote).
+//
+// Bit-exactness: each row is processed by ONE thread in exactly the
+// reference's per-row order (ascending L columns; ascending U columns;
+// final division), with explicit _rn intrinsics (no FMA contraction).
+// Parallelism comes from the DAG: rows are claimed in dependency-compatible
+// order through an atomic ticket (forward rows ascending, backward rows
+// descending), and a row waits only on rows with smaller tickets, which are
+// held by resident warps -> deadlock-free without a level barrier
+// ("sync-free" scheduling; critical path = level depth).
+// Readiness is signalled by the value itself: outputs are pre-filled with a
+// signalling-NaN sentinel and read with L1-bypassing volatile loads.
+#pragma once
+
+#include "common.cuh"
+
+namespace mpk {
+
+struct SweepArgs {
+  int n;
+  const int *rp, *ci, *dp;
+  const double *lu;  // real: [nnz]; complex: double2 [nnz]
+  // adjoint gather structures (BiCG): U^T rows ascending, L^T descending
+  const int *ut_rp, *ut_ci;
+  const double *ut_val;  // real [nnzU] / complex double2
+  const int *lt_rp, *lt_ci;
+  const double *lt_val;
+  // input: head plane(s) of an MC vector (complex: re plane, im plane)
+  const double *in_re, *in_im;
+  // scratch y (sentinel-filled) and output z (F vector, sentinel-filled)
+  double *y, *z;
+  int *tick;       // [0] ticket, [1] exit counter
+  int *err;        // set to 1 on a non-finite z (NumericBreakdownError)
+  const int *done; // solver done flag (skip when set), may be null
+};
+
+void launch_sweep(const SweepArgs &a, bool cx, bool adjoint,
+                  cudaStream_t st);
+void launch_sweep_reset(double *y, double *z, int n, bool cx,
+                        const int *done, cudaStream_t st);
+
+struct FactorArgs {
+  int n;
+  const int *rp, *ci, *dp;
+  double *lu;      // in: A values, out: factors (in place)
+  int *rowflag;    // per-row completion flags (zeroed)
+  int *tick;       // [0] ticket, [1] exit counter
+  int *bad_row;    // atomicMin of zero-pivot rows (init INT_MAX)
+  int *nonfinite;  // set if any factor is non-finite
+};
+void launch_factor(const FactorArgs &a, bool cx, cudaStream_t st);
+
+}  // namespace mpk

@@ -1,0 +1,101 @@
+// krylov.cuh -- device-side solver state and host-side solver object.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+#include "ilu.cuh"
+
+namespace mpk {
+
+enum Method { kBiCG = 0, kCGS = 1, kBiCGSTAB = 2, kGPBiCG = 3 };
+
+enum Breakdown {
+  kBdNone = 0,
+  kBdSigmaZero = 1,
+  kBdRhoZero = 2,
+  kBdOmegaZero = 3,
+  kBdNonfinite = 4,
+  kBdLs = 5,
+  kBdZetaZero = 6,
+  kBdSingularPivot = 7,
+  kBdNumericFactor = 8,
+  kBdNumericSweep = 9
+};
+
+// All MC scalars of the four methods live here, on the device; the host
+// never sees them during the iteration (no per-iteration sync).
+struct State {
+  Sc rho, rho_old, alpha, omega, beta, sigma, nrm, nrm0, thr, zeta, eta;
+  long long it, max_iter, iterations, hist_len, hist_cap;
+  int done, converged, breakdown, half_exit, have_nrm, sweep_err;
+  double eps_rel, eps_abs;
+  double relres, true_relres;
+};
+
+// Device matrix: binary64 CSR (int32 indices) + ILU(0) factors + the
+// transposed gather structures used by the adjoint paths (BiCG).
+struct DMat {
+  int n;
+  long long nnz;
+  bool cx;
+  int *rp = nullptr, *ci = nullptr, *dp = nullptr;
+  double *val = nullptr;  // real [nnz] or double2 [nnz]
+  double *lu = nullptr;   // factors, same layout
+  bool factored = false;
+  // A^T gather (ascending source row) for spmv_adjoint
+  int *at_rp = nullptr, *at_ci = nullptr, *at_perm = nullptr;
+  double *at_val = nullptr;
+  // U^T (ascending rows) and L^T (descending rows) for the adjoint sweeps
+  int *ut_rp = nullptr, *ut_ci = nullptr, *ut_perm = nullptr;
+  int *lt_rp = nullptr, *lt_ci = nullptr, *lt_perm = nullptr;
+  double *ut_val = nullptr, *lt_val = nullptr;
+  bool adj_ready = false;
+  long long h_adj_sizes[2] = {0, 0};
+  // sweep scratch
+  double *sw_y = nullptr, *sw_y2 = nullptr;
+  int *tick = nullptr;  // 4 ints: [0..1] sweep A, [2..3] sweep B
+  int *err = nullptr;
+  // host copies of the pattern (for building transposes)
+  std::vector<int> h_rp, h_ci, h_dp;
+};
+
+struct SolveParams {
+  int method, k;
+  double eps_rel, eps_abs;
+  long long max_iter;
+  int precond_ilu;  // 1: ILU(0)-mixed, 0: identity
+  long long hist_cap;
+};
+
+struct SolveOut {
+  long long iterations;
+  int converged, breakdown, half_exit;
+  double relres, true_relres;
+  long long hist_len;
+  float factor_ms, loop_ms;
+};
+
+// Solve with the right-hand side already on the device (planar MC layout,
+// K [x2] planes of ld doubles).  x_out: planar MC, hist_out: device
+// [hist_cap * k] doubles.  Factorization must have been done (if ILU).
+int run_solve(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
+              double *d_hist, SolveOut *out, cudaStream_t st, char *errbuf);
+
+// unit kernels used by the C-ABI (parity tests)
+int unit_spmv(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
+              double *d_y, cudaStream_t st);
+int unit_reduce(int k, bool cx, int op, long long n, const double *d_x,
+                const double *d_y, double *h_out, cudaStream_t st);
+int unit_axpy(int k, bool cx, long long n, const double *alpha_re,
+              const double *alpha_im, const double *d_x, const double *d_y,
+              double *d_out, cudaStream_t st);
+int unit_mc(int op, int k, const double *a_re, const double *a_im,
+            const double *b_re, const double *b_im, double *o_re,
+            double *o_im, int n, cudaStream_t st);
+
+void ensure_adjoint(DMat &A, cudaStream_t st);
+
+inline long long plane_ld(long long n) { return (n + 31) / 32 * 32; }
+
+}  // namespace mpk

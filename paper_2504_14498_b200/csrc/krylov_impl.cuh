@@ -1,0 +1,1112 @@
+// krylov.cu -- BiCG / CGS / BiCGSTAB / GPBiCG with binary64 ILU(0)-mixed
+// preconditioning, entirely on the device.
+//
+// Reference: /root/reference/pkg/src/mpkrylov/solvers.py:183-412.  Every
+// vector operation of the reference method bodies is executed with the
+// same MC operation sequence per element (mc.cuh twins); consecutive
+// element-wise operations are fused into one pass over HBM ("row
+// kernels"), and each reduction is produced as block partials by the
+// kernel that produces its operands, then folded by a one-block
+// "finalize" kernel that also runs the scalar recurrence (alpha, beta,
+// omega, zeta, eta; MC division on the device) and the stopping test.
+// One iteration is captured once into a CUDA graph and replayed by a
+// device-side WHILE conditional node: the host never synchronises inside
+// the solve.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "krylov.cuh"
+#include "rows.cuh"
+
+namespace mpk {
+
+// ---------------------------------------------------------------------
+// scalar helpers run by thread 0 of a finalize kernel
+// ---------------------------------------------------------------------
+__device__ __forceinline__ void finish_state(State *S, long long it, int conv,
+                                             int bd) {
+  S->iterations = it;
+  S->converged = conv;
+  S->breakdown = bd;
+  S->done = 1;
+}
+
+template <int K>
+__device__ __forceinline__ void record(State *S, double *hist, const Sc &v) {
+  if (S->hist_len < S->hist_cap) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) hist[S->hist_len * K + c] = v.re[c];
+  }
+  S->hist_len++;
+}
+
+template <int K>
+__device__ __forceinline__ Sc sqrt_sc(const Sc &ss) {
+  Sc o = sc_zero();
+  sqrt_mc<K>(R<K>(ss), R<K>(o));
+  return o;
+}
+
+template <int K>
+__device__ __forceinline__ bool lt(const Sc &a, const Sc &b) {
+  return cmp<K>(R<K>(a), R<K>(b)) < 0;
+}
+
+// _Ctx.threshold solvers.py:146-149 and the r0 test; returns true if done
+template <int K>
+__device__ __forceinline__ bool setup_norm0(State *S, double *hist,
+                                            const Sc &ss) {
+  const Sc nrm0 = sqrt_sc<K>(ss);
+  S->nrm0 = nrm0;
+  S->nrm = nrm0;
+  record<K>(S, hist, nrm0);
+  Sc er = sc_zero(), ea = sc_zero(), t = sc_zero();
+  er.re[0] = S->eps_rel;
+  ea.re[0] = S->eps_abs;
+  mul<K>(R<K>(er), R<K>(nrm0), R<K>(t));
+  Sc thr = sc_zero();
+  add<K>(R<K>(t), R<K>(ea), R<K>(thr));
+  S->thr = thr;
+  S->it = 1;
+  if (lt<K>(nrm0, thr)) {
+    S->have_nrm = 1;
+    finish_state(S, 0, 1, kBdNone);
+    return true;
+  }
+  if (S->max_iter < 1) {
+    finish_state(S, S->max_iter < 0 ? 0 : S->max_iter, 0, kBdNone);
+    return true;
+  }
+  return false;
+}
+
+// residual norm bookkeeping after norm2(r) / norm2(s); true if done
+template <int K>
+__device__ __forceinline__ bool check_nrm(State *S, double *hist,
+                                          const Sc &ss) {
+  const Sc nrm = sqrt_sc<K>(ss);
+  S->nrm = nrm;
+  S->have_nrm = 1;
+  record<K>(S, hist, nrm);
+  if (!is_finite<K>(R<K>(nrm))) {
+    finish_state(S, S->it, 0, kBdNonfinite);
+    return true;
+  }
+  if (lt<K>(nrm, S->thr)) {
+    finish_state(S, S->it, 1, kBdNone);
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void next_iter(State *S) {
+  S->it++;
+  if (S->it > S->max_iter) finish_state(S, S->max_iter, 0, kBdNone);
+}
+
+static __global__ void set_cond_kernel(cudaGraphConditionalHandle h,
+                                       const State *S) {
+  cudaGraphSetConditional(h, S->done ? 0u : 1u);
+}
+
+// report tail: final_recursive_relres = (nrm / nrm0).to_float()
+template <int K>
+__global__ void relres_kernel(State *S) {
+  S->relres = NAN;
+  if (S->have_nrm && !is_zero<K>(R<K>(S->nrm0))) {
+    double q[K];
+    div<K>(R<K>(S->nrm), R<K>(S->nrm0), q);
+    S->relres = q[0];
+  }
+}
+
+template <int K, bool CX>
+__global__ void true_res_kernel_impl(State *S_, const double *pt_, int G_) {
+  __shared__ double sm[kWarpsPerBlock * 8];
+  const Sc rr = finalize_slot<K, false>(pt_, 0, G_, sm);
+  const Sc bb = finalize_slot<K, false>(pt_, 1, G_, sm);
+  if (threadIdx.x == 0) {
+    S_->true_relres = NAN;
+    const Sc nb = sqrt_sc<K>(bb);
+    if (!is_zero<K>(R<K>(nb))) {
+      const Sc nr = sqrt_sc<K>(rr);
+      double q[K];
+      div<K>(R<K>(nr), R<K>(nb), q);
+      S_->true_relres = q[0];
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------
+// solver object
+// ---------------------------------------------------------------------
+template <int K, bool CX>
+struct Solver {
+  using MVt = MV<K, CX>;
+  using FVt = FV<CX>;
+  DMat &A;
+  DA da;
+  SolveParams p;
+  cudaStream_t st;
+  int n;
+  long long ld;
+  int G;
+  State *S = nullptr;
+  double *part = nullptr;
+  double *hist = nullptr;
+  const int *done = nullptr;
+  int *err = nullptr;
+  std::vector<void *> allocs;
+  bool ok = true;
+  char *errbuf;
+
+  Solver(DMat &A_, const SolveParams &p_, cudaStream_t st_, double *hist_,
+         char *eb)
+      : A(A_), p(p_), st(st_), hist(hist_), errbuf(eb) {
+    n = A.n;
+    ld = plane_ld(n);
+    G = grid_for(n);
+    da = DA{A.n, A.rp, A.ci, A.val, A.at_rp, A.at_ci, A.at_val};
+    S = (State *)dalloc(sizeof(State));
+    part = (double *)dalloc(sizeof(double) * 6 * kMaxGrid * 8);
+    done = &S->done;
+    err = A.err;
+  }
+  ~Solver() {
+    for (void *q : allocs) cudaFree(q);
+  }
+  void *dalloc(size_t bytes) {
+    void *q = nullptr;
+    if (cudaMalloc(&q, bytes < 16 ? 16 : bytes) != cudaSuccess) {
+      ok = false;
+      snprintf(errbuf, 256, "cudaMalloc(%zu) failed", bytes);
+      return nullptr;
+    }
+    cudaMemsetAsync(q, 0, bytes < 16 ? 16 : bytes, st);
+    allocs.push_back(q);
+    return q;
+  }
+  double *mc() { return (double *)dalloc(sizeof(double) * K * (CX ? 2 : 1) * ld); }
+  double *fv() { return (double *)dalloc(sizeof(double) * (CX ? 2 : 1) * ld); }
+  MVt mv(double *q) const { return MVt{q, ld}; }
+  FVt fvv(double *q) const { return FVt{q}; }
+
+  // ILU(0)-mixed apply: z = promote(U^-1 L^-1 demote(in)).
+  void sweep(const double *in_re, const double *in_im, double *y, double *z,
+             bool adjoint, int which) {
+    SweepArgs a{};
+    a.n = n;
+    a.rp = A.rp;
+    a.ci = A.ci;
+    a.dp = A.dp;
+    a.lu = A.lu;
+    a.ut_rp = A.ut_rp;
+    a.ut_ci = A.ut_ci;
+    a.ut_val = A.ut_val;
+    a.lt_rp = A.lt_rp;
+    a.lt_ci = A.lt_ci;
+    a.lt_val = A.lt_val;
+    a.in_re = in_re;
+    a.in_im = in_im;
+    a.y = y;
+    a.z = z;
+    a.tick = A.tick + 2 * which;
+    a.err = A.err;
+    a.done = done;
+    launch_sweep(a, CX, adjoint, st);
+  }
+  const double *head_re(const double *v) const { return v; }
+  const double *head_im(const double *v) const { return CX ? v + K * ld : nullptr; }
+
+  // ---------------- BiCGSTAB (solvers.py:275-328) ----------------
+  double *b, *x, *r, *rt0, *pp, *v, *s, *t, *phat, *shat, *fzero;
+  double *u, *q, *w, *uhat, *whead;                 // CGS
+  double *Bp, *Bt, *yv, *tpr, *zz, *yhat, *Mp, *Mt; // GPBiCG
+  double *rt, *pt, *qv, *qt, *zf, *ztf;             // BiCG
+
+  void alloc_common(const double *d_b) {
+    b = const_cast<double *>(d_b);
+    fzero = fv();
+  }
+
+  // r = b - A*0 (the reference forms matvec(zeros), solvers.py:189 etc.),
+  // plus partial norm2(r) [slot NH] and hdot(r, r) as rho [slot 0].
+  void setup_residual(double *r_, double *r2_, bool with_rho) {
+    const MVt B = mv(b), Rv = mv(r_), R2 = mv(r2_ ? r2_ : r_);
+    const DA a = da;
+    const double *fz = fzero;
+    const long long L = ld;
+    const bool two = r2_ != nullptr;
+    rows<K, CX, 1, 1>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 1> &red) {
+                        double axr[K], axi[K], br[K], bi[K], rr[K], ri[K];
+                        spmv_row<K, CX, true, false>(a, (int)i, fz, L, axr, axi);
+                        B.load(i, br, bi);
+                        e_sub<K, CX>(br, bi, axr, axi, rr, ri);
+                        Rv.store(i, rr, ri);
+                        if (two) R2.store(i, rr, ri);
+                        if (with_rho) acc_hdot<K, CX>(red.h[0], rr, ri, rr, ri);
+                        acc_sumsq<K, CX>(red.nr[0], rr, ri);
+                      });
+    double *H = hist;
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc rho = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          const Sc ss = finalize_slot<K, false>(pt_, 1, G_, sm);
+          if (threadIdx.x == 0) {
+            S_->rho = rho;
+            setup_norm0<K>(S_, H, ss);
+          }
+        });
+  }
+
+  void bicgstab_setup() {
+    x = mc(); r = mc(); rt0 = mc(); pp = mc(); v = mc(); s = mc(); t = mc();
+    phat = fv(); shat = fv();
+    setup_residual(r, rt0, true);
+  }
+
+  void bicgstab_iter() {
+    const MVt X = mv(x), Rr = mv(r), RT = mv(rt0), P = mv(pp), V = mv(v),
+              Sv = mv(s), T = mv(t);
+    const FVt PH = fvv(phat), SH = fvv(shat), Y = fvv(A.sw_y);
+    State *Sd = S;
+    double *H = hist;
+    const DA a = da;
+    const long long L = ld;
+    // F1: rho, omega check, beta
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc rho = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) {
+            S_->rho = rho;
+            if (s_is_zero<K, CX>(rho)) {
+              finish_state(S_, S_->it, 0, kBdRhoZero);
+              return;
+            }
+            if (S_->it > 1) {
+              if (s_is_zero<K, CX>(S_->omega)) {
+                finish_state(S_, S_->it, 0, kBdOmegaZero);
+                return;
+              }
+              S_->beta = s_mul<K, CX>(s_div<K, CX>(rho, S_->rho_old),
+                                      s_div<K, CX>(S_->alpha, S_->omega));
+            }
+          }
+        });
+    // K2: p = r (it 1) | p = r + beta*(p - omega*v); reset sweep buffers
+    rows<K, CX, 0, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double rr[K], ri[K];
+                        Rr.load(i, rr, ri);
+                        if (Sd->it == 1) {
+                          P.store(i, rr, ri);
+                        } else {
+                          double pr[K], pi[K], vr[K], vi[K], tr[K], ti[K];
+                          P.load(i, pr, pi);
+                          V.load(i, vr, vi);
+                          const Sc mo = s_neg<K>(Sd->omega);
+                          e_axpy<K, CX>(mo, vr, vi, pr, pi, tr, ti);
+                          e_axpy<K, CX>(Sd->beta, tr, ti, rr, ri, pr, pi);
+                          P.store(i, pr, pi);
+                        }
+                        Y.set_sent(i);
+                        PH.set_sent(i);
+                      });
+    sweep(head_re(pp), head_im(pp), A.sw_y, phat, false, 0);
+    // K4: v = A phat ; sigma = hdot(rt0, v)
+    const double *phc = phat;
+    rows<K, CX, 1, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
+                        double vr[K], vi[K], rr[K], ri[K];
+                        spmv_row<K, CX, true, false>(a, (int)i, phc, L, vr, vi);
+                        V.store(i, vr, vi);
+                        RT.load(i, rr, ri);
+                        acc_hdot<K, CX>(red.h[0], rr, ri, vr, vi);
+                      });
+    // F2: alpha
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc sg = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) {
+            if (s_is_zero<K, CX>(sg)) {
+              finish_state(S_, S_->it, 0, kBdSigmaZero);
+              return;
+            }
+            S_->alpha = s_div<K, CX>(S_->rho, sg);
+          }
+        });
+    // K5: s = r - alpha v ; norm2(s)
+    rows<K, CX, 0, 1>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 1> &red) {
+                        double rr[K], ri[K], vr[K], vi[K], sr[K], si[K];
+                        Rr.load(i, rr, ri);
+                        V.load(i, vr, vi);
+                        const Sc ma = s_neg<K>(Sd->alpha);
+                        e_axpy<K, CX>(ma, vr, vi, rr, ri, sr, si);
+                        Sv.store(i, sr, si);
+                        acc_sumsq<K, CX>(red.nr[0], sr, si);
+                        Y.set_sent(i);
+                        SH.set_sent(i);
+                      });
+    // F3: half-step test
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc ss = finalize_slot<K, false>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) {
+            if (check_nrm<K>(S_, H, ss) && S_->converged) S_->half_exit = 1;
+          }
+        });
+    sweep(head_re(s), head_im(s), A.sw_y, shat, false, 0);
+    // K7: t = A shat ; tt = hdot(t,t), ts = hdot(t,s)
+    const double *shc = shat;
+    rows<K, CX, 2, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 2, 0> &red) {
+                        double tr[K], ti[K], sr[K], si[K];
+                        spmv_row<K, CX, true, false>(a, (int)i, shc, L, tr, ti);
+                        T.store(i, tr, ti);
+                        Sv.load(i, sr, si);
+                        acc_hdot<K, CX>(red.h[0], tr, ti, tr, ti);
+                        acc_hdot<K, CX>(red.h[1], tr, ti, sr, si);
+                      });
+    // F4: omega
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc tt = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          const Sc ts = finalize_slot<K, CX>(pt_, 1, G_, sm);
+          if (threadIdx.x == 0) {
+            if (s_is_zero<K, CX>(tt)) {
+              finish_state(S_, S_->it, 0, kBdOmegaZero);
+              return;
+            }
+            S_->omega = s_div<K, CX>(ts, tt);
+          }
+        });
+    // K8: x = (x + alpha phat) + omega shat ; r = s - omega t ;
+    //     norm2(r) [slot 1], next rho = hdot(rt0, r) [slot 0]
+    rows<K, CX, 1, 1>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 1> &red) {
+                        double xr[K], xi[K], fr[K], fi[K], tr[K], ti[K];
+                        X.load(i, xr, xi);
+                        PH.template load_mc<K>(i, fr, fi);
+                        e_axpy<K, CX>(Sd->alpha, fr, fi, xr, xi, tr, ti);
+                        SH.template load_mc<K>(i, fr, fi);
+                        e_axpy<K, CX>(Sd->omega, fr, fi, tr, ti, xr, xi);
+                        X.store(i, xr, xi);
+                        double sr[K], si[K], rr[K], ri[K], qr[K], qi[K];
+                        Sv.load(i, sr, si);
+                        T.load(i, tr, ti);
+                        const Sc mo = s_neg<K>(Sd->omega);
+                        e_axpy<K, CX>(mo, tr, ti, sr, si, rr, ri);
+                        Rr.store(i, rr, ri);
+                        RT.load(i, qr, qi);
+                        acc_hdot<K, CX>(red.h[0], qr, qi, rr, ri);
+                        acc_sumsq<K, CX>(red.nr[0], rr, ri);
+                      });
+    // F5
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc ss = finalize_slot<K, false>(pt_, 1, G_, sm);
+          if (threadIdx.x == 0) {
+            S_->rho_old = S_->rho;
+            if (check_nrm<K>(S_, H, ss)) return;
+            next_iter(S_);
+          }
+        });
+  }
+
+  void bicgstab_finish(const State &hs) {
+    if (hs.half_exit) {
+      const MVt X = mv(x);
+      const FVt PH = fvv(phat);
+      State *Sd = S;
+      rows<K, CX, 0, 0>(n, nullptr, part, st,
+                        [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                          double xr[K], xi[K], fr[K], fi[K], tr[K], ti[K];
+                          X.load(i, xr, xi);
+                          PH.template load_mc<K>(i, fr, fi);
+                          e_axpy<K, CX>(Sd->alpha, fr, fi, xr, xi, tr, ti);
+                          X.store(i, tr, ti);
+                        });
+    }
+  }
+
+  // ---------------- CGS (solvers.py:229-272) ----------------
+  void cgs_setup() {
+    x = mc(); r = mc(); rt0 = mc(); u = mc(); pp = mc(); q = mc(); v = mc();
+    phat = fv(); uhat = fv();
+    whead = (double *)dalloc(sizeof(double) * 2 * ld);
+    setup_residual(r, rt0, true);
+  }
+
+  void cgs_iter() {
+    const MVt X = mv(x), Rr = mv(r), RT = mv(rt0), U = mv(u), P = mv(pp),
+              Q = mv(q), V = mv(v);
+    const FVt PH = fvv(phat), UH = fvv(uhat), Y = fvv(A.sw_y);
+    State *Sd = S;
+    double *H = hist;
+    const DA a = da;
+    const long long L = ld;
+    double *WH = whead;
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc rho = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) {
+            S_->rho = rho;
+            if (s_is_zero<K, CX>(rho)) {
+              finish_state(S_, S_->it, 0, kBdRhoZero);
+              return;
+            }
+            if (S_->it > 1) S_->beta = s_div<K, CX>(rho, S_->rho_old);
+          }
+        });
+    // u = r + beta q ; p = u + beta (q + beta p)
+    rows<K, CX, 0, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double rr[K], ri[K];
+                        Rr.load(i, rr, ri);
+                        if (Sd->it == 1) {
+                          U.store(i, rr, ri);
+                          P.store(i, rr, ri);
+                        } else {
+                          double qr[K], qi[K], ur[K], ui[K], pr[K], pi[K],
+                              tr[K], ti[K];
+                          Q.load(i, qr, qi);
+                          P.load(i, pr, pi);
+                          const Sc be = Sd->beta;
+                          e_axpy<K, CX>(be, qr, qi, rr, ri, ur, ui);
+                          e_axpy<K, CX>(be, pr, pi, qr, qi, tr, ti);
+                          e_axpy<K, CX>(be, tr, ti, ur, ui, pr, pi);
+                          U.store(i, ur, ui);
+                          P.store(i, pr, pi);
+                        }
+                        Y.set_sent(i);
+                        PH.set_sent(i);
+                      });
+    sweep(head_re(pp), head_im(pp), A.sw_y, phat, false, 0);
+    const double *phc = phat;
+    rows<K, CX, 1, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
+                        double vr[K], vi[K], rr[K], ri[K];
+                        spmv_row<K, CX, true, false>(a, (int)i, phc, L, vr, vi);
+                        V.store(i, vr, vi);
+                        RT.load(i, rr, ri);
+                        acc_hdot<K, CX>(red.h[0], rr, ri, vr, vi);
+                      });
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc sg = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) {
+            if (s_is_zero<K, CX>(sg)) {
+              finish_state(S_, S_->it, 0, kBdSigmaZero);
+              return;
+            }
+            S_->alpha = s_div<K, CX>(S_->rho, sg);
+          }
+        });
+    // q = u - alpha v ; head(u + q) -> sweep input
+    rows<K, CX, 0, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double ur[K], ui[K], vr[K], vi[K], qr[K], qi[K],
+                            wr[K], wi[K];
+                        U.load(i, ur, ui);
+                        V.load(i, vr, vi);
+                        const Sc ma = s_neg<K>(Sd->alpha);
+                        e_axpy<K, CX>(ma, vr, vi, ur, ui, qr, qi);
+                        Q.store(i, qr, qi);
+                        e_add<K, CX>(ur, ui, qr, qi, wr, wi);
+                        WH[i] = wr[0];
+                        if (CX) WH[L + i] = wi[0];
+                        Y.set_sent(i);
+                        UH.set_sent(i);
+                      });
+    sweep(whead, CX ? whead + ld : nullptr, A.sw_y, uhat, false, 0);
+    // qhat = A uhat ; x += alpha uhat ; r -= alpha qhat ; norm2(r), rho
+    const double *uhc = uhat;
+    rows<K, CX, 1, 1>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 1> &red) {
+                        double qr[K], qi[K], xr[K], xi[K], fr[K], fi[K],
+                            tr[K], ti[K], rr[K], ri[K];
+                        spmv_row<K, CX, true, false>(a, (int)i, uhc, L, qr, qi);
+                        X.load(i, xr, xi);
+                        UH.template load_mc<K>(i, fr, fi);
+                        e_axpy<K, CX>(Sd->alpha, fr, fi, xr, xi, tr, ti);
+                        X.store(i, tr, ti);
+                        Rr.load(i, rr, ri);
+                        const Sc ma = s_neg<K>(Sd->alpha);
+                        e_axpy<K, CX>(ma, qr, qi, rr, ri, tr, ti);
+                        Rr.store(i, tr, ti);
+                        RT.load(i, qr, qi);
+                        acc_hdot<K, CX>(red.h[0], qr, qi, tr, ti);
+                        acc_sumsq<K, CX>(red.nr[0], tr, ti);
+                      });
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc ss = finalize_slot<K, false>(pt_, 1, G_, sm);
+          if (threadIdx.x == 0) {
+            S_->rho_old = S_->rho;
+            if (check_nrm<K>(S_, H, ss)) return;
+            next_iter(S_);
+          }
+        });
+  }
+
+  // ---------------- GPBiCG (solvers.py:331-412) ----------------
+  void gpbicg_setup() {
+    r = mc(); rt0 = mc(); u = mc(); zz = mc(); pp = mc(); Bp = mc();
+    yv = mc(); t = mc(); Bt = mc(); w = mc(); tpr = mc(); yhat = mc();
+    Mp = fv(); Mt = fv(); x = fv();
+    setup_residual(r, rt0, true);
+  }
+
+  void gpbicg_iter() {
+    const MVt Rr = mv(r), RT = mv(rt0), U = mv(u), Z = mv(zz), P = mv(pp),
+              BP = mv(Bp), YV = mv(yv), T = mv(t), BT = mv(Bt), W = mv(w),
+              TPR = mv(tpr), YH = mv(yhat);
+    const FVt MPv = fvv(Mp), MTv = fvv(Mt), Y = fvv(A.sw_y);
+    State *Sd = S;
+    double *H = hist;
+    const DA a = da;
+    const long long L = ld;
+    // K2: w = Bt + beta Bp (end of previous iteration), p = r + beta (p - u)
+    rows<K, CX, 0, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double rr[K], ri[K];
+                        Rr.load(i, rr, ri);
+                        if (Sd->it == 1) {
+                          P.store(i, rr, ri);
+                        } else {
+                          double br[K], bi[K], tr[K], ti[K], pr[K], pi[K],
+                              ur[K], ui[K];
+                          BP.load(i, br, bi);
+                          BT.load(i, tr, ti);
+                          const Sc be = Sd->beta;
+                          double wr[K], wi[K];
+                          e_axpy<K, CX>(be, br, bi, tr, ti, wr, wi);
+                          W.store(i, wr, wi);
+                          P.load(i, pr, pi);
+                          U.load(i, ur, ui);
+                          e_sub<K, CX>(pr, pi, ur, ui, tr, ti);
+                          e_axpy<K, CX>(be, tr, ti, rr, ri, pr, pi);
+                          P.store(i, pr, pi);
+                        }
+                        Y.set_sent(i);
+                        MPv.set_sent(i);
+                      });
+    sweep(head_re(pp), head_im(pp), A.sw_y, Mp, false, 0);
+    const double *mpc = Mp;
+    rows<K, CX, 1, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
+                        double vr[K], vi[K], rr[K], ri[K];
+                        spmv_row<K, CX, true, false>(a, (int)i, mpc, L, vr, vi);
+                        BP.store(i, vr, vi);
+                        RT.load(i, rr, ri);
+                        acc_hdot<K, CX>(red.h[0], rr, ri, vr, vi);
+                      });
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc sg = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) {
+            if (s_is_zero<K, CX>(sg)) {
+              finish_state(S_, S_->it, 0, kBdSigmaZero);
+              return;
+            }
+            if (s_is_zero<K, CX>(S_->rho)) {
+              finish_state(S_, S_->it, 0, kBdRhoZero);
+              return;
+            }
+            S_->alpha = s_div<K, CX>(S_->rho, sg);
+          }
+        });
+    // K5: tpr = t_prev - r ; y = tpr + alpha (Bp - w) ; t = r - alpha Bp
+    rows<K, CX, 0, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double tr[K], ti[K], rr[K], ri[K], dr[K], di[K];
+                        T.load(i, tr, ti);
+                        Rr.load(i, rr, ri);
+                        e_sub<K, CX>(tr, ti, rr, ri, dr, di);
+                        TPR.store(i, dr, di);
+                        double br[K], bi[K], wr[K], wi[K], gr[K], gi[K];
+                        BP.load(i, br, bi);
+                        W.load(i, wr, wi);
+                        e_sub<K, CX>(br, bi, wr, wi, gr, gi);
+                        double yr[K], yi[K];
+                        e_axpy<K, CX>(Sd->alpha, gr, gi, dr, di, yr, yi);
+                        YV.store(i, yr, yi);
+                        const Sc ma = s_neg<K>(Sd->alpha);
+                        e_axpy<K, CX>(ma, br, bi, rr, ri, tr, ti);
+                        T.store(i, tr, ti);
+                        Y.set_sent(i);
+                        MTv.set_sent(i);
+                      });
+    sweep(head_re(t), head_im(t), A.sw_y, Mt, false, 0);
+    // K7: Bt = A Mt ; btbt, btt (+ yy, ybt, bty, yt when it > 1)
+    const double *mtc = Mt;
+    rows<K, CX, 6, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 6, 0> &red) {
+                        double br[K], bi[K], tr[K], ti[K];
+                        spmv_row<K, CX, true, false>(a, (int)i, mtc, L, br, bi);
+                        BT.store(i, br, bi);
+                        T.load(i, tr, ti);
+                        acc_hdot<K, CX>(red.h[0], br, bi, br, bi);
+                        acc_hdot<K, CX>(red.h[1], br, bi, tr, ti);
+                        if (Sd->it > 1) {
+                          double yr[K], yi[K];
+                          YV.load(i, yr, yi);
+                          acc_hdot<K, CX>(red.h[2], yr, yi, yr, yi);
+                          acc_hdot<K, CX>(red.h[3], yr, yi, br, bi);
+                          acc_hdot<K, CX>(red.h[4], br, bi, yr, yi);
+                          acc_hdot<K, CX>(red.h[5], yr, yi, tr, ti);
+                        }
+                      });
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc btbt = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          const Sc btt = finalize_slot<K, CX>(pt_, 1, G_, sm);
+          const bool more = S_->it > 1;  // uniform
+          Sc yy = sc_zero(), ybt = sc_zero(), bty = sc_zero(), yt = sc_zero();
+          if (more) {
+            yy = finalize_slot<K, CX>(pt_, 2, G_, sm);
+            ybt = finalize_slot<K, CX>(pt_, 3, G_, sm);
+            bty = finalize_slot<K, CX>(pt_, 4, G_, sm);
+            yt = finalize_slot<K, CX>(pt_, 5, G_, sm);
+          }
+          if (threadIdx.x == 0) {
+            if (!more) {
+              if (s_is_zero<K, CX>(btbt)) {
+                finish_state(S_, S_->it, 0, kBdLs);
+                return;
+              }
+              S_->zeta = s_div<K, CX>(btt, btbt);
+              S_->eta = sc_zero();
+            } else {
+              const Sc delta = s_sub<K, CX>(s_mul<K, CX>(yy, btbt),
+                                            s_mul<K, CX>(ybt, bty));
+              if (s_is_zero<K, CX>(delta)) {
+                finish_state(S_, S_->it, 0, kBdLs);
+                return;
+              }
+              S_->eta = s_div<K, CX>(s_sub<K, CX>(s_mul<K, CX>(btbt, yt),
+                                                  s_mul<K, CX>(ybt, btt)),
+                                     delta);
+              S_->zeta = s_div<K, CX>(s_sub<K, CX>(s_mul<K, CX>(yy, btt),
+                                                   s_mul<K, CX>(bty, yt)),
+                                      delta);
+            }
+          }
+        });
+    // K8: u, z, yhat, r updates ; norm2(r) [slot 1], rho_new [slot 0]
+    rows<K, CX, 1, 1>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 1> &red) {
+                        const Sc ze = Sd->zeta, et = Sd->eta, al = Sd->alpha;
+                        double br[K], bi[K], ur[K], ui[K];
+                        BP.load(i, br, bi);
+                        if (Sd->it > 1) {
+                          double dr[K], di[K], tr[K], ti[K], sr[K], si[K];
+                          TPR.load(i, dr, di);
+                          U.load(i, ur, ui);
+                          e_axpy<K, CX>(Sd->beta, ur, ui, dr, di, tr, ti);
+                          e_scale<K, CX>(et, tr, ti, sr, si);
+                          e_axpy<K, CX>(ze, br, bi, sr, si, ur, ui);
+                        } else {
+                          e_scale<K, CX>(ze, br, bi, ur, ui);
+                        }
+                        U.store(i, ur, ui);
+                        double zr[K], zi[K], z1r[K], z1i[K], rr[K], ri[K];
+                        Z.load(i, zr, zi);
+                        Rr.load(i, rr, ri);
+                        e_scale<K, CX>(et, zr, zi, z1r, z1i);
+                        e_axpy<K, CX>(ze, rr, ri, z1r, z1i, zr, zi);
+                        const Sc ma = s_neg<K>(al);
+                        e_axpy<K, CX>(ma, ur, ui, zr, zi, z1r, z1i);
+                        Z.store(i, z1r, z1i);
+                        double pr[K], pi[K], hr[K], hi[K], gr[K], gi[K];
+                        P.load(i, pr, pi);
+                        e_axpy<K, CX>(al, pr, pi, z1r, z1i, gr, gi);
+                        YH.load(i, hr, hi);
+                        e_add<K, CX>(hr, hi, gr, gi, pr, pi);
+                        YH.store(i, pr, pi);
+                        double tr[K], ti[K], bt_r[K], bt_i[K], yr[K], yi[K];
+                        T.load(i, tr, ti);
+                        BT.load(i, bt_r, bt_i);
+                        YV.load(i, yr, yi);
+                        e_axpy<K, CX>(s_neg<K>(ze), bt_r, bt_i, tr, ti, gr, gi);
+                        e_axpy<K, CX>(s_neg<K>(et), yr, yi, gr, gi, rr, ri);
+                        Rr.store(i, rr, ri);
+                        double qr[K], qi[K];
+                        RT.load(i, qr, qi);
+                        acc_hdot<K, CX>(red.h[0], qr, qi, rr, ri);
+                        acc_sumsq<K, CX>(red.nr[0], rr, ri);
+                      });
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc rn = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          const Sc ss = finalize_slot<K, false>(pt_, 1, G_, sm);
+          if (threadIdx.x == 0) {
+            if (check_nrm<K>(S_, H, ss)) return;
+            if (s_is_zero<K, CX>(S_->zeta)) {
+              finish_state(S_, S_->it, 0, kBdZetaZero);
+              return;
+            }
+            if (s_is_zero<K, CX>(S_->rho)) {
+              finish_state(S_, S_->it, 0, kBdRhoZero);
+              return;
+            }
+            S_->beta = s_mul<K, CX>(s_div<K, CX>(S_->alpha, S_->zeta),
+                                    s_div<K, CX>(rn, S_->rho));
+            S_->rho = rn;
+            next_iter(S_);
+          }
+        });
+  }
+
+  // ---------------- BiCG (solvers.py:183-226) ----------------
+  void bicg_setup() {
+    x = mc(); r = mc(); rt = mc(); pp = mc(); pt = mc(); qv = mc(); qt = mc();
+    zf = fv(); ztf = fv();
+    setup_residual(r, rt, false);
+    const FVt Z = fvv(zf), ZT = fvv(ztf), Y = fvv(A.sw_y), Y2 = fvv(A.sw_y2);
+    rows<K, CX, 0, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        Y.set_sent(i);
+                        Z.set_sent(i);
+                        Y2.set_sent(i);
+                        ZT.set_sent(i);
+                      });
+    sweep(head_re(r), head_im(r), A.sw_y, zf, false, 0);
+    sweep(head_re(rt), head_im(rt), A.sw_y2, ztf, true, 1);
+    const MVt P = mv(pp), PT = mv(pt), Rr = mv(r);
+    rows<K, CX, 1, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
+                        double zr[K], zi[K], wr[K], wi[K], rr[K], ri[K];
+                        Z.template load_mc<K>(i, zr, zi);
+                        ZT.template load_mc<K>(i, wr, wi);
+                        P.store(i, zr, zi);
+                        PT.store(i, wr, wi);
+                        Rr.load(i, rr, ri);
+                        acc_hdot<K, CX>(red.h[0], wr, wi, rr, ri);
+                      });
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc rho = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) S_->rho = rho;
+        });
+  }
+
+  void bicg_iter() {
+    const MVt X = mv(x), Rr = mv(r), RTv = mv(rt), P = mv(pp), PT = mv(pt),
+              Q = mv(qv), QT = mv(qt);
+    const FVt Z = fvv(zf), ZT = fvv(ztf), Y = fvv(A.sw_y), Y2 = fvv(A.sw_y2);
+    State *Sd = S;
+    double *H = hist;
+    const DA a = da;
+    const long long L = ld;
+    const double *pc = pp, *ptc = pt;
+    // q = A p ; qt = A^H pt ; sigma = hdot(pt, q)
+    rows<K, CX, 1, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
+                        double qr[K], qi[K], wr[K], wi[K], pr[K], pi[K];
+                        spmv_row<K, CX, false, false>(a, (int)i, pc, L, qr, qi);
+                        spmv_row<K, CX, false, true>(a, (int)i, ptc, L, wr, wi);
+                        Q.store(i, qr, qi);
+                        QT.store(i, wr, wi);
+                        PT.load(i, pr, pi);
+                        acc_hdot<K, CX>(red.h[0], pr, pi, qr, qi);
+                      });
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc sg = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) {
+            if (s_is_zero<K, CX>(sg)) {
+              finish_state(S_, S_->it, 0, kBdSigmaZero);
+              return;
+            }
+            if (s_is_zero<K, CX>(S_->rho)) {
+              finish_state(S_, S_->it, 0, kBdRhoZero);
+              return;
+            }
+            S_->alpha = s_div<K, CX>(S_->rho, sg);
+          }
+        });
+    rows<K, CX, 0, 1>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 1> &red) {
+                        const Sc al = Sd->alpha;
+                        double xr[K], xi[K], pr[K], pi[K], tr[K], ti[K];
+                        X.load(i, xr, xi);
+                        P.load(i, pr, pi);
+                        e_axpy<K, CX>(al, pr, pi, xr, xi, tr, ti);
+                        X.store(i, tr, ti);
+                        double rr[K], ri[K], qr[K], qi[K];
+                        Rr.load(i, rr, ri);
+                        Q.load(i, qr, qi);
+                        e_axpy<K, CX>(s_neg<K>(al), qr, qi, rr, ri, tr, ti);
+                        Rr.store(i, tr, ti);
+                        acc_sumsq<K, CX>(red.nr[0], tr, ti);
+                        RTv.load(i, rr, ri);
+                        QT.load(i, qr, qi);
+                        e_axpy<K, CX>(s_neg<K>(s_conj<K, CX>(al)), qr, qi, rr,
+                                      ri, xr, xi);
+                        RTv.store(i, xr, xi);
+                        Y.set_sent(i);
+                        Z.set_sent(i);
+                        Y2.set_sent(i);
+                        ZT.set_sent(i);
+                      });
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc ss = finalize_slot<K, false>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) check_nrm<K>(S_, H, ss);
+        });
+    sweep(head_re(r), head_im(r), A.sw_y, zf, false, 0);
+    sweep(head_re(rt), head_im(rt), A.sw_y2, ztf, true, 1);
+    rows<K, CX, 1, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
+                        double wr[K], wi[K], rr[K], ri[K];
+                        ZT.template load_mc<K>(i, wr, wi);
+                        Rr.load(i, rr, ri);
+                        acc_hdot<K, CX>(red.h[0], wr, wi, rr, ri);
+                      });
+    fin(S, err, part, G, st,
+        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
+          const Sc rn = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          if (threadIdx.x == 0) {
+            S_->beta = s_div<K, CX>(rn, S_->rho);
+            S_->rho = rn;
+            next_iter(S_);
+          }
+        });
+    // p = z + beta p ; pt = zt + conj(beta) pt (runs unless stopped above)
+    rows<K, CX, 0, 0>(n, done, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        const Sc be = Sd->beta;
+                        double pr[K], pi[K], zr[K], zi[K], tr[K], ti[K];
+                        P.load(i, pr, pi);
+                        Z.template load_mc<K>(i, zr, zi);
+                        e_axpy<K, CX>(be, pr, pi, zr, zi, tr, ti);
+                        P.store(i, tr, ti);
+                        PT.load(i, pr, pi);
+                        ZT.template load_mc<K>(i, zr, zi);
+                        e_axpy<K, CX>(s_conj<K, CX>(be), pr, pi, zr, zi, tr, ti);
+                        PT.store(i, tr, ti);
+                      });
+  }
+
+  // ---------------- driver ----------------
+  void setup() {
+    switch (p.method) {
+      case kBiCG: bicg_setup(); break;
+      case kCGS: cgs_setup(); break;
+      case kBiCGSTAB: bicgstab_setup(); break;
+      default: gpbicg_setup(); break;
+    }
+  }
+  void iter() {
+    switch (p.method) {
+      case kBiCG: bicg_iter(); break;
+      case kCGS: cgs_iter(); break;
+      case kBiCGSTAB: bicgstab_iter(); break;
+      default: gpbicg_iter(); break;
+    }
+  }
+
+  // x_out (planar MC) after the loop; returns false on error
+  void finish(const State &hs, double *d_x) {
+    const long long planes = K * (CX ? 2 : 1);
+    if (p.method == kBiCGSTAB) bicgstab_finish(hs);
+    if (p.method == kGPBiCG) {
+      // x = M^-1 yhat (solvers.py:357-359), or yhat itself on the r0 exit
+      if (hs.iterations == 0 && hs.converged) {
+        cudaMemcpyAsync(d_x, yhat, sizeof(double) * planes * ld,
+                        cudaMemcpyDeviceToDevice, st);
+        return;
+      }
+      launch_sweep_reset(A.sw_y, x, n, CX, nullptr, st);
+      sweep(head_re(yhat), head_im(yhat), A.sw_y, x, false, 0);
+      promote(x, d_x);
+      return;
+    }
+    cudaMemcpyAsync(d_x, x, sizeof(double) * planes * ld,
+                    cudaMemcpyDeviceToDevice, st);
+  }
+
+  void promote(const double *f, double *d_x) {
+    const FVt F = fvv(const_cast<double *>(f));
+    const MVt X = mv(d_x);
+    rows<K, CX, 0, 0>(n, nullptr, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double xr[K], xi[K];
+                        F.template load_mc<K>(i, xr, xi);
+                        X.store(i, xr, xi);
+                      });
+  }
+
+  // true residual ||b - A x|| / ||b|| (solvers.py:446-450); x planar MC
+  void true_residual(const double *d_x) {
+    const MVt B = mv(b);
+    const DA a = da;
+    const long long L = ld;
+    rows<K, CX, 0, 2>(n, nullptr, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 2> &red) {
+                        double axr[K], axi[K], br[K], bi[K], rr[K], ri[K];
+                        spmv_row<K, CX, false, false>(a, (int)i, d_x, L, axr, axi);
+                        B.load(i, br, bi);
+                        e_sub<K, CX>(br, bi, axr, axi, rr, ri);
+                        acc_sumsq<K, CX>(red.nr[0], rr, ri);
+                        acc_sumsq<K, CX>(red.nr[1], br, bi);
+                      });
+    true_res_kernel_impl<K, CX><<<1, kBlock, 0, st>>>(S, part, G);
+  }
+};
+
+// ---------------------------------------------------------------------
+// graph execution
+// ---------------------------------------------------------------------
+#define CK(x)                                                              \
+  do {                                                                     \
+    cudaError_t e_ = (x);                                                  \
+    if (e_ != cudaSuccess) {                                               \
+      snprintf(errbuf, 256, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+               __FILE__, __LINE__);                                        \
+      return 4;                                                            \
+    }                                                                      \
+  } while (0)
+
+template <int K, bool CX>
+int run_typed(DMat &A, const SolveParams &p, const double *d_b,
+                     double *d_x, double *d_hist, SolveOut *out,
+                     cudaStream_t st, char *errbuf) {
+  if (!p.precond_ilu) {
+    snprintf(errbuf, 256, "precond 'none' is not implemented on the device path");
+    return 3;
+  }
+  if (p.method == kBiCG) ensure_adjoint(A, st);
+  Solver<K, CX> sv(A, p, st, d_hist, errbuf);
+  if (!sv.ok) return 4;
+  State hs{};
+  hs.max_iter = p.max_iter;
+  hs.hist_cap = p.hist_cap;
+  hs.eps_rel = p.eps_rel;
+  hs.eps_abs = p.eps_abs;
+  hs.relres = NAN;
+  hs.true_relres = NAN;
+  CK(cudaMemcpyAsync(sv.S, &hs, sizeof(State), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(A.err, 0, sizeof(int), st));
+  sv.alloc_common(d_b);
+  if (!sv.ok) return 4;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  sv.setup();
+  if (!sv.ok) return 4;
+  CK(cudaGetLastError());
+
+  // one iteration -> WHILE body
+  const char *nocond = getenv("MPK_NO_COND_GRAPH");
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  if (!nocond || nocond[0] == '0') {
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+    cudaKernelNodeParams kp{};
+    State *Sd = sv.S;
+    void *args[] = {&h, &Sd};
+    kp.func = (void *)set_cond_kernel;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = args;
+    cudaGraphNode_t n1, n2;
+    CK(cudaGraphAddKernelNode(&n1, g, nullptr, 0, &kp));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    CK(cudaGraphAddNode(&n2, g, &n1, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    sv.iter();
+    set_cond_kernel<<<1, 1, 0, st>>>(h, sv.S);
+    CK(cudaStreamEndCapture(st, &body));
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    CK(cudaGraphLaunch(ge, st));
+  } else {
+    // fallback: replay a plain one-iteration graph in chunks, polling done
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    sv.iter();
+    CK(cudaStreamEndCapture(st, &g));
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    long long launched = 0;
+    int chunk = 4;
+    State probe{};
+    while (launched < p.max_iter) {
+      for (int c = 0; c < chunk && launched < p.max_iter; ++c, ++launched)
+        CK(cudaGraphLaunch(ge, st));
+      CK(cudaMemcpyAsync(&probe, sv.S, sizeof(State), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (probe.done) break;
+      if (chunk < 64) chunk *= 2;
+    }
+  }
+  cudaEventRecord(e1, st);
+  CK(cudaMemcpyAsync(&hs, sv.S, sizeof(State), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (!hs.done) {
+    // loop ran out without a device-side stop (max_iter reached)
+    hs.iterations = p.max_iter;
+    hs.converged = 0;
+    hs.breakdown = kBdNone;
+  }
+  float loop_ms = 0;
+  cudaEventElapsedTime(&loop_ms, e0, e1);
+  if (ge) cudaGraphExecDestroy(ge);
+  if (g) cudaGraphDestroy(g);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+
+  out->hist_len = hs.hist_len;
+  if (hs.breakdown == kBdNumericSweep) {
+    out->iterations = 0;
+    out->converged = 0;
+    out->breakdown = kBdNumericSweep;
+    out->half_exit = 0;
+    out->relres = NAN;
+    out->true_relres = NAN;
+    out->loop_ms = loop_ms;
+    return 0;
+  }
+  sv.finish(hs, d_x);
+  int e_after = 0;
+  if (p.method == kGPBiCG && !(hs.iterations == 0 && hs.converged)) {
+    CK(cudaMemcpyAsync(&e_after, A.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
+  relres_kernel<K><<<1, 1, 0, st>>>(sv.S);
+  sv.true_residual(d_x);
+  CK(cudaMemcpyAsync(&hs, sv.S, sizeof(State), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  if (e_after) {
+    out->iterations = 0;
+    out->converged = 0;
+    out->breakdown = kBdNumericSweep;
+    out->half_exit = 0;
+    out->relres = NAN;
+    out->true_relres = NAN;
+    out->loop_ms = loop_ms;
+    return 0;
+  }
+  out->iterations = hs.iterations;
+  out->converged = hs.converged;
+  out->breakdown = hs.breakdown;
+  out->half_exit = hs.half_exit;
+  out->relres = hs.relres;
+  out->true_relres = hs.true_relres;
+  out->loop_ms = loop_ms;
+  return 0;
+}
+
+}  // namespace mpk

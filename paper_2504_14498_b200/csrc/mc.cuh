@@ -1,0 +1,589 @@
+// mc.cuh -- multi-component (DD/TD/QD) binary64 arithmetic, host+device.
+//
+// Bit-identical twin of the reference's scalar MC arithmetic
+// (/root/reference/pkg/src/mpkrylov/_mccore.py:19-186,222-266,322-347 and
+// its numba twin _kernels.py:24-214), re-designed for registers:
+//
+//  * renorm<M,K> runs the reference's distillation passes (VecSum +
+//    zero-eliminating extraction + strictness check, <= 8 passes,
+//    _mccore.py:54-116) on a FIXED M-slot register array.  Instead of
+//    compacting the list (dynamic indexing -> local memory), eliminated
+//    slots are left as +0.0 "holes".  A zero term is transparent to every
+//    step of a pass: two_sum(x, 0) = (x, 0) exactly, extraction skips it, and
+//    the strictness check / final truncation skip it as well, so the emitted
+//    component sequence is identical to the compacted reference (only the
+//    sign of zero results can differ, and the reference normalises those to
+//    +0.0 at the end, _mccore.py:112-115).  This also means terms that are
+//    known to be zero (zero tails of promoted binary64 values) can be dropped
+//    at compile time: mul_lf / mul_rf / mul_ff below are the reference's
+//    mc_mul with a promoted binary64 operand, minus its zero terms.
+//  * TwoProd uses FMA: bit-identical to the reference's Dekker split for
+//    operands whose product neither overflows nor underflows (SURVEY.md
+//    finding 8).  All other binary64 operations use explicit _rn intrinsics,
+//    so no FMA contraction can occur regardless of compiler flags.
+//
+// Non-finite operands follow the reference's non-finite path (plain sum of
+// the terms in the head) except that products of a dropped zero term with
+// an infinite operand are not formed; the result is non-finite either way.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define MPK_HD __host__ __device__ __forceinline__
+// scalar-only operations (run once per iteration by one thread): keep them
+// out of line so the kernels that call them stay small.
+#define MPK_SCALAR __host__ __device__ __noinline__
+#else
+#define MPK_HD inline
+#define MPK_SCALAR inline
+#endif
+
+namespace mpk {
+
+MPK_HD double dadd(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  volatile double r = a + b;
+  return r;
+#endif
+}
+MPK_HD double dsub(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dsub_rn(a, b);
+#else
+  volatile double r = a - b;
+  return r;
+#endif
+}
+MPK_HD double dmul(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  volatile double r = a * b;
+  return r;
+#endif
+}
+MPK_HD double ddiv(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __ddiv_rn(a, b);
+#else
+  volatile double r = a / b;
+  return r;
+#endif
+}
+MPK_HD double dfma(double a, double b, double c) {
+#ifdef __CUDA_ARCH__
+  return __fma_rn(a, b, c);
+#else
+  return std::fma(a, b, c);
+#endif
+}
+MPK_HD double dsqrt(double a) {
+#ifdef __CUDA_ARCH__
+  return __dsqrt_rn(a);
+#else
+  return std::sqrt(a);
+#endif
+}
+MPK_HD bool isfin(double a) {
+#ifdef __CUDA_ARCH__
+  return isfinite(a);
+#else
+  return std::isfinite(a);
+#endif
+}
+MPK_HD double dabs(double a) { return fabs(a); }
+
+// two_sum _mccore.py:19-24
+MPK_HD void two_sum(double a, double b, double &s, double &e) {
+  double q = dadd(a, b);
+  double bb = dsub(q, a);
+  e = dadd(dsub(a, dsub(q, bb)), dsub(b, bb));
+  s = q;
+}
+
+// two_prod _mccore.py:40-51 (FMA form, see header)
+MPK_HD void two_prod(double a, double b, double &p, double &e) {
+  p = dmul(a, b);
+  e = dfma(a, b, -p);
+}
+
+// renorm_terms _mccore.py:90-116 on M register slots (holes = +0.0).
+template <int M, int K>
+MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < M; ++i) fin = fin && isfin(t[i]);
+  if (!fin) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) s = dadd(s, t[i]);
+    out[0] = s;
+#pragma unroll
+    for (int i = 1; i < K; ++i) out[i] = 0.0;
+    return;
+  }
+#pragma unroll 1
+  for (int pass = 0; pass < 8; ++pass) {
+    double e[M];
+    double s = t[M - 1];
+#pragma unroll
+    for (int i = M - 2; i >= 0; --i) {
+      double q, err;
+      two_sum(t[i], s, q, err);
+      e[i + 1] = err;
+      s = q;
+    }
+    e[0] = s;
+    double eps = e[0];
+#pragma unroll
+    for (int i = 1; i < M; ++i) {
+      double q, en;
+      two_sum(eps, e[i], q, en);
+      const bool em = (en != 0.0);
+      t[i - 1] = em ? q : 0.0;
+      eps = em ? en : q;
+    }
+    t[M - 1] = eps;
+    bool ok = true;
+    double prev = 0.0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      const double c = t[i];
+      if (c != 0.0) {
+        if (prev != 0.0 && dadd(prev, c) != prev) ok = false;
+        prev = c;
+      }
+    }
+    if (ok) break;
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) out[j] = 0.0;
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    const double c = t[i];
+    if (c != 0.0) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (cnt == j) out[j] = c;
+      ++cnt;
+    }
+  }
+}
+
+// Reference merge of two component lists by magnitude, ties prefer x
+// (_mccore.py:134-154), for arbitrary (not necessarily sorted) inputs.
+template <int KX, int KY>
+MPK_HD void merge(const double (&x)[KX], const double (&y)[KY],
+                  double (&buf)[KX + KY]) {
+  int i = 0;
+#pragma unroll
+  for (int t = 0; t < KX + KY; ++t) {
+    double xi = 0.0, yj = 0.0;
+#pragma unroll
+    for (int a = 0; a < KX; ++a)
+      if (i == a) xi = x[a];
+#pragma unroll
+    for (int a = 0; a < KY; ++a)
+      if (t - i == a) yj = y[a];
+    const bool xv = i < KX, yv = (t - i) < KY;
+    const bool tx = xv && (!yv || dabs(xi) >= dabs(yj));
+    buf[t] = tx ? xi : yj;
+    i += tx ? 1 : 0;
+  }
+}
+
+// mc_add _mccore.py:129-155
+template <int K>
+MPK_HD void add(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
+  if (K == 1) {
+    out[0] = dadd(x[0], y[0]);
+    return;
+  }
+  double buf[2 * K];
+  merge<K, K>(x, y, buf);
+  renorm<2 * K, K>(buf, out);
+}
+
+// mc_add(x, (y0, y1, 0, ..., 0)): the trailing zeros of y are merged after
+// every element of x (|x_i| >= 0), so they are transparent.
+template <int K>
+MPK_HD void add2(const double (&x)[K], double y0, double y1,
+                 double (&out)[K]) {
+  if (K == 1) {
+    out[0] = dadd(x[0], y0);
+    return;
+  }
+  const double y[2] = {y0, y1};
+  double buf[K + 2];
+  merge<K, 2>(x, y, buf);
+  renorm<K + 2, K>(buf, out);
+}
+
+// mc_sub _mccore.py:158-159 (add of the componentwise negation)
+template <int K>
+MPK_HD void sub(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
+  double ny[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) ny[i] = -y[i];
+  add<K>(x, ny, out);
+}
+
+template <int K>
+MPK_HD void neg(const double (&x)[K], double (&out)[K]) {
+#pragma unroll
+  for (int i = 0; i < K; ++i) out[i] = -x[i];
+}
+
+// mc_mul _mccore.py:162-186: level l < K-1 two-prods (errors carried to
+// level l+1), level K-1 plain products, renorm of the K*K terms.
+template <int K>
+MPK_HD void mul(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
+  if (K == 1) {
+    out[0] = dmul(x[0], y[0]);
+    return;
+  }
+  double t[K * K];
+  double carry[K > 1 ? K - 1 : 1];
+  double nxt[K > 1 ? K - 1 : 1];
+  int nt = 0;
+#pragma unroll
+  for (int lvl = 0; lvl < K; ++lvl) {
+    if (lvl < K - 1) {
+#pragma unroll
+      for (int i = 0; i <= lvl; ++i) {
+        double p, e;
+        two_prod(x[i], y[lvl - i], p, e);
+        t[nt++] = p;
+        nxt[i] = e;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i <= lvl; ++i) t[nt++] = dmul(x[i], y[lvl - i]);
+    }
+#pragma unroll
+    for (int c = 0; c < lvl; ++c) t[nt++] = carry[c];
+    if (lvl < K - 1) {
+#pragma unroll
+      for (int c = 0; c <= lvl; ++c) carry[c] = nxt[c];
+    }
+  }
+  renorm<K * K, K>(t, out);
+}
+
+// mc_mul((a,0,..,0), y): non-zero terms in reference order are
+// p(a,y0) | p(a,y1) e(a,y0) | ... | a*y_{K-1} e(a,y_{K-2})  (2K-1 slots)
+template <int K>
+MPK_HD void mul_lf(double a, const double (&y)[K], double (&out)[K]) {
+  if (K == 1) {
+    out[0] = dmul(a, y[0]);
+    return;
+  }
+  double t[2 * K - 1];
+  double pe = 0.0;
+  int nt = 0;
+#pragma unroll
+  for (int l = 0; l < K; ++l) {
+    if (l < K - 1) {
+      double p, e;
+      two_prod(a, y[l], p, e);
+      t[nt++] = p;
+      if (l > 0) t[nt++] = pe;
+      pe = e;
+    } else {
+      t[nt++] = dmul(a, y[l]);
+      t[nt++] = pe;
+    }
+  }
+  renorm<2 * K - 1, K>(t, out);
+}
+
+// mc_mul(x, (f,0,..,0)): same slot pattern with p(x_l, f).
+template <int K>
+MPK_HD void mul_rf(const double (&x)[K], double f, double (&out)[K]) {
+  if (K == 1) {
+    out[0] = dmul(x[0], f);
+    return;
+  }
+  double t[2 * K - 1];
+  double pe = 0.0;
+  int nt = 0;
+#pragma unroll
+  for (int l = 0; l < K; ++l) {
+    if (l < K - 1) {
+      double p, e;
+      two_prod(x[l], f, p, e);
+      t[nt++] = p;
+      if (l > 0) t[nt++] = pe;
+      pe = e;
+    } else {
+      t[nt++] = dmul(x[l], f);
+      t[nt++] = pe;
+    }
+  }
+  renorm<2 * K - 1, K>(t, out);
+}
+
+// mc_mul((a,0..), (f,0..)) = renorm([p, e]) = (p+0, e+0, 0, ..) when p is
+// finite (|e| <= ulp(p)/2 and fl(p+e) = p by round-to-nearest-even).
+MPK_HD void mul_ff2(double a, double f, double &h, double &l) {
+  double p, e;
+  two_prod(a, f, p, e);
+  if (isfin(p)) {
+    h = dadd(p, 0.0);
+    l = dadd(e, 0.0);
+  } else {
+    h = dadd(dadd(0.0, p), e);
+    l = 0.0;
+  }
+}
+
+// complex product (twin _cmul1 _kernels.py:206-214 / cx_mul _mccore.py:322)
+template <int K>
+MPK_HD void cmul(const double (&ar)[K], const double (&ai)[K],
+                 const double (&br)[K], const double (&bi)[K],
+                 double (&outr)[K], double (&outi)[K]) {
+  double t1[K], t2[K], r[K];
+  mul<K>(ar, br, t1);
+  mul<K>(ai, bi, t2);
+  sub<K>(t1, t2, r);
+  mul<K>(ar, bi, t1);
+  mul<K>(ai, br, t2);
+  add<K>(t1, t2, outi);
+#pragma unroll
+  for (int i = 0; i < K; ++i) outr[i] = r[i];
+}
+
+// complex product with a promoted binary64 left operand (ar,0..)+i(ai,0..)
+template <int K>
+MPK_HD void cmul_lf(double ar, double ai, const double (&br)[K],
+                    const double (&bi)[K], double (&outr)[K],
+                    double (&outi)[K]) {
+  double t1[K], t2[K], r[K];
+  mul_lf<K>(ar, br, t1);
+  mul_lf<K>(ai, bi, t2);
+  sub<K>(t1, t2, r);
+  mul_lf<K>(ar, bi, t1);
+  mul_lf<K>(ai, br, t2);
+  add<K>(t1, t2, outi);
+#pragma unroll
+  for (int i = 0; i < K; ++i) outr[i] = r[i];
+}
+
+// complex product of two promoted binary64 values: each real product is a
+// 2-term value (p, e); sub/add merge two 2-term lists (zeros transparent).
+template <int K>
+MPK_HD void cmul_ff(double ar, double ai, double br, double bi,
+                    double (&outr)[K], double (&outi)[K]) {
+  double h1, l1, h2, l2;
+  mul_ff2(ar, br, h1, l1);
+  mul_ff2(ai, bi, h2, l2);
+  {
+    const double x[2] = {h1, l1};
+    const double y[2] = {-h2, -l2};
+    double buf[4];
+    merge<2, 2>(x, y, buf);
+    renorm<4, K>(buf, outr);
+  }
+  mul_ff2(ar, bi, h1, l1);
+  mul_ff2(ai, br, h2, l2);
+  {
+    const double x[2] = {h1, l1};
+    const double y[2] = {h2, l2};
+    double buf[4];
+    merge<2, 2>(x, y, buf);
+    renorm<4, K>(buf, outi);
+  }
+}
+
+template <int K>
+MPK_HD bool is_zero(const double (&x)[K]) {
+  bool z = true;
+#pragma unroll
+  for (int i = 0; i < K; ++i) z = z && (x[i] == 0.0);
+  return z;
+}
+
+template <int K>
+MPK_HD bool is_finite(const double (&x)[K]) {
+  bool f = true;
+#pragma unroll
+  for (int i = 0; i < K; ++i) f = f && isfin(x[i]);
+  return f;
+}
+
+// _div_by_zero _mccore.py:216-219
+MPK_HD double div_by_zero(double x0, double y0) {
+  if (x0 == 0.0) return NAN;
+  return dmul(copysign(INFINITY, x0), copysign(1.0, y0));
+}
+
+// mc_div _mccore.py:222-237 (Newton reciprocal seeded by binary64 1/y0)
+template <int K>
+MPK_SCALAR void div(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
+  if (K == 1) {
+    out[0] = (y[0] == 0.0) ? div_by_zero(x[0], y[0]) : ddiv(x[0], y[0]);
+    return;
+  }
+  if (y[0] == 0.0 && is_zero<K>(y)) {
+    out[0] = div_by_zero(x[0], y[0]);
+#pragma unroll
+    for (int i = 1; i < K; ++i) out[i] = 0.0;
+    return;
+  }
+  double one[K], w[K], t1[K], t2[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) one[i] = w[i] = 0.0;
+  one[0] = 1.0;
+  w[0] = ddiv(1.0, y[0]);
+  const int iters = (K == 2) ? 1 : 2;
+  for (int it = 0; it < iters; ++it) {
+    mul<K>(y, w, t1);
+    sub<K>(one, t1, t2);
+    mul<K>(w, t2, t1);
+    add<K>(w, t1, t2);
+#pragma unroll
+    for (int i = 0; i < K; ++i) w[i] = t2[i];
+  }
+  double q[K], r[K];
+  mul<K>(x, w, q);
+  mul<K>(q, y, t1);
+  sub<K>(x, t1, r);
+  mul<K>(r, w, t2);
+  add<K>(q, t2, out);
+}
+
+// mc_sqrt _mccore.py:245-266 (Newton on rsqrt). Returns false if x0 < 0.
+template <int K>
+MPK_SCALAR bool sqrt_mc(const double (&x)[K], double (&out)[K]) {
+  if (x[0] < 0.0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) out[i] = NAN;
+    return false;
+  }
+  if (x[0] == 0.0 && is_zero<K>(x)) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) out[i] = 0.0;
+    return true;
+  }
+  if (K == 1) {
+    out[0] = dsqrt(x[0]);
+    return true;
+  }
+  double one[K], z[K], t[K], a[K], b[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) one[i] = z[i] = 0.0;
+  one[0] = 1.0;
+  z[0] = ddiv(1.0, dsqrt(x[0]));
+  const int iters = (K == 2) ? 1 : 2;
+  for (int it = 0; it < iters; ++it) {
+    mul<K>(z, z, a);
+    mul<K>(x, a, b);
+    sub<K>(one, b, t);
+    mul<K>(z, t, a);
+#pragma unroll
+    for (int i = 0; i < K; ++i) a[i] = dmul(a[i], 0.5);
+    add<K>(z, a, b);
+#pragma unroll
+    for (int i = 0; i < K; ++i) z[i] = b[i];
+  }
+  double r[K];
+  mul<K>(x, z, r);
+  mul<K>(r, r, a);
+  sub<K>(x, a, t);
+#pragma unroll
+  for (int i = 0; i < K; ++i) b[i] = dmul(z[i], 0.5);
+  mul<K>(t, b, a);
+  add<K>(r, a, out);
+  return true;
+}
+
+// mc_cmp _mccore.py:283-290
+template <int K>
+MPK_SCALAR int cmp(const double (&x)[K], const double (&y)[K]) {
+  double d[K];
+  sub<K>(x, y, d);
+  if (d[0] > 0.0) return 1;
+  if (d[0] < 0.0) return -1;
+  return 0;
+}
+
+// cx_div _mccore.py:328-347 (Smith)
+template <int K>
+MPK_SCALAR void cdiv(const double (&ar)[K], const double (&ai)[K],
+                 const double (&br)[K], const double (&bi)[K],
+                 double (&outr)[K], double (&outi)[K]) {
+  double t[K], d[K], u[K], v[K], re[K], im[K];
+  if (dabs(br[0]) >= dabs(bi[0])) {
+    if (is_zero<K>(br) && is_zero<K>(bi)) {
+      outr[0] = div_by_zero(ar[0], 0.0);
+      outi[0] = div_by_zero(ai[0], 0.0);
+#pragma unroll
+      for (int i = 1; i < K; ++i) outr[i] = outi[i] = 0.0;
+      return;
+    }
+    div<K>(bi, br, t);
+    mul<K>(bi, t, u);
+    add<K>(br, u, d);
+    mul<K>(ai, t, u);
+    add<K>(ar, u, v);
+    div<K>(v, d, re);
+    mul<K>(ar, t, u);
+    sub<K>(ai, u, v);
+    div<K>(v, d, im);
+  } else {
+    div<K>(br, bi, t);
+    mul<K>(br, t, u);
+    add<K>(u, bi, d);
+    mul<K>(ar, t, u);
+    add<K>(u, ai, v);
+    div<K>(v, d, re);
+    mul<K>(ai, t, u);
+    sub<K>(u, ar, v);
+    div<K>(v, d, im);
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    outr[i] = re[i];
+    outi[i] = im[i];
+  }
+}
+
+// ---------------------------------------------------------------------
+// CPython binary64 complex arithmetic (k=1 complex ILU(0), ilu.py:195-220,
+// :377-381): product without FMA, Smith division as in _Py_c_quot.
+// ---------------------------------------------------------------------
+MPK_HD void py_cmul(double ar, double ai, double br, double bi, double &pr,
+                    double &pi) {
+  pr = dsub(dmul(ar, br), dmul(ai, bi));
+  pi = dadd(dmul(ar, bi), dmul(ai, br));
+}
+
+MPK_HD void py_cdiv(double ar, double ai, double br, double bi, double &qr,
+                    double &qi) {
+  const double abr = br < 0 ? -br : br;
+  const double abi = bi < 0 ? -bi : bi;
+  if (abr >= abi) {
+    if (abr == 0.0) {
+      qr = qi = 0.0;  // CPython raises ZeroDivisionError; unreachable
+    } else {
+      const double ratio = ddiv(bi, br);
+      const double denom = dadd(br, dmul(bi, ratio));
+      qr = ddiv(dadd(ar, dmul(ai, ratio)), denom);
+      qi = ddiv(dsub(ai, dmul(ar, ratio)), denom);
+    }
+  } else if (abi >= abr) {
+    const double ratio = ddiv(br, bi);
+    const double denom = dadd(dmul(br, ratio), bi);
+    qr = ddiv(dadd(dmul(ar, ratio), ai), denom);
+    qi = ddiv(dsub(dmul(ai, ratio), ar), denom);
+  } else {
+    qr = qi = NAN;
+  }
+}
+
+}  // namespace mpk

@@ -1,0 +1,309 @@
+// units.cu -- single-operation device kernels behind the C-ABI unit entry
+// points (spmv, hdot, norm2, axpy, element-wise MC ops, layout transposes).
+// They reuse the solver's row framework so the parity tests exercise the
+// exact code the solver runs.
+#include <cstdio>
+
+#include "rows.cuh"
+
+namespace mpk {
+
+template <int K, bool CX>
+static void spmv_typed(DMat &A, bool adjoint, bool xf, const double *d_x,
+                       double *d_y, cudaStream_t st) {
+  const DA a{A.n, A.rp, A.ci, A.val, A.at_rp, A.at_ci, A.at_val};
+  const long long L = plane_ld(A.n);
+  const MV<K, CX> Y{d_y, L};
+  if (xf && !adjoint)
+    rows<K, CX, 0, 0>(A.n, nullptr, nullptr, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double yr[K], yi[K];
+                        spmv_row<K, CX, true, false>(a, (int)i, d_x, L, yr, yi);
+                        Y.store(i, yr, yi);
+                      });
+  else if (xf && adjoint)
+    rows<K, CX, 0, 0>(A.n, nullptr, nullptr, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double yr[K], yi[K];
+                        spmv_row<K, CX, true, true>(a, (int)i, d_x, L, yr, yi);
+                        Y.store(i, yr, yi);
+                      });
+  else if (!adjoint)
+    rows<K, CX, 0, 0>(A.n, nullptr, nullptr, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double yr[K], yi[K];
+                        spmv_row<K, CX, false, false>(a, (int)i, d_x, L, yr, yi);
+                        Y.store(i, yr, yi);
+                      });
+  else
+    rows<K, CX, 0, 0>(A.n, nullptr, nullptr, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                        double yr[K], yi[K];
+                        spmv_row<K, CX, false, true>(a, (int)i, d_x, L, yr, yi);
+                        Y.store(i, yr, yi);
+                      });
+}
+
+int unit_spmv(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
+              double *d_y, cudaStream_t st) {
+  if (adjoint) ensure_adjoint(A, st);
+#define DISPATCH(KK)                                              \
+  if (k == KK) {                                                  \
+    if (A.cx)                                                     \
+      spmv_typed<KK, true>(A, adjoint, x_is_f, d_x, d_y, st);     \
+    else                                                          \
+      spmv_typed<KK, false>(A, adjoint, x_is_f, d_x, d_y, st);    \
+    return 0;                                                     \
+  }
+  DISPATCH(2)
+  DISPATCH(3)
+  DISPATCH(4)
+#undef DISPATCH
+  return 3;
+}
+
+template <int K, bool CX>
+__global__ void unit_fin_kernel(const double *part, int G, int op,
+                                double *out) {
+  __shared__ double sm[kWarpsPerBlock * 8];
+  if (op == 0) {
+    const Sc s = finalize_slot<K, CX>(part, 0, G, sm);
+    if (threadIdx.x == 0)
+      for (int c = 0; c < K; ++c) {
+        out[c] = s.re[c];
+        out[4 + c] = s.im[c];
+      }
+  } else {
+    const Sc s = finalize_slot<K, false>(part, 0, G, sm);
+    if (threadIdx.x == 0) {
+      double o[K];
+      sqrt_mc<K>(R<K>(s), o);
+      for (int c = 0; c < K; ++c) out[c] = o[c];
+    }
+  }
+}
+
+template <int K, bool CX>
+static int reduce_typed(int op, long long n, const double *d_x,
+                        const double *d_y, double *h_out, cudaStream_t st) {
+  const long long L = plane_ld(n);
+  const MV<K, CX> X{const_cast<double *>(d_x), L},
+      Y{const_cast<double *>(d_y), L};
+  double *part = nullptr, *out = nullptr;
+  cudaMalloc(&part, sizeof(double) * kMaxGrid * 8);
+  cudaMalloc(&out, sizeof(double) * 8);
+  if (op == 0)
+    rows<K, CX, 1, 0>(n, nullptr, part, st,
+                      [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
+                        double xr[K], xi[K], yr[K], yi[K];
+                        X.load(i, xr, xi);
+                        Y.load(i, yr, yi);
+                        acc_hdot<K, CX>(red.h[0], xr, xi, yr, yi);
+                      });
+  else
+    rows<K, CX, 0, 1>(n, nullptr, part, st,
+                      [=] __device__(long long i, Red<K, CX, 0, 1> &red) {
+                        double xr[K], xi[K];
+                        X.load(i, xr, xi);
+                        acc_sumsq<K, CX>(red.nr[0], xr, xi);
+                      });
+  unit_fin_kernel<K, CX><<<1, kBlock, 0, st>>>(part, grid_for(n), op, out);
+  cudaMemcpyAsync(h_out, out, sizeof(double) * 8, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(part);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+int unit_reduce(int k, bool cx, int op, long long n, const double *d_x,
+                const double *d_y, double *h_out, cudaStream_t st) {
+#define DISPATCH(KK)                                                 \
+  if (k == KK)                                                       \
+    return cx ? reduce_typed<KK, true>(op, n, d_x, d_y, h_out, st)   \
+              : reduce_typed<KK, false>(op, n, d_x, d_y, h_out, st);
+  DISPATCH(2)
+  DISPATCH(3)
+  DISPATCH(4)
+#undef DISPATCH
+  return 3;
+}
+
+template <int K, bool CX>
+static int axpy_typed(long long n, const double *are, const double *aim,
+                      const double *d_x, const double *d_y, double *d_out,
+                      cudaStream_t st) {
+  const long long L = plane_ld(n);
+  const MV<K, CX> X{const_cast<double *>(d_x), L},
+      Y{const_cast<double *>(d_y), L}, O{d_out, L};
+  Sc al = sc_zero();
+  for (int c = 0; c < K; ++c) {
+    al.re[c] = are[c];
+    al.im[c] = aim ? aim[c] : 0.0;
+  }
+  rows<K, CX, 0, 0>(n, nullptr, nullptr, st,
+                    [=] __device__(long long i, Red<K, CX, 0, 0> &) {
+                      double xr[K], xi[K], yr[K], yi[K], orr[K], oi[K];
+                      X.load(i, xr, xi);
+                      Y.load(i, yr, yi);
+                      e_axpy<K, CX>(al, xr, xi, yr, yi, orr, oi);
+                      O.store(i, orr, oi);
+                    });
+  return 0;
+}
+
+int unit_axpy(int k, bool cx, long long n, const double *alpha_re,
+              const double *alpha_im, const double *d_x, const double *d_y,
+              double *d_out, cudaStream_t st) {
+#define DISPATCH(KK)                                                        \
+  if (k == KK)                                                              \
+    return cx ? axpy_typed<KK, true>(n, alpha_re, alpha_im, d_x, d_y, d_out, \
+                                     st)                                    \
+              : axpy_typed<KK, false>(n, alpha_re, alpha_im, d_x, d_y,      \
+                                      d_out, st);
+  DISPATCH(2)
+  DISPATCH(3)
+  DISPATCH(4)
+#undef DISPATCH
+  return 3;
+}
+
+// element-wise MC ops on (n,k) AoS arrays (twin tests)
+template <int K>
+__host__ __device__ void mc_op_one(int op, const double *ar, const double *ai,
+                                   const double *br, const double *bi,
+                                   double *orr, double *oi) {
+  double a[K], b[K], c[K], d[K], o[K], o2[K];
+  for (int q = 0; q < K; ++q) {
+    a[q] = ar[q];
+    b[q] = br ? br[q] : 0.0;
+    c[q] = ai ? ai[q] : 0.0;
+    d[q] = bi ? bi[q] : 0.0;
+    o[q] = o2[q] = 0.0;
+  }
+  switch (op) {
+    case 0: add<K>(a, b, o); break;
+    case 1: sub<K>(a, b, o); break;
+    case 2: mul<K>(a, b, o); break;
+    case 3: div<K>(a, b, o); break;
+    case 4: sqrt_mc<K>(a, o); break;
+    case 5: cmul<K>(a, c, b, d, o, o2); break;
+    case 6: cdiv<K>(a, c, b, d, o, o2); break;
+    case 7: {
+      double t[7];
+      for (int q = 0; q < 7; ++q) t[q] = ar[q];
+      renorm<7, K>(t, o);
+      break;
+    }
+    case 8: mul_lf<K>(a[0], b, o); break;
+    case 9: mul_rf<K>(a, b[0], o); break;
+    case 10: {
+      double h, l;
+      mul_ff2(a[0], b[0], h, l);
+      o[0] = h;
+      o[1] = l;
+      break;
+    }
+    default: break;
+  }
+  for (int q = 0; q < K; ++q) {
+    orr[q] = o[q];
+    if (oi) oi[q] = o2[q];
+  }
+}
+
+template <int K>
+__global__ void mc_kernel(int op, long long n, const double *ar,
+                          const double *ai, const double *br,
+                          const double *bi, double *orr, double *oi) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int sa = (op == 7) ? 7 : K;
+  mc_op_one<K>(op, ar + i * sa, ai ? ai + i * K : nullptr,
+               br ? br + i * K : nullptr, bi ? bi + i * K : nullptr,
+               orr + i * K, oi ? oi + i * K : nullptr);
+}
+
+int unit_mc(int op, int k, const double *a_re, const double *a_im,
+            const double *b_re, const double *b_im, double *o_re,
+            double *o_im, int n, cudaStream_t st) {
+  const int g = (n + 127) / 128;
+  if (n <= 0) return 0;
+  switch (k) {
+    case 2: mc_kernel<2><<<g, 128, 0, st>>>(op, n, a_re, a_im, b_re, b_im, o_re, o_im); break;
+    case 3: mc_kernel<3><<<g, 128, 0, st>>>(op, n, a_re, a_im, b_re, b_im, o_re, o_im); break;
+    case 4: mc_kernel<4><<<g, 128, 0, st>>>(op, n, a_re, a_im, b_re, b_im, o_re, o_im); break;
+    default: return 3;
+  }
+  return 0;
+}
+
+int host_mc(int op, int k, const double *a_re, const double *a_im,
+            const double *b_re, const double *b_im, double *o_re,
+            double *o_im) {
+  switch (k) {
+    case 1: {
+      // k = 1 degenerates to native binary64 (multicomponent.py:31-66)
+      double o = 0.0;
+      switch (op) {
+        case 0: o = dadd(a_re[0], b_re[0]); break;
+        case 1: o = dsub(a_re[0], b_re[0]); break;
+        case 2: o = dmul(a_re[0], b_re[0]); break;
+        case 3: {
+          const double x[1] = {a_re[0]}, y[1] = {b_re[0]};
+          double q[1];
+          div<1>(x, y, q);
+          o = q[0];
+          break;
+        }
+        case 4: {
+          const double x[1] = {a_re[0]};
+          double q[1];
+          sqrt_mc<1>(x, q);
+          o = q[0];
+          break;
+        }
+        default: return 3;
+      }
+      o_re[0] = o;
+      return 0;
+    }
+    case 2: mc_op_one<2>(op, a_re, a_im, b_re, b_im, o_re, o_im); return 0;
+    case 3: mc_op_one<3>(op, a_re, a_im, b_re, b_im, o_re, o_im); return 0;
+    case 4: mc_op_one<4>(op, a_re, a_im, b_re, b_im, o_re, o_im); return 0;
+    default: return 3;
+  }
+}
+
+// (n,k) AoS <-> planar
+__global__ void to_planar_kernel(long long n, int k, const double *re,
+                                 const double *im, double *dev, long long L) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int c = 0; c < k; ++c) {
+    dev[c * L + i] = re[i * k + c];
+    if (im) dev[(k + c) * L + i] = im[i * k + c];
+  }
+}
+__global__ void from_planar_kernel(long long n, int k, const double *dev,
+                                   long long L, double *re, double *im) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int c = 0; c < k; ++c) {
+    re[i * k + c] = dev[c * L + i];
+    if (im) im[i * k + c] = dev[(k + c) * L + i];
+  }
+}
+void launch_to_planar(long long n, int k, const double *re, const double *im,
+                      double *dev, cudaStream_t st) {
+  if (n <= 0) return;
+  to_planar_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      n, k, re, im, dev, plane_ld(n));
+}
+void launch_from_planar(long long n, int k, const double *dev, double *re,
+                        double *im, cudaStream_t st) {
+  if (n <= 0) return;
+  from_planar_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      n, k, dev, plane_ld(n), re, im);
+}
+
+}  // namespace mpk

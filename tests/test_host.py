@@ -1,0 +1,125 @@
+"""CPU-side checks of the product: the C-ABI library loads and exports the
+header's symbols, host MC scalar arithmetic is bitwise the reference's,
+the problem generators reproduce the inputs the golden runs used, and
+the drop-in API validates like the reference (ValueError paths)."""
+
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, bits_equal, golden
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2504_14498_b200 import _lib
+
+    L = _lib.lib()
+    hdr = (ROOT / "include" / "mpk_b200.h").read_text()
+    declared = set(re.findall(r"\b(mpk_[a-z0-9_]+)\s*\(", hdr))
+    assert declared == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def test_library_is_sm100a():
+    so = ROOT / "paper_2504_14498_b200" / "_lib" / "libmpkb200.so"
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(so)],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_host_mc_scalars_bitwise(k):
+    import paper_2504_14498_b200 as mpk
+
+    g = golden("mc_ops.npz")
+    P = mpk.Precision.from_k(k)
+    a, b = g[f"k{k}_a"][:120], g[f"k{k}_b"][:120]
+    for i in range(len(a)):
+        x, y = mpk.MCFloat(tuple(a[i])), mpk.MCFloat(tuple(b[i]))
+        assert bits_equal((x + y).components, g[f"k{k}_add"][i])
+        assert bits_equal((x - y).components, g[f"k{k}_sub"][i])
+        assert bits_equal((x * y).components, g[f"k{k}_mul"][i])
+    idx = g[f"k{k}_div_idx"][:60]
+    for j, i in enumerate(idx):
+        q = mpk.MCFloat(tuple(g[f"k{k}_a"][i])) / mpk.MCFloat(tuple(g[f"k{k}_b"][i]))
+        assert bits_equal(q.components, g[f"k{k}_div"][j])
+    for i in range(40):
+        s = mpk.MCFloat(tuple(g[f"k{k}_sqrt_in"][i])).sqrt()
+        assert bits_equal(s.components, g[f"k{k}_sqrt"][i])
+    for i in range(40):
+        za = mpk.MCComplex(mpk.MCFloat(tuple(g[f"k{k}_car"][i])),
+                           mpk.MCFloat(tuple(g[f"k{k}_cai"][i])))
+        zb = mpk.MCComplex(mpk.MCFloat(tuple(g[f"k{k}_cbr"][i])),
+                           mpk.MCFloat(tuple(g[f"k{k}_cbi"][i])))
+        m = za * zb
+        d = za / zb
+        assert bits_equal(m.re.components, g[f"k{k}_cmul_re"][i])
+        assert bits_equal(m.im.components, g[f"k{k}_cmul_im"][i])
+        assert bits_equal(d.re.components, g[f"k{k}_cdiv_re"][i])
+        assert bits_equal(d.im.components, g[f"k{k}_cdiv_im"][i])
+    assert P.k == k
+
+
+def test_problem_generators_match_golden_inputs():
+    from paper_2504_14498_b200 import problems
+
+    assert problems.cfg1().checksum() == str(golden("solver_cfg1.npz")["cfg1_checksum"])
+    assert problems.cfg2().checksum() == str(golden("solver_cfg2.npz")["cfg2_checksum"])
+    assert problems.cfg3().checksum() == str(golden("solver_cfg3.npz")["cfg3_checksum"])
+    assert problems.cfg5(0).checksum() == str(golden("solver_cfg5.npz")["cfg5_0_checksum"])
+
+
+def test_cfg_shapes():
+    from paper_2504_14498_b200 import problems
+
+    p1 = problems.cfg1()
+    assert (p1.n, p1.nnz) == (4096, 20224)
+    p3 = problems.cfg3(m=48)
+    assert (p3.n, p3.nnz) == (110592, 760320)
+    p4 = problems.cfg4(m=64)  # full size is exercised by bench.py
+    assert p4.nnz == (3 * 64 - 2) ** 2
+    p2 = problems.cfg2()
+    assert p2.n == 20000 and 250_000 < p2.nnz < 270_000
+    # strictly increasing columns, diagonal present in every row
+    for p in (p1, p2, p3):
+        rp, ci = p.row_ptr, p.col_idx
+        row = np.repeat(np.arange(p.n), np.diff(rp))
+        assert np.all((np.diff(ci) > 0) | (np.diff(row) > 0))
+        assert np.count_nonzero(ci == row) == p.n
+
+
+def test_api_validation_errors():
+    import paper_2504_14498_b200 as mpk
+
+    P = mpk.Precision.DD
+    with pytest.raises(ValueError, match="unknown method"):
+        mpk.SolverConfig(method="gmres")
+    with pytest.raises(ValueError, match="mixed SpMV needs"):
+        mpk.SolverConfig(precision=mpk.Precision.F64, spmv_mode="mixed")
+    with pytest.raises(ValueError, match="eps_rel"):
+        mpk.SolverConfig(eps_rel=0.0)
+    with pytest.raises(ValueError, match="strictly increasing"):
+        mpk.CsrMatrix(2, np.array([0, 2, 3]), np.array([1, 0, 1]),
+                      np.ones((3, 2)), None, P)
+    with pytest.raises(ValueError, match="row_ptr"):
+        mpk.CsrMatrix(2, np.array([0, 2, 2]), np.array([0, 1, 1]),
+                      np.ones((3, 2)), None, P)
+    assert mpk.PrecondMode.from_label("ilu0-mixed") is mpk.PrecondMode.ILU0_MIXED
+    assert mpk.Precision.from_label("qd").k == 4
+
+
+def test_product_does_not_import_oracle():
+    pkg = ROOT / "paper_2504_14498_b200"
+    for f in pkg.rglob("*.py"):
+        txt = f.read_text()
+        assert "import oracle" not in txt and "from oracle" not in txt, f
+    for f in list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
+        assert "mpk_oracle" not in f.read_text(), f

@@ -1,0 +1,200 @@
+"""Pin the C oracle (oracle/mpk_oracle.c) to the reference's own outputs.
+
+Every comparison here is BITWISE (sign of zero included) against golden
+vectors produced by running the unmodified reference
+(tests/golden/make_golden.py).  These mirror the reference's test
+strategy one layer down: twin element ops (tests/test_twins.py:24-74),
+SpMV / adjoint / mixed-vs-promoted (tests/test_sparse.py:66-147), plus
+what the reference never pinned: ILU(0) factors and sweeps and whole
+solver runs.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal, golden
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_mc_ops_bitwise(orc, k):
+    g = golden("mc_ops.npz")
+    a, b = g[f"k{k}_a"], g[f"k{k}_b"]
+    for op in ("add", "sub", "mul"):
+        assert bits_equal(orc.mc_op(op, a, b), g[f"k{k}_{op}"]), op
+    idx = g[f"k{k}_div_idx"]
+    assert bits_equal(orc.mc_op("div", a[idx], b[idx]), g[f"k{k}_div"])
+    assert bits_equal(orc.mc_op("sqrt", g[f"k{k}_sqrt_in"]), g[f"k{k}_sqrt"])
+    assert bits_equal(orc.renorm(g[f"k{k}_renorm_in"], k), g[f"k{k}_renorm"])
+    re, im = orc.mc_op("cmul", g[f"k{k}_car"], g[f"k{k}_cbr"], g[f"k{k}_cai"],
+                       g[f"k{k}_cbi"])
+    assert bits_equal(re, g[f"k{k}_cmul_re"]) and bits_equal(im, g[f"k{k}_cmul_im"])
+    re, im = orc.mc_op("cdiv", g[f"k{k}_car"], g[f"k{k}_cbr"], g[f"k{k}_cai"],
+                       g[f"k{k}_cbi"])
+    assert bits_equal(re, g[f"k{k}_cdiv_re"]) and bits_equal(im, g[f"k{k}_cdiv_im"])
+    f, x, gg = g[f"k{k}_f"], g[f"k{k}_x"], g[f"k{k}_g"]
+    fz = np.zeros_like(x)
+    fz[:, 0] = f
+    gz = np.zeros_like(x)
+    gz[:, 0] = gg
+    assert bits_equal(orc.mc_op("mul", fz, x), g[f"k{k}_mul_lf"])
+    assert bits_equal(orc.mc_op("mul", x, fz), g[f"k{k}_mul_rf"])
+    assert bits_equal(orc.mc_op("mul", fz, gz), g[f"k{k}_mul_ff"])
+
+
+@pytest.mark.parametrize("field", ["r", "c"])
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_sparse_kernels_bitwise(orc, field, k):
+    g = golden("sparse_small.npz")
+    cx = field == "c"
+    rp, ci, vre = g[f"{field}_rp"], g[f"{field}_ci"], g[f"{field}_vre"]
+    vim = g[f"{field}_vim"] if cx else None
+    n = len(rp) - 1
+    t = f"{field}{k}"
+    xre, yre = g[f"{t}_xre"], g[f"{t}_yre"]
+    xim = g[f"{t}_xim"] if cx else None
+    yim = g[f"{t}_yim"] if cx else None
+    yr, yi = orc.spmv_mixed(n, rp, ci, vre, vim, xre, xim)
+    assert bits_equal(yr, g[f"{t}_spmv_re"])
+    if cx:
+        assert bits_equal(yi, g[f"{t}_spmv_im"])
+    ar, ai = orc.spmv_mixed(n, rp, ci, vre, vim, xre, xim, adjoint=True)
+    assert bits_equal(ar, g[f"{t}_adj_re"])
+    if cx:
+        assert bits_equal(ai, g[f"{t}_adj_im"])
+    xf = np.zeros_like(xre)
+    xf[:, 0] = xre[:, 0]
+    xfi = None
+    if cx:
+        c = xre[:, 0] + 1j * xim[:, 0]
+        xf[:, 0] = c.real
+        xfi = np.zeros_like(xre)
+        xfi[:, 0] = c.imag
+    fr, fi = orc.spmv_mixed(n, rp, ci, vre, vim, xf, xfi)
+    assert bits_equal(fr, g[f"{t}_spmvf_re"])
+    if cx:
+        assert bits_equal(fi, g[f"{t}_spmvf_im"])
+    hr, hi = orc.hdot(xre, yre, xim, yim)
+    assert bits_equal(hr, g[f"{t}_hdot_re"])
+    if cx:
+        assert bits_equal(hi, g[f"{t}_hdot_im"])
+    assert bits_equal(orc.norm2(xre, xim), g[f"{t}_norm2"])
+    o_re, o_im = orc.axpy(g[f"{t}_alpha_re"], xre, yre,
+                          g[f"{t}_alpha_im"] if cx else None, xim, yim)
+    assert bits_equal(o_re, g[f"{t}_axpy_re"])
+    if cx:
+        assert bits_equal(o_im, g[f"{t}_axpy_im"])
+
+
+@pytest.mark.parametrize("tag", ["tri3", "rnd_r", "rnd_c", "cfg1"])
+def test_ilu0_factor_and_apply_bitwise(orc, tag):
+    g = golden("ilu_small.npz")
+    rp, ci = g[f"{tag}_rp"], g[f"{tag}_ci"]
+    n = len(rp) - 1
+    cx = f"{tag}_vim" in g.files
+    vim = g[f"{tag}_vim"] if cx else None
+    rc, lre, lim, _, _ = orc.ilu0_factor(n, rp, ci, g[f"{tag}_vre"], vim)
+    assert rc == 0
+    assert bits_equal(lre, g[f"{tag}_lu_re"])
+    if cx:
+        assert bits_equal(lim, g[f"{tag}_lu_im"])
+    for k in (2, 4):
+        r_re = g[f"{tag}_k{k}_r_re"]
+        r_im = g[f"{tag}_k{k}_r_im"] if cx else None
+        for adj, key in ((False, "z"), (True, "za")):
+            rc, zr, zi = orc.ilu0_apply_mixed(n, rp, ci, lre, lim, r_re, r_im, adjoint=adj)
+            assert rc == 0
+            assert bits_equal(zr, g[f"{tag}_k{k}_{key}_re"]), (k, key)
+            if cx:
+                assert bits_equal(zi, g[f"{tag}_k{k}_{key}_im"]), (k, key)
+
+
+def test_spec_tridiagonal_known_answer(orc):
+    """SPEC.md:267-268,276-277 known answers."""
+    g = golden("ilu_small.npz")
+    rp, ci = g["tri3_rp"], g["tri3_ci"]
+    rc, lre, _, _, _ = orc.ilu0_factor(3, rp, ci, g["tri3_vre"])
+    assert rc == 0
+    assert list(lre) == [2.0, -1.0, -0.5, 1.5, -1.0, -0.6666666666666666,
+                         1.3333333333333335]
+    rc, z, _ = orc.ilu0_apply_f64(3, rp, ci, lre, None, np.array([1.0, 0.0, 1.0]))
+    assert list(z) == [1.0, 1.0, 0.9999999999999999]
+
+
+def test_zero_pivot_row(orc):
+    g = golden("ilu_small.npz")
+    rc, _, _, bad, structural = orc.ilu0_factor(3, g["zp_rp"], g["zp_ci"], g["zp_vre"])
+    assert rc == 1 and structural == 0
+    assert bad == int(g["zero_pivot_row"])
+
+
+def _check_run(orc, rep, hist, x_re, x_im, g, pre, cx):
+    assert rep.iterations == int(g[f"{pre}_iterations"])
+    assert bool(rep.converged) == bool(g[f"{pre}_converged"])
+    bd = orc.BREAKDOWN[rep.breakdown]
+    assert (bd or "") == str(g[f"{pre}_breakdown"]).split(":")[0]
+    assert bits_equal(hist, g[f"{pre}_hist"])
+    assert bits_equal(np.array(rep.final_recursive_relres),
+                      g[f"{pre}_final_recursive_relres"])
+    assert bits_equal(np.array(rep.true_relres), g[f"{pre}_true_relres"])
+    if f"{pre}_x_re" in g.files:
+        assert bits_equal(x_re, g[f"{pre}_x_re"])
+        if cx:
+            assert bits_equal(x_im, g[f"{pre}_x_im"])
+
+
+@pytest.mark.parametrize("field", ["r", "c"])
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("method", ["bicg", "cgs", "bicgstab", "gpbicg"])
+def test_solver_small_bitwise(orc, field, k, method):
+    g = golden("solver_small.npz")
+    cx = field == "c"
+    rp, ci = g[f"{field}_rp"], g[f"{field}_ci"]
+    n = len(rp) - 1
+    tol = {2: 1e-25, 3: 1e-40, 4: 1e-55}[k]
+    rep, xr, xi, hist = orc.solve(n, rp, ci, g[f"{field}_vre"],
+                                  g[f"{field}_vim"] if cx else None, method, k,
+                                  g[f"{field}{k}_b_re"],
+                                  g[f"{field}{k}_b_im"] if cx else None,
+                                  eps_rel=tol, eps_abs=1e-100)
+    _check_run(orc, rep, hist, xr, xi, g, f"{field}{k}_{method}", cx)
+
+
+def _cfg_fixture(name):
+    return golden(name)
+
+
+def test_cfg1_dd_bicgstab_bitwise(orc):
+    from paper_2504_14498_b200 import problems
+
+    g = _cfg_fixture("solver_cfg1.npz")
+    p = problems.cfg1()
+    assert p.checksum() == str(g["cfg1_checksum"])
+    b = np.zeros((p.n, 2))
+    b[:, 0] = p.x_true
+    b_re, _ = orc.spmv_mixed(p.n, p.row_ptr, p.col_idx, p.val_re, None, b)
+    assert bits_equal(b_re, g["cfg1_b_re"])
+    rep, xr, xi, hist = orc.solve(p.n, p.row_ptr, p.col_idx, p.val_re, None,
+                                  "bicgstab", 2, b_re, eps_rel=p.eps_rel,
+                                  max_iter=p.max_iter)
+    _check_run(orc, rep, hist, xr, xi, g, "cfg1_bicgstab_dd", False)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("method", ["bicg", "cgs", "bicgstab", "gpbicg"])
+@pytest.mark.parametrize("lab", ["td", "qd"])
+def test_cfg2_bitwise(orc, method, lab):
+    from paper_2504_14498_b200 import problems
+
+    g = _cfg_fixture("solver_cfg2.npz")
+    p = problems.cfg2()
+    assert p.checksum() == str(g["cfg2_checksum"])
+    k = {"td": 3, "qd": 4}[lab]
+    x = np.zeros((p.n, k))
+    x[:, 0] = p.x_true
+    b_re, _ = orc.spmv_mixed(p.n, p.row_ptr, p.col_idx, p.val_re, None, x)
+    assert bits_equal(b_re[:64], g[f"cfg2_{lab}_b_head"])
+    rep, xr, xi, hist = orc.solve(p.n, p.row_ptr, p.col_idx, p.val_re, None, method,
+                                  k, b_re, eps_rel=p.eps_rel, max_iter=p.max_iter)
+    _check_run(orc, rep, hist, xr, xi, g, f"cfg2_{method}_{lab}", False)
