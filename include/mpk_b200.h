@@ -66,6 +66,7 @@ typedef struct {
   double factor_ms;       /* device time of the ILU(0) factorization */
   double solve_ms;        /* device time of the Krylov loop */
   double total_ms;        /* host wall time of the whole call */
+  int64_t launches;       /* kernels executed by the call */
 } mpk_report;
 
 const char *mpk_last_error(void);
@@ -75,6 +76,8 @@ int mpk_version(void);
 int mpk_ctx_create(int device, mpk_ctx **out);
 void mpk_ctx_destroy(mpk_ctx *ctx);
 int mpk_ctx_synchronize(mpk_ctx *ctx);
+/* the context's cudaStream_t (for event timing by the caller) */
+void *mpk_ctx_stream(mpk_ctx *ctx);
 
 /* CsrMatrix.demoted() upload (sparse.py:192-249): binary64 values, val_im
  * NULL for the real field.  Columns must be strictly increasing per row. */
@@ -154,6 +157,11 @@ int mpk_to_planar(mpk_ctx *ctx, int64_t n, int k, const double *re,
                   const double *im, double *dev);
 int mpk_from_planar(mpk_ctx *ctx, int64_t n, int k, const double *dev,
                     double *re, double *im, int cx);
+
+/* Kernel probe for the roofline: average device time (CUDA events on the
+ * context stream) of one ILU(0)-mixed apply (forward + backward sweep
+ * kernel) of a k-component input, over reps launches.  Needs factors. */
+int mpk_bench_apply(mpk_matrix *m, int k, int reps, double *ms_avg);
 
 /* Independent systems (cfg5 batch): matrices[i] already uploaded, each
  * solved on its own stream of the context's device.  b/x host (n_i,k). */

@@ -46,7 +46,7 @@ EXPORTS = (
     "mpk_ilu0_download", "mpk_ilu0_apply_f64", "mpk_ilu0_apply_mixed",
     "mpk_spmv_mixed", "mpk_hdot", "mpk_norm2", "mpk_axpy", "mpk_mc_elementwise",
     "mpk_mc_host", "mpk_solve", "mpk_plane_ld", "mpk_solve_dev", "mpk_to_planar",
-    "mpk_from_planar", "mpk_solve_batch",
+    "mpk_from_planar", "mpk_solve_batch", "mpk_ctx_stream", "mpk_bench_apply",
 )
 
 
@@ -64,6 +64,7 @@ class MpkReport(ctypes.Structure):
         ("factor_ms", ctypes.c_double),
         ("solve_ms", ctypes.c_double),
         ("total_ms", ctypes.c_double),
+        ("launches", ctypes.c_int64),
     ]
 
 

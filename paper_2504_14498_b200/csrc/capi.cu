@@ -82,6 +82,37 @@ void gather(const double *src, const int *perm, double *dst, long long m,
                                                               m, cx ? 1 : 0);
 }
 
+// Level order of a triangular dependency DAG: rows are visited in `visit`
+// order (every dependency visited first), level(i) = 1 + max level of its
+// dependencies deps[dlo(i) .. dhi(i)); returns the rows sorted by level
+// (stable), i.e. a topological order whose warps hold independent rows.
+template <class Lo, class Hi>
+static int level_order(int n, bool descending, const int *deps, Lo dlo, Hi dhi,
+                       std::vector<int> &ord, std::vector<int> &ptr) {
+  std::vector<int> lev(n, 0);
+  int nlev = 0;
+  for (int s = 0; s < n; ++s) {
+    const int i = descending ? n - 1 - s : s;
+    int l = 0;
+    for (int p = dlo(i); p < dhi(i); ++p) {
+      const int d = lev[deps[p]] + 1;
+      if (d > l) l = d;
+    }
+    lev[i] = l;
+    if (l + 1 > nlev) nlev = l + 1;
+  }
+  std::vector<int> cnt(nlev + 1, 0);
+  for (int i = 0; i < n; ++i) cnt[lev[i] + 1]++;
+  for (int l = 0; l < nlev; ++l) cnt[l + 1] += cnt[l];
+  ptr = cnt;
+  ord.assign(n, 0);
+  for (int s = 0; s < n; ++s) {
+    const int i = descending ? n - 1 - s : s;
+    ord[cnt[lev[i]]++] = i;
+  }
+  return nlev;
+}
+
 }  // namespace
 
 namespace mpk {
@@ -135,6 +166,17 @@ void ensure_adjoint(DMat &A, cudaStream_t st) {
     upload(&A.lt_rp, lcnt, st);
     upload(&A.lt_ci, lt_ci, st);
     upload(&A.lt_perm, lt_perm, st);
+    std::vector<int> of, ob, pf, pb;
+    A.levels_fa = level_order(
+        n, false, ut_ci.data(), [&](int c) { return ucnt[c]; },
+        [&](int c) { return ucnt[c + 1]; }, of, pf);
+    A.levels_ba = level_order(
+        n, true, lt_ci.data(), [&](int c) { return lcnt[c]; },
+        [&](int c) { return lcnt[c + 1]; }, ob, pb);
+    upload(&A.ord_fa, of, st);
+    upload(&A.ord_ba, ob, st);
+    upload(&A.lev_fa, pf, st);
+    upload(&A.lev_ba, pb, st);
     const size_t w = cx ? 2 : 1;
     cudaMalloc(&A.at_val, sizeof(double) * w * (A.nnz ? A.nnz : 1));
     cudaMalloc(&A.ut_val, sizeof(double) * w * (ut_ci.size() + 1));
@@ -183,6 +225,8 @@ int mpk_ctx_synchronize(mpk_ctx *ctx) {
   return MPK_OK;
 }
 
+void *mpk_ctx_stream(mpk_ctx *ctx) { return (void *)ctx->stream; }
+
 int64_t mpk_plane_ld(int64_t n) { return plane_ld(n); }
 
 int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
@@ -223,8 +267,23 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
     for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
       if (col_idx[p] == i) A.h_dp[i] = (int)p;
   cudaStream_t st = ctx->stream;
+  // level orders of the L (forward) and U (backward) DAGs; a missing
+  // diagonal (dp = -1) only matters for the structural check at factor time
+  std::vector<int> of, ob, pf, pb;
+  {
+    const int *rp = A.h_rp.data(), *dp = A.h_dp.data();
+    A.levels_f = level_order(
+        (int)n, false, A.h_ci.data(), [&](int i) { return rp[i]; },
+        [&](int i) { return dp[i] < 0 ? rp[i] : dp[i]; }, of, pf);
+    A.levels_b = level_order(
+        (int)n, true, A.h_ci.data(),
+        [&](int i) { return dp[i] < 0 ? rp[i + 1] : dp[i] + 1; },
+        [&](int i) { return rp[i + 1]; }, ob, pb);
+  }
   if (upload(&A.rp, A.h_rp, st) || upload(&A.ci, A.h_ci, st) ||
-      upload(&A.dp, A.h_dp, st)) {
+      upload(&A.dp, A.h_dp, st) || upload(&A.ord_f, of, st) ||
+      upload(&A.ord_b, ob, st) || upload(&A.lev_f, pf, st) ||
+      upload(&A.lev_b, pb, st)) {
     delete m;
     return fail(MPK_CUDA_ERROR, "allocation failed");
   }
@@ -265,6 +324,8 @@ void mpk_csr_free(mpk_matrix *m) {
                   A.at_rp,  A.at_ci,  A.at_perm, A.at_val, A.ut_rp,
                   A.ut_ci,  A.ut_perm, A.lt_rp,  A.lt_ci,  A.lt_perm,
                   A.ut_val, A.lt_val, A.sw_y,    A.sw_y2,  A.tick,
+                  A.ord_f,  A.ord_b,  A.ord_fa,  A.ord_ba,
+                  A.lev_f,  A.lev_b,  A.lev_fa,  A.lev_ba,
                   A.err,    m->rowflag, m->fscratch};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -300,6 +361,9 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   fa.dp = A.dp;
   fa.lu = A.lu;
   fa.rowflag = m->rowflag;
+  fa.ord = A.ord_f;
+  fa.lev = A.lev_f;
+  fa.nlev = A.levels_f;
   fa.tick = m->fscratch;
   fa.bad_row = m->fscratch + 2;
   fa.nonfinite = m->fscratch + 3;
@@ -371,6 +435,12 @@ static int apply_dev(mpk_matrix *m, int k, const double *in_mc, double *fz,
   a.lt_rp = A.lt_rp;
   a.lt_ci = A.lt_ci;
   a.lt_val = A.lt_val;
+  a.ord_f = adjoint ? A.ord_fa : A.ord_f;
+  a.ord_b = adjoint ? A.ord_ba : A.ord_b;
+  a.lev_f = adjoint ? A.lev_fa : A.lev_f;
+  a.lev_b = adjoint ? A.lev_ba : A.lev_b;
+  a.nlev_f = adjoint ? A.levels_fa : A.levels_f;
+  a.nlev_b = adjoint ? A.levels_ba : A.levels_b;
   a.in_re = in_mc;
   a.in_im = A.cx ? in_mc + (long long)k * L : nullptr;
   a.y = A.sw_y;
@@ -651,6 +721,63 @@ static void fill_report(mpk_report *rep, const SolveOut &o, float factor_ms) {
   rep->solve_ms = o.loop_ms;
 }
 
+int mpk_bench_apply(mpk_matrix *m, int k, int reps, double *ms_avg) {
+  DMat &A = m->A;
+  if (!A.factored) return fail(MPK_INVALID, "matrix is not factored");
+  if (k < 1 || k > 4 || reps < 1) return fail(MPK_INVALID, "bad k/reps");
+  CKR(cudaSetDevice(m->ctx->device));
+  cudaStream_t st = m->ctx->stream;
+  const long long L = plane_ld(A.n);
+  double *din = nullptr, *dz = nullptr;
+  const size_t planes = (size_t)k * (A.cx ? 2 : 1);
+  CKR(cudaMalloc(&din, sizeof(double) * planes * L));
+  CKR(cudaMalloc(&dz, sizeof(double) * 2 * L));
+  // input: the matrix values reused as a deterministic right-hand side head
+  CKR(cudaMemsetAsync(din, 0, sizeof(double) * planes * L, st));
+  CKR(cudaMemcpyAsync(din, A.val, sizeof(double) * (A.n < A.nnz ? A.n : A.nnz),
+                      cudaMemcpyDeviceToDevice, st));
+  SweepArgs a{};
+  a.n = A.n;
+  a.rp = A.rp;
+  a.ci = A.ci;
+  a.dp = A.dp;
+  a.lu = A.lu;
+  a.ord_f = A.ord_f;
+  a.ord_b = A.ord_b;
+  a.lev_f = A.lev_f;
+  a.lev_b = A.lev_b;
+  a.nlev_f = A.levels_f;
+  a.nlev_b = A.levels_b;
+  a.in_re = din;
+  a.in_im = A.cx ? din + (long long)k * L : nullptr;
+  a.y = A.sw_y;
+  a.z = dz;
+  a.tick = A.tick;
+  a.err = A.err;
+  a.done = nullptr;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double tot = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    launch_sweep_reset(A.sw_y, dz, A.n, A.cx, nullptr, st);
+    cudaEventRecord(e0, st);
+    launch_sweep(a, A.cx, false, st);
+    cudaEventRecord(e1, st);
+    CKR(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    tot += ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(din);
+  cudaFree(dz);
+  CKR(cudaGetLastError());
+  *ms_avg = tot / reps;
+  return MPK_OK;
+}
+
 static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
                       double eps_abs, int64_t max_iter, const double *d_b,
                       double *d_x, double *d_hist, int64_t hist_cap,
@@ -701,12 +828,14 @@ int mpk_solve_dev(mpk_matrix *m, int method, int k, double eps_rel,
                   double *x_dev, double *hist_dev, int64_t hist_cap,
                   mpk_report *rep) {
   const auto t0 = std::chrono::steady_clock::now();
+  const long long l0 = tl_launches;
   CKR(cudaSetDevice(m->ctx->device));
   int rc = solve_core(m, method, k, eps_rel, eps_abs, max_iter, b_dev, x_dev,
                       hist_dev, hist_cap, rep);
   rep->total_ms = std::chrono::duration<double, std::milli>(
                       std::chrono::steady_clock::now() - t0)
                       .count();
+  rep->launches = tl_launches - l0;
   return rc;
 }
 
@@ -715,6 +844,7 @@ int mpk_solve(mpk_matrix *m, int method, int k, double eps_rel,
               const double *b_im, double *x_re, double *x_im, double *hist,
               int64_t hist_cap, mpk_report *rep) {
   const auto t0 = std::chrono::steady_clock::now();
+  const long long l0 = tl_launches;
   DMat &A = m->A;
   if (A.cx != (b_im != nullptr))
     return fail(MPK_INVALID, "matrix/vector field mismatch");
@@ -742,6 +872,7 @@ int mpk_solve(mpk_matrix *m, int method, int k, double eps_rel,
   rep->total_ms = std::chrono::duration<double, std::milli>(
                       std::chrono::steady_clock::now() - t0)
                       .count();
+  rep->launches = tl_launches - l0;
   return rc;
 }
 

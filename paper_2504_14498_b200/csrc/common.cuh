@@ -21,6 +21,10 @@ constexpr int kBlock = 256;       // threads per block for streaming kernels
 constexpr int kMaxGrid = 592;     // 4 x 148 SMs: fixed => deterministic trees
 constexpr int kWarpsPerBlock = kBlock / 32;
 
+// Host-side count of kernels launched (or captured) by this thread; the
+// C ABI reports per-call deltas (mpk_report.launches).
+inline thread_local long long tl_launches = 0;
+
 // Sentinel for sync-free triangular sweeps: a signalling NaN payload that no
 // binary64 operation produces (hardware NaNs are quiet).
 constexpr unsigned long long kSentBits = 0x7FF40000DEADBEEFull;
@@ -43,6 +47,18 @@ __device__ __forceinline__ double ld_volatile(const double *p) {
 __device__ __forceinline__ double2 ld_volatile2(const double2 *p) {
   double2 v;
   asm volatile("ld.volatile.global.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_relaxed(const double *p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_relaxed2(const double2 *p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];"
                : "=d"(v.x), "=d"(v.y)
                : "l"(p));
   return v;
@@ -180,21 +196,21 @@ __host__ __device__ __forceinline__ Sc sc_zero() {
 }
 
 template <int K, bool CX>
-__device__ __noinline__ Sc s_add(const Sc &a, const Sc &b) {
+__device__ __noinline__ Sc s_add(Sc a, Sc b) {
   Sc o = sc_zero();
   add<K>(R<K>(a), R<K>(b), R<K>(o));
   if constexpr (CX) add<K>(I<K>(a), I<K>(b), I<K>(o));
   return o;
 }
 template <int K, bool CX>
-__device__ __noinline__ Sc s_sub(const Sc &a, const Sc &b) {
+__device__ __noinline__ Sc s_sub(Sc a, Sc b) {
   Sc o = sc_zero();
   sub<K>(R<K>(a), R<K>(b), R<K>(o));
   if constexpr (CX) sub<K>(I<K>(a), I<K>(b), I<K>(o));
   return o;
 }
 template <int K, bool CX>
-__device__ __noinline__ Sc s_mul(const Sc &a, const Sc &b) {
+__device__ __noinline__ Sc s_mul(Sc a, Sc b) {
   Sc o = sc_zero();
   if constexpr (CX)
     cmul<K>(R<K>(a), I<K>(a), R<K>(b), I<K>(b), R<K>(o), I<K>(o));
@@ -203,7 +219,7 @@ __device__ __noinline__ Sc s_mul(const Sc &a, const Sc &b) {
   return o;
 }
 template <int K, bool CX>
-__device__ __noinline__ Sc s_div(const Sc &a, const Sc &b) {
+__device__ __noinline__ Sc s_div(Sc a, Sc b) {
   Sc o = sc_zero();
   if constexpr (CX)
     cdiv<K>(R<K>(a), I<K>(a), R<K>(b), I<K>(b), R<K>(o), I<K>(o));

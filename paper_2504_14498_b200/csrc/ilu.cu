@@ -1,5 +1,6 @@
 // ilu.cu -- sync-free binary64 ILU(0) factorization and sweeps (see ilu.cuh)
 #include <climits>
+#include <cstdlib>
 
 #include "ilu.cuh"
 
@@ -43,6 +44,8 @@ template <bool CX>
 __device__ void factor_row(const FactorArgs &a, int i) {
   const int lo = a.rp[i], hi = a.rp[i + 1], d = a.dp[i];
   double2 *lu2 = reinterpret_cast<double2 *>(a.lu);
+  // each elimination step waits only for its own pivot row, so the work on
+  // early L entries overlaps the wait for later ones
   for (int t = lo; t < d; ++t) {
     const int kc = a.ci[t];
     while (ld_volatile_i(&a.rowflag[kc]) == 0) __nanosleep(32);
@@ -104,8 +107,8 @@ __global__ void __launch_bounds__(kBlock) factor_kernel(FactorArgs a) {
   for (;;) {
     const int base = grab_ticket(a.tick);
     if (base >= a.n) break;
-    const int i = base + lane;
-    if (i < a.n) factor_row<CX>(a, i);
+    const int t = base + lane;
+    if (t < a.n) factor_row<CX>(a, a.ord ? a.ord[t] : t);
   }
   exit_protocol(a.tick);
 }
@@ -154,16 +157,29 @@ __device__ __forceinline__ void ldval(const double *v, int p, double &r,
   }
 }
 
-template <bool CX>
-__device__ __forceinline__ void pollv(const double *buf, int j, double &r,
+// Loads of values published by other threads of the same kernel: volatile
+// (L1-bypassing, system scope) or relaxed at gpu scope.
+template <bool CX, bool REL>
+__device__ __forceinline__ void ldpub(const double *buf, int j, double &r,
                                       double &m) {
   if constexpr (CX) {
-    const double2 w = poll2(reinterpret_cast<const double2 *>(buf) + j);
+    const double2 *p = reinterpret_cast<const double2 *>(buf) + j;
+    const double2 w = REL ? ld_relaxed2(p) : ld_volatile2(p);
     r = w.x;
     m = w.y;
   } else {
-    r = poll1(buf + j);
+    r = REL ? ld_relaxed(buf + j) : ld_volatile(buf + j);
     m = 0.0;
+  }
+}
+
+template <bool CX, bool REL>
+__device__ __forceinline__ void pollv(const double *buf, int j, double &r,
+                                      double &m) {
+  ldpub<CX, REL>(buf, j, r, m);
+  while (is_sent(r) || (CX && is_sent(m))) {
+    __nanosleep(20);
+    ldpub<CX, REL>(buf, j, r, m);
   }
 }
 
@@ -178,35 +194,59 @@ __device__ __forceinline__ void publish(double *buf, int j, double r,
   }
 }
 
+// acc -= val[q] * buf[col[q]] for q = lo..hi-1 IN ORDER (the reference's
+// per-row accumulation order).  PREF > 1 fetches the dependency values in
+// batches of PREF independent loads before the ordered chain consumes them
+// (a value still carrying the sentinel is re-polled individually).
+template <bool CX, bool CONJ, int PREF, bool REL>
+__device__ __forceinline__ void chain(double &ar, double &ai, const int *col,
+                                      const double *val, const double *buf,
+                                      int lo, int hi) {
+  if constexpr (PREF == 1) {
+    for (int p = lo; p < hi; ++p) {
+      double vr, vi, lr, li;
+      pollv<CX, REL>(buf, col[p], vr, vi);
+      ldval<CX>(val, p, lr, li);
+      mulsub<CX, CONJ>(ar, ai, lr, li, vr, vi);
+    }
+  } else {
+    for (int p0 = lo; p0 < hi; p0 += PREF) {
+      double vr[PREF], vi[PREF];
+#pragma unroll
+      for (int q = 0; q < PREF; ++q) {
+        vr[q] = vi[q] = 0.0;
+        if (p0 + q < hi) ldpub<CX, REL>(buf, col[p0 + q], vr[q], vi[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < PREF; ++q) {
+        if (p0 + q < hi) {
+          if (is_sent(vr[q]) || (CX && is_sent(vi[q])))
+            pollv<CX, REL>(buf, col[p0 + q], vr[q], vi[q]);
+          double lr, li;
+          ldval<CX>(val, p0 + q, lr, li);
+          mulsub<CX, CONJ>(ar, ai, lr, li, vr[q], vi[q]);
+        }
+      }
+    }
+  }
+}
+
 // _sweep_forward ilu.py:322-331
-template <bool CX>
+template <bool CX, int PREF, bool REL>
 __device__ void fwd_row(const SweepArgs &a, int i) {
   double ar, ai;
   load_in<CX>(a, i, ar, ai);
-  const int lo = a.rp[i], d = a.dp[i];
-  for (int p = lo; p < d; ++p) {
-    const int j = a.ci[p];
-    double lr, li, yr, yi;
-    ldval<CX>(a.lu, p, lr, li);
-    pollv<CX>(a.y, j, yr, yi);
-    mulsub<CX, false>(ar, ai, lr, li, yr, yi);
-  }
+  chain<CX, false, PREF, REL>(ar, ai, a.ci, a.lu, a.y, a.rp[i], a.dp[i]);
   publish<CX>(a.y, i, ar, ai);
 }
 
 // _sweep_backward ilu.py:334-343
-template <bool CX>
+template <bool CX, int PREF, bool REL>
 __device__ void bwd_row(const SweepArgs &a, int i) {
   double ar, ai;
-  pollv<CX>(a.y, i, ar, ai);
+  pollv<CX, REL>(a.y, i, ar, ai);
   const int d = a.dp[i], hi = a.rp[i + 1];
-  for (int p = d + 1; p < hi; ++p) {
-    const int j = a.ci[p];
-    double ur, ui, zr, zi;
-    ldval<CX>(a.lu, p, ur, ui);
-    pollv<CX>(a.z, j, zr, zi);
-    mulsub<CX, false>(ar, ai, ur, ui, zr, zi);
-  }
+  chain<CX, false, PREF, REL>(ar, ai, a.ci, a.lu, a.z, d + 1, hi);
   double dr, di, qr, qi;
   ldval<CX>(a.lu, d, dr, di);
   if constexpr (CX) {
@@ -222,18 +262,12 @@ __device__ void bwd_row(const SweepArgs &a, int i) {
 // _sweep_forward_adjoint ilu.py:346-357 in gather form: U^H is lower
 // triangular; the scatter of row j into acc[c] runs in ascending j, so the
 // gather over column c of U visits rows in ascending order.
-template <bool CX>
+template <bool CX, int PREF, bool REL>
 __device__ void fwd_row_adj(const SweepArgs &a, int c) {
   double ar, ai;
   load_in<CX>(a, c, ar, ai);
-  const int lo = a.ut_rp[c], hi = a.ut_rp[c + 1];
-  for (int q = lo; q < hi; ++q) {
-    const int j = a.ut_ci[q];
-    double ur, ui, yr, yi;
-    ldval<CX>(a.ut_val, q, ur, ui);
-    pollv<CX>(a.y, j, yr, yi);
-    mulsub<CX, true>(ar, ai, ur, ui, yr, yi);
-  }
+  chain<CX, true, PREF, REL>(ar, ai, a.ut_ci, a.ut_val, a.y, a.ut_rp[c],
+                             a.ut_rp[c + 1]);
   double dr, di, qr, qi;
   ldval<CX>(a.lu, a.dp[c], dr, di);
   if constexpr (CX) {
@@ -248,23 +282,17 @@ __device__ void fwd_row_adj(const SweepArgs &a, int c) {
 // _sweep_backward_adjoint ilu.py:360-371: L^H unit upper; rows j scatter in
 // DESCENDING order, so the gather over column c of L visits rows j > c in
 // descending order (lt_ci is stored that way).
-template <bool CX>
+template <bool CX, int PREF, bool REL>
 __device__ void bwd_row_adj(const SweepArgs &a, int c) {
   double ar, ai;
-  pollv<CX>(a.y, c, ar, ai);
-  const int lo = a.lt_rp[c], hi = a.lt_rp[c + 1];
-  for (int q = lo; q < hi; ++q) {
-    const int j = a.lt_ci[q];
-    double lr, li, zr, zi;
-    ldval<CX>(a.lt_val, q, lr, li);
-    pollv<CX>(a.z, j, zr, zi);
-    mulsub<CX, true>(ar, ai, lr, li, zr, zi);
-  }
+  pollv<CX, REL>(a.y, c, ar, ai);
+  chain<CX, true, PREF, REL>(ar, ai, a.lt_ci, a.lt_val, a.z, a.lt_rp[c],
+                             a.lt_rp[c + 1]);
   if (!isfin(ar) || !isfin(ai)) atomicOr(a.err, 1);
   publish<CX>(a.z, c, ar, ai);
 }
 
-template <bool CX, bool ADJ>
+template <bool CX, bool ADJ, int PREF, bool REL>
 __global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs a) {
   if (a.done && *a.done) return;
   const int lane = threadIdx.x & 31;
@@ -274,18 +302,210 @@ __global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs a) {
     if (base >= 2 * n) break;
     const int t = base + lane;
     if (t < n) {
+      const int row = a.ord_f ? a.ord_f[t] : t;
       if constexpr (ADJ)
-        fwd_row_adj<CX>(a, t);
+        fwd_row_adj<CX, PREF, REL>(a, row);
       else
-        fwd_row<CX>(a, t);
+        fwd_row<CX, PREF, REL>(a, row);
     } else if (t < 2 * n) {
+      const int row = a.ord_b ? a.ord_b[t - n] : 2 * n - 1 - t;
       if constexpr (ADJ)
-        bwd_row_adj<CX>(a, 2 * n - 1 - t);
+        bwd_row_adj<CX, PREF, REL>(a, row);
       else
-        bwd_row<CX>(a, 2 * n - 1 - t);
+        bwd_row<CX, PREF, REL>(a, row);
     }
   }
   exit_protocol(a.tick);
+}
+
+// ---------------------------------------------------------------------
+// Single-CTA level-synchronous sweeps for systems whose binary64 vector
+// fits in shared memory (n*8 B real, n*16 B complex <= 227 KB): the whole
+// forward/backward solve runs in ONE thread block; the vector lives in
+// SMEM (z overwrites y in place: backward row i reads its own y_i first,
+// and only z_j of earlier backward levels), levels are separated by
+// __syncthreads (~tens of ns) instead of L2 round trips, and each row's
+// entries are fetched from L2 in independent batches.  Per-row operation
+// order is the reference's, so results are bitwise identical.
+// ---------------------------------------------------------------------
+constexpr int kSmemThreads = 1024;
+
+template <bool CX>
+__device__ __forceinline__ void sm_ld(const double *sv, int j, double &r,
+                                      double &m) {
+  if constexpr (CX) {
+    const double2 w = reinterpret_cast<const double2 *>(sv)[j];
+    r = w.x;
+    m = w.y;
+  } else {
+    r = sv[j];
+    m = 0.0;
+  }
+}
+template <bool CX>
+__device__ __forceinline__ void sm_st(double *sv, int j, double r, double m) {
+  if constexpr (CX)
+    reinterpret_cast<double2 *>(sv)[j] = make_double2(r, m);
+  else
+    sv[j] = r;
+}
+
+// acc -= val[q] * sv[col[q]], q = lo..hi-1 in order, entries batch-loaded
+template <bool CX, bool CONJ>
+__device__ __forceinline__ void sm_chain(double &ar, double &ai,
+                                         const int *col, const double *val,
+                                         const double *sv, int lo, int hi) {
+  for (int p0 = lo; p0 < hi; p0 += 8) {
+    int c[8];
+    double lr[8], li[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      c[q] = 0;
+      lr[q] = li[q] = 0.0;
+      if (p0 + q < hi) {
+        c[q] = col[p0 + q];
+        ldval<CX>(val, p0 + q, lr[q], li[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (p0 + q < hi) {
+        double vr, vi;
+        sm_ld<CX>(sv, c[q], vr, vi);
+        mulsub<CX, CONJ>(ar, ai, lr[q], li[q], vr, vi);
+      }
+    }
+  }
+}
+
+template <bool CX, bool ADJ>
+__global__ void __launch_bounds__(kSmemThreads, 1)
+    sweep_smem_kernel(SweepArgs a) {
+  if (a.done && *a.done) return;
+  extern __shared__ double sv[];
+  const int tid = threadIdx.x;
+  for (int L = 0; L < a.nlev_f; ++L) {
+    const int r1 = a.lev_f[L + 1];
+    for (int r = a.lev_f[L] + tid; r < r1; r += kSmemThreads) {
+      const int i = a.ord_f[r];
+      double ar, ai;
+      load_in<CX>(a, i, ar, ai);
+      if constexpr (!ADJ) {
+        sm_chain<CX, false>(ar, ai, a.ci, a.lu, sv, a.rp[i], a.dp[i]);
+        sm_st<CX>(sv, i, ar, ai);
+      } else {
+        sm_chain<CX, true>(ar, ai, a.ut_ci, a.ut_val, sv, a.ut_rp[i],
+                           a.ut_rp[i + 1]);
+        double dr, di, qr, qi;
+        ldval<CX>(a.lu, a.dp[i], dr, di);
+        if constexpr (CX) {
+          py_cdiv(ar, ai, dr, -di, qr, qi);
+        } else {
+          qr = ddiv(ar, dr);
+          qi = 0.0;
+        }
+        sm_st<CX>(sv, i, qr, qi);
+      }
+    }
+    __syncthreads();
+  }
+  bool bad = false;
+  for (int L = 0; L < a.nlev_b; ++L) {
+    const int r1 = a.lev_b[L + 1];
+    for (int r = a.lev_b[L] + tid; r < r1; r += kSmemThreads) {
+      const int i = a.ord_b[r];
+      double ar, ai, qr, qi;
+      sm_ld<CX>(sv, i, ar, ai);
+      if constexpr (!ADJ) {
+        const int d = a.dp[i];
+        sm_chain<CX, false>(ar, ai, a.ci, a.lu, sv, d + 1, a.rp[i + 1]);
+        double dr, di;
+        ldval<CX>(a.lu, d, dr, di);
+        if constexpr (CX) {
+          py_cdiv(ar, ai, dr, di, qr, qi);
+        } else {
+          qr = ddiv(ar, dr);
+          qi = 0.0;
+        }
+      } else {
+        sm_chain<CX, true>(ar, ai, a.lt_ci, a.lt_val, sv, a.lt_rp[i],
+                           a.lt_rp[i + 1]);
+        qr = ar;
+        qi = ai;
+      }
+      bad = bad || !isfin(qr) || !isfin(qi);
+      sm_st<CX>(sv, i, qr, qi);
+      if constexpr (CX)
+        reinterpret_cast<double2 *>(a.z)[i] = make_double2(qr, qi);
+      else
+        a.z[i] = qr;
+    }
+    __syncthreads();
+  }
+  if (bad) atomicOr(a.err, 1);
+}
+
+// Level-synchronous single-CTA factorization (small n): rows of one level
+// are independent; __syncthreads orders the global-memory factor values
+// between levels within the block, so no per-row flags are needed.
+template <bool CX>
+__device__ void factor_row_nowait(const FactorArgs &a, int i) {
+  const int lo = a.rp[i], hi = a.rp[i + 1], d = a.dp[i];
+  double2 *lu2 = reinterpret_cast<double2 *>(a.lu);
+  for (int t = lo; t < d; ++t) {
+    const int kc = a.ci[t];
+    const int uk = a.dp[kc];
+    const int kend = a.rp[kc + 1];
+    if constexpr (!CX) {
+      const double l = ddiv(a.lu[t], a.lu[uk]);
+      a.lu[t] = l;
+      int q = t + 1;
+      for (int s = uk + 1; s < kend; ++s) {
+        const int col = a.ci[s];
+        while (q < hi && a.ci[q] < col) ++q;
+        if (q < hi && a.ci[q] == col) a.lu[q] = dsub(a.lu[q], dmul(l, a.lu[s]));
+      }
+    } else {
+      const double2 at = lu2[t];
+      const double2 ukk = lu2[uk];
+      double lr, li;
+      py_cdiv(at.x, at.y, ukk.x, ukk.y, lr, li);
+      lu2[t] = make_double2(lr, li);
+      int q = t + 1;
+      for (int s = uk + 1; s < kend; ++s) {
+        const int col = a.ci[s];
+        while (q < hi && a.ci[q] < col) ++q;
+        if (q < hi && a.ci[q] == col) {
+          const double2 u = lu2[s];
+          double pr, pi;
+          py_cmul(lr, li, u.x, u.y, pr, pi);
+          const double2 v = lu2[q];
+          lu2[q] = make_double2(dsub(v.x, pr), dsub(v.y, pi));
+        }
+      }
+    }
+  }
+  bool zero, fin = true;
+  if constexpr (!CX) {
+    zero = a.lu[d] == 0.0;
+    for (int p = lo; p < hi; ++p) fin = fin && isfin(a.lu[p]);
+  } else {
+    zero = (lu2[d].x == 0.0) && (lu2[d].y == 0.0);
+    for (int p = lo; p < hi; ++p) fin = fin && isfin(lu2[p].x) && isfin(lu2[p].y);
+  }
+  if (zero) atomicMin(a.bad_row, i);
+  if (!fin) atomicOr(a.nonfinite, 1);
+}
+
+template <bool CX>
+__global__ void __launch_bounds__(kSmemThreads, 1)
+    factor_smem_kernel(FactorArgs a) {
+  for (int L = 0; L < a.nlev; ++L) {
+    const int r1 = a.lev[L + 1];
+    for (int r = a.lev[L] + threadIdx.x; r < r1; r += kSmemThreads)
+      factor_row_nowait<CX>(a, a.ord[r]);
+    __syncthreads();
+  }
 }
 
 template <bool CX>
@@ -316,18 +536,78 @@ int sweep_grid(int n) {
 
 }  // namespace
 
+// Sweep variant (A/B measured on B200): MPK_SWEEP_VAR
+// 0 = one dependency load at a time (volatile), 1 = batches of 8
+// (volatile), 2 = batches of 8 (relaxed.gpu), 3 = one at a time (relaxed).
+static int sweep_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPK_SWEEP_VAR");
+    v = e ? atoi(e) : 3;
+    if (v < 0 || v > 3) v = 3;
+  }
+  return v;
+}
+
+template <bool CX, bool ADJ>
+static void launch_sweep_t(const SweepArgs &a, int g, cudaStream_t st) {
+  switch (sweep_variant()) {
+    case 0: sweep_kernel<CX, ADJ, 1, false><<<g, kBlock, 0, st>>>(a); break;
+    case 1: sweep_kernel<CX, ADJ, 8, false><<<g, kBlock, 0, st>>>(a); break;
+    case 2: sweep_kernel<CX, ADJ, 8, true><<<g, kBlock, 0, st>>>(a); break;
+    default: sweep_kernel<CX, ADJ, 1, true><<<g, kBlock, 0, st>>>(a); break;
+  }
+}
+
+static bool env_on(const char *name, bool dflt) {
+  const char *e = getenv(name);
+  if (!e) return dflt;
+  return e[0] != '0';
+}
+
+constexpr size_t kSmemMax = 227 * 1024;
+
+template <bool CX, bool ADJ>
+static void launch_sweep_smem(const SweepArgs &a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sweep_smem_kernel<CX, ADJ>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemMax);
+    attr = true;
+  }
+  const size_t bytes = (size_t)a.n * (CX ? 16 : 8);
+  sweep_smem_kernel<CX, ADJ><<<1, kSmemThreads, bytes, st>>>(a);
+}
+
+bool sweep_uses_smem(int n, bool cx) {
+  return env_on("MPK_SWEEP_SMEM", true) &&
+         (size_t)n * (cx ? 16 : 8) <= kSmemMax;
+}
+
 void launch_sweep(const SweepArgs &a, bool cx, bool adjoint,
                   cudaStream_t st) {
+  ++tl_launches;
+  if (a.lev_f && a.lev_b && sweep_uses_smem(a.n, cx)) {
+    if (!cx && !adjoint) launch_sweep_smem<false, false>(a, st);
+    if (!cx && adjoint) launch_sweep_smem<false, true>(a, st);
+    if (cx && !adjoint) launch_sweep_smem<true, false>(a, st);
+    if (cx && adjoint) launch_sweep_smem<true, true>(a, st);
+    return;
+  }
+  SweepArgs b = a;  // multi-CTA sync-free kernel: natural row order
+  b.ord_f = b.ord_b = nullptr;
   const int g = sweep_grid(a.n);
-  if (!cx && !adjoint) sweep_kernel<false, false><<<g, kBlock, 0, st>>>(a);
-  if (!cx && adjoint) sweep_kernel<false, true><<<g, kBlock, 0, st>>>(a);
-  if (cx && !adjoint) sweep_kernel<true, false><<<g, kBlock, 0, st>>>(a);
-  if (cx && adjoint) sweep_kernel<true, true><<<g, kBlock, 0, st>>>(a);
+  if (!cx && !adjoint) launch_sweep_t<false, false>(b, g, st);
+  if (!cx && adjoint) launch_sweep_t<false, true>(b, g, st);
+  if (cx && !adjoint) launch_sweep_t<true, false>(b, g, st);
+  if (cx && adjoint) launch_sweep_t<true, true>(b, g, st);
 }
 
 void launch_sweep_reset(double *y, double *z, int n, bool cx,
                         const int *done, cudaStream_t st) {
   const int g = grid_for(n);
+  ++tl_launches;
   if (cx)
     sweep_reset_kernel<true><<<g, kBlock, 0, st>>>(y, z, n, done);
   else
@@ -335,14 +615,24 @@ void launch_sweep_reset(double *y, double *z, int n, bool cx,
 }
 
 void launch_factor(const FactorArgs &a, bool cx, cudaStream_t st) {
+  ++tl_launches;
+  if (a.lev && a.n <= 65536 && env_on("MPK_FACTOR_SMEM", false)) {
+    if (cx)
+      factor_smem_kernel<true><<<1, kSmemThreads, 0, st>>>(a);
+    else
+      factor_smem_kernel<false><<<1, kSmemThreads, 0, st>>>(a);
+    return;
+  }
+  FactorArgs b = a;  // multi-CTA sync-free kernel: natural row order
+  b.ord = nullptr;
   long long warps = (a.n + 31) / 32;
   long long blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 6) blocks = 148 * 6;
   if (cx)
-    factor_kernel<true><<<(int)blocks, kBlock, 0, st>>>(a);
+    factor_kernel<true><<<(int)blocks, kBlock, 0, st>>>(b);
   else
-    factor_kernel<false><<<(int)blocks, kBlock, 0, st>>>(a);
+    factor_kernel<false><<<(int)blocks, kBlock, 0, st>>>(b);
 }
 
 }  // namespace mpk

@@ -21,6 +21,11 @@ namespace mpk {
 
 struct SweepArgs {
   int n;
+  // level schedule: rows sorted by level (a topological order of the sweep
+  // DAG), lev_f[L]..lev_f[L+1] = rows of forward level L (ord_f), same for
+  // the backward phase.  Used by the single-CTA shared-memory kernel.
+  const int *ord_f, *ord_b, *lev_f, *lev_b;
+  int nlev_f, nlev_b;
   const int *rp, *ci, *dp;
   const double *lu;  // real: [nnz]; complex: double2 [nnz]
   // adjoint gather structures (BiCG): U^T rows ascending, L^T descending
@@ -47,6 +52,9 @@ struct FactorArgs {
   const int *rp, *ci, *dp;
   double *lu;      // in: A values, out: factors (in place)
   int *rowflag;    // per-row completion flags (zeroed)
+  const int *ord;  // level order of the L DAG (single-CTA path)
+  const int *lev;  // level pointers into ord
+  int nlev;
   int *tick;       // [0] ticket, [1] exit counter
   int *bad_row;    // atomicMin of zero-pivot rows (init INT_MAX)
   int *nonfinite;  // set if any factor is non-finite

@@ -1,6 +1,8 @@
 // krylov.cuh -- device-side solver state and host-side solver object.
 #pragma once
 
+#include <map>
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -28,14 +30,21 @@ enum Breakdown {
 struct State {
   Sc rho, rho_old, alpha, omega, beta, sigma, nrm, nrm0, thr, zeta, eta;
   long long it, max_iter, iterations, hist_len, hist_cap;
+  long long body_runs;  // executions of the captured iteration graph
   int done, converged, breakdown, half_exit, have_nrm, sweep_err;
   double eps_rel, eps_abs;
   double relres, true_relres;
 };
 
+// Cached per-(method, K, field) solver workspace + graph (krylov_impl.cuh)
+struct PlanBase {
+  virtual ~PlanBase() {}
+};
+
 // Device matrix: binary64 CSR (int32 indices) + ILU(0) factors + the
 // transposed gather structures used by the adjoint paths (BiCG).
 struct DMat {
+  std::map<int, std::unique_ptr<PlanBase>> plans;
   int n;
   long long nnz;
   bool cx;
@@ -54,6 +63,11 @@ struct DMat {
   long long h_adj_sizes[2] = {0, 0};
   // sweep scratch
   double *sw_y = nullptr, *sw_y2 = nullptr;
+  // level orders (host-computed once per pattern): plain L / U sweeps and
+  // the adjoint U^H / L^H sweeps
+  int *ord_f = nullptr, *ord_b = nullptr, *ord_fa = nullptr, *ord_ba = nullptr;
+  int *lev_f = nullptr, *lev_b = nullptr, *lev_fa = nullptr, *lev_ba = nullptr;
+  int levels_f = 0, levels_b = 0, levels_fa = 0, levels_ba = 0;
   int *tick = nullptr;  // 4 ints: [0..1] sweep A, [2..3] sweep B
   int *err = nullptr;
   // host copies of the pattern (for building transposes)
@@ -74,6 +88,7 @@ struct SolveOut {
   double relres, true_relres;
   long long hist_len;
   float factor_ms, loop_ms;
+  long long launches;  // kernels executed by this solve
 };
 
 // Solve with the right-hand side already on the device (planar MC layout,

@@ -105,8 +105,9 @@ __device__ __forceinline__ void next_iter(State *S) {
   if (S->it > S->max_iter) finish_state(S, S->max_iter, 0, kBdNone);
 }
 
-static __global__ void set_cond_kernel(cudaGraphConditionalHandle h,
-                                       const State *S) {
+static __global__ void set_cond_kernel(cudaGraphConditionalHandle h, State *S,
+                                       int count) {
+  if (count) S->body_runs++;
   cudaGraphSetConditional(h, S->done ? 0u : 1u);
 }
 
@@ -142,8 +143,13 @@ __global__ void true_res_kernel_impl(State *S_, const double *pt_, int G_) {
 // ---------------------------------------------------------------------
 // solver object
 // ---------------------------------------------------------------------
+// A solver "plan": the per-(matrix, method, K, field) device workspace and
+// the instantiated iteration graph.  Built on the first solve and cached on
+// the matrix (DMat::plans), so repeated solves pay no allocation and no
+// graph construction; every run-time parameter (eps, max_iter, scalars)
+// lives in the device State the kernels read.
 template <int K, bool CX>
-struct Solver {
+struct Solver : PlanBase {
   using MVt = MV<K, CX>;
   using FVt = FV<CX>;
   DMat &A;
@@ -156,26 +162,49 @@ struct Solver {
   State *S = nullptr;
   double *part = nullptr;
   double *hist = nullptr;
+  long long hist_cap = 0;
   const int *done = nullptr;
   int *err = nullptr;
   std::vector<void *> allocs;
   bool ok = true;
   char *errbuf;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  long long body_nodes = 0;
+  bool cond_graph = true;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
-  Solver(DMat &A_, const SolveParams &p_, cudaStream_t st_, double *hist_,
-         char *eb)
-      : A(A_), p(p_), st(st_), hist(hist_), errbuf(eb) {
+  Solver(DMat &A_, const SolveParams &p_, cudaStream_t st_, char *eb)
+      : A(A_), p(p_), st(st_), errbuf(eb) {
     n = A.n;
     ld = plane_ld(n);
     G = grid_for(n);
     da = DA{A.n, A.rp, A.ci, A.val, A.at_rp, A.at_ci, A.at_val};
     S = (State *)dalloc(sizeof(State));
     part = (double *)dalloc(sizeof(double) * 6 * kMaxGrid * 8);
+    hist_cap = p.hist_cap > 0 ? p.hist_cap : 1;
+    hist = (double *)dalloc(sizeof(double) * K * hist_cap);
+    fzero = fv();
     done = &S->done;
     err = A.err;
+    switch (p.method) {
+      case kBiCG: bicg_alloc(); break;
+      case kCGS: cgs_alloc(); break;
+      case kBiCGSTAB: bicgstab_alloc(); break;
+      default: gpbicg_alloc(); break;
+    }
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
   }
-  ~Solver() {
+  ~Solver() override {
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
     for (void *q : allocs) cudaFree(q);
+  }
+  void zero_mc(double *q) {
+    cudaMemsetAsync(q, 0, sizeof(double) * K * (CX ? 2 : 1) * ld, st);
   }
   void *dalloc(size_t bytes) {
     void *q = nullptr;
@@ -195,7 +224,7 @@ struct Solver {
 
   // ILU(0)-mixed apply: z = promote(U^-1 L^-1 demote(in)).
   void sweep(const double *in_re, const double *in_im, double *y, double *z,
-             bool adjoint, int which) {
+             bool adjoint, int which, bool after_loop = false) {
     SweepArgs a{};
     a.n = n;
     a.rp = A.rp;
@@ -208,13 +237,19 @@ struct Solver {
     a.lt_rp = A.lt_rp;
     a.lt_ci = A.lt_ci;
     a.lt_val = A.lt_val;
+    a.ord_f = adjoint ? A.ord_fa : A.ord_f;
+    a.ord_b = adjoint ? A.ord_ba : A.ord_b;
+    a.lev_f = adjoint ? A.lev_fa : A.lev_f;
+    a.lev_b = adjoint ? A.lev_ba : A.lev_b;
+    a.nlev_f = adjoint ? A.levels_fa : A.levels_f;
+    a.nlev_b = adjoint ? A.levels_ba : A.levels_b;
     a.in_re = in_re;
     a.in_im = in_im;
     a.y = y;
     a.z = z;
     a.tick = A.tick + 2 * which;
     a.err = A.err;
-    a.done = done;
+    a.done = after_loop ? nullptr : done;
     launch_sweep(a, CX, adjoint, st);
   }
   const double *head_re(const double *v) const { return v; }
@@ -226,10 +261,7 @@ struct Solver {
   double *Bp, *Bt, *yv, *tpr, *zz, *yhat, *Mp, *Mt; // GPBiCG
   double *rt, *pt, *qv, *qt, *zf, *ztf;             // BiCG
 
-  void alloc_common(const double *d_b) {
-    b = const_cast<double *>(d_b);
-    fzero = fv();
-  }
+  void alloc_common(const double *d_b) { b = const_cast<double *>(d_b); }
 
   // r = b - A*0 (the reference forms matvec(zeros), solvers.py:189 etc.),
   // plus partial norm2(r) [slot NH] and hdot(r, r) as rho [slot 0].
@@ -262,9 +294,12 @@ struct Solver {
         });
   }
 
-  void bicgstab_setup() {
+  void bicgstab_alloc() {
     x = mc(); r = mc(); rt0 = mc(); pp = mc(); v = mc(); s = mc(); t = mc();
     phat = fv(); shat = fv();
+  }
+  void bicgstab_setup() {
+    zero_mc(x);
     setup_residual(r, rt0, true);
   }
 
@@ -434,10 +469,13 @@ struct Solver {
   }
 
   // ---------------- CGS (solvers.py:229-272) ----------------
-  void cgs_setup() {
+  void cgs_alloc() {
     x = mc(); r = mc(); rt0 = mc(); u = mc(); pp = mc(); q = mc(); v = mc();
     phat = fv(); uhat = fv();
     whead = (double *)dalloc(sizeof(double) * 2 * ld);
+  }
+  void cgs_setup() {
+    zero_mc(x);
     setup_residual(r, rt0, true);
   }
 
@@ -554,10 +592,18 @@ struct Solver {
   }
 
   // ---------------- GPBiCG (solvers.py:331-412) ----------------
-  void gpbicg_setup() {
+  void gpbicg_alloc() {
     r = mc(); rt0 = mc(); u = mc(); zz = mc(); pp = mc(); Bp = mc();
     yv = mc(); t = mc(); Bt = mc(); w = mc(); tpr = mc(); yhat = mc();
     Mp = fv(); Mt = fv(); x = fv();
+  }
+  void gpbicg_setup() {
+    // t_prev, w, u, z, yhat start at zero (solvers.py:341-352)
+    zero_mc(u);
+    zero_mc(zz);
+    zero_mc(t);
+    zero_mc(w);
+    zero_mc(yhat);
     setup_residual(r, rt0, true);
   }
 
@@ -763,9 +809,12 @@ struct Solver {
   }
 
   // ---------------- BiCG (solvers.py:183-226) ----------------
-  void bicg_setup() {
+  void bicg_alloc() {
     x = mc(); r = mc(); rt = mc(); pp = mc(); pt = mc(); qv = mc(); qt = mc();
     zf = fv(); ztf = fv();
+  }
+  void bicg_setup() {
+    zero_mc(x);
     setup_residual(r, rt, false);
     const FVt Z = fvv(zf), ZT = fvv(ztf), Y = fvv(A.sw_y), Y2 = fvv(A.sw_y2);
     rows<K, CX, 0, 0>(n, done, part, st,
@@ -923,7 +972,7 @@ struct Solver {
         return;
       }
       launch_sweep_reset(A.sw_y, x, n, CX, nullptr, st);
-      sweep(head_re(yhat), head_im(yhat), A.sw_y, x, false, 0);
+      sweep(head_re(yhat), head_im(yhat), A.sw_y, x, false, 0, true);
       promote(x, d_x);
       return;
     }
@@ -974,16 +1023,41 @@ struct Solver {
   } while (0)
 
 template <int K, bool CX>
-int run_typed(DMat &A, const SolveParams &p, const double *d_b,
-                     double *d_x, double *d_hist, SolveOut *out,
-                     cudaStream_t st, char *errbuf) {
+int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
+              double *d_hist, SolveOut *out, cudaStream_t st, char *errbuf) {
   if (!p.precond_ilu) {
     snprintf(errbuf, 256, "precond 'none' is not implemented on the device path");
     return 3;
   }
   if (p.method == kBiCG) ensure_adjoint(A, st);
-  Solver<K, CX> sv(A, p, st, d_hist, errbuf);
-  if (!sv.ok) return 4;
+  const char *nocond = getenv("MPK_NO_COND_GRAPH");
+  const bool use_cond = !nocond || nocond[0] == '0';
+  // plan cache: one workspace + graph per (method, K, field) on this matrix
+  const int key = p.method * 100 + K * 10 + (CX ? 1 : 0);
+  Solver<K, CX> *sv = nullptr;
+  auto it = A.plans.find(key);
+  if (it != A.plans.end()) {
+    sv = static_cast<Solver<K, CX> *>(it->second.get());
+    if (sv->hist_cap < p.hist_cap || sv->cond_graph != use_cond) {
+      A.plans.erase(it);
+      sv = nullptr;
+    }
+  }
+  if (!sv) {
+    SolveParams pp = p;
+    pp.hist_cap = p.hist_cap > 0 ? p.hist_cap : 1;
+    auto *fresh = new Solver<K, CX>(A, pp, st, errbuf);
+    A.plans[key].reset(fresh);
+    sv = fresh;
+    if (!sv->ok) {
+      A.plans.erase(key);
+      return 4;
+    }
+    sv->cond_graph = use_cond;
+  }
+  sv->p = p;
+  sv->errbuf = errbuf;
+  const long long launches0 = tl_launches;
   State hs{};
   hs.max_iter = p.max_iter;
   hs.hist_cap = p.hist_cap;
@@ -991,70 +1065,77 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b,
   hs.eps_abs = p.eps_abs;
   hs.relres = NAN;
   hs.true_relres = NAN;
-  CK(cudaMemcpyAsync(sv.S, &hs, sizeof(State), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(sv->S, &hs, sizeof(State), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(A.err, 0, sizeof(int), st));
-  sv.alloc_common(d_b);
-  if (!sv.ok) return 4;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventRecord(e0, st);
-  sv.setup();
-  if (!sv.ok) return 4;
+  sv->alloc_common(d_b);
+  cudaEventRecord(sv->ev0, st);
+  sv->setup();
   CK(cudaGetLastError());
 
-  // one iteration -> WHILE body
-  const char *nocond = getenv("MPK_NO_COND_GRAPH");
-  cudaGraph_t g = nullptr;
-  cudaGraphExec_t ge = nullptr;
-  if (!nocond || nocond[0] == '0') {
-    CK(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle h;
-    CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
-    cudaKernelNodeParams kp{};
-    State *Sd = sv.S;
-    void *args[] = {&h, &Sd};
-    kp.func = (void *)set_cond_kernel;
-    kp.gridDim = dim3(1);
-    kp.blockDim = dim3(1);
-    kp.kernelParams = args;
-    cudaGraphNode_t n1, n2;
-    CK(cudaGraphAddKernelNode(&n1, g, nullptr, 0, &kp));
-    cudaGraphNodeParams cp{};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    CK(cudaGraphAddNode(&n2, g, &n1, 1, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
-                                     cudaStreamCaptureModeThreadLocal));
-    sv.iter();
-    set_cond_kernel<<<1, 1, 0, st>>>(h, sv.S);
-    CK(cudaStreamEndCapture(st, &body));
-    CK(cudaGraphInstantiate(&ge, g, 0));
-    CK(cudaGraphLaunch(ge, st));
+  if (!sv->ge) {
+    if (use_cond) {
+      // one iteration -> body of a device-side WHILE conditional node
+      CK(cudaGraphCreate(&sv->g, 0));
+      cudaGraphConditionalHandle h;
+      CK(cudaGraphConditionalHandleCreate(&h, sv->g, 0, 0));
+      cudaKernelNodeParams kp{};
+      State *Sd = sv->S;
+      int no_count = 0;
+      void *args[] = {&h, &Sd, &no_count};
+      kp.func = (void *)set_cond_kernel;
+      kp.gridDim = dim3(1);
+      kp.blockDim = dim3(1);
+      kp.kernelParams = args;
+      cudaGraphNode_t n1, n2;
+      CK(cudaGraphAddKernelNode(&n1, sv->g, nullptr, 0, &kp));
+      cudaGraphNodeParams cp{};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      CK(cudaGraphAddNode(&n2, sv->g, &n1, 1, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeThreadLocal));
+      const long long c0 = tl_launches;
+      sv->iter();
+      set_cond_kernel<<<1, 1, 0, st>>>(h, sv->S, 1);
+      sv->body_nodes = tl_launches - c0 + 1;
+      tl_launches = c0;
+      CK(cudaStreamEndCapture(st, &body));
+    } else {
+      // fallback: a plain one-iteration graph replayed in polled chunks
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      const long long c0 = tl_launches;
+      sv->iter();
+      sv->body_nodes = tl_launches - c0;
+      tl_launches = c0;
+      CK(cudaStreamEndCapture(st, &sv->g));
+    }
+    CK(cudaGraphInstantiate(&sv->ge, sv->g, 0));
+  }
+  if (use_cond) {
+    CK(cudaGraphLaunch(sv->ge, st));
+    tl_launches += 1;  // the init node; body nodes counted per run below
   } else {
-    // fallback: replay a plain one-iteration graph in chunks, polling done
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    sv.iter();
-    CK(cudaStreamEndCapture(st, &g));
-    CK(cudaGraphInstantiate(&ge, g, 0));
     long long launched = 0;
     int chunk = 4;
     State probe{};
     while (launched < p.max_iter) {
-      for (int c = 0; c < chunk && launched < p.max_iter; ++c, ++launched)
-        CK(cudaGraphLaunch(ge, st));
-      CK(cudaMemcpyAsync(&probe, sv.S, sizeof(State), cudaMemcpyDeviceToHost, st));
+      for (int c = 0; c < chunk && launched < p.max_iter; ++c, ++launched) {
+        CK(cudaGraphLaunch(sv->ge, st));
+        tl_launches += sv->body_nodes;
+      }
+      CK(cudaMemcpyAsync(&probe, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       if (probe.done) break;
       if (chunk < 64) chunk *= 2;
     }
   }
-  cudaEventRecord(e1, st);
-  CK(cudaMemcpyAsync(&hs, sv.S, sizeof(State), cudaMemcpyDeviceToHost, st));
+  cudaEventRecord(sv->ev1, st);
+  CK(cudaMemcpyAsync(&hs, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (use_cond) tl_launches += sv->body_nodes * hs.body_runs;
   if (!hs.done) {
     // loop ran out without a device-side stop (max_iter reached)
     hs.iterations = p.max_iter;
@@ -1062,50 +1143,42 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b,
     hs.breakdown = kBdNone;
   }
   float loop_ms = 0;
-  cudaEventElapsedTime(&loop_ms, e0, e1);
-  if (ge) cudaGraphExecDestroy(ge);
-  if (g) cudaGraphDestroy(g);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-
+  cudaEventElapsedTime(&loop_ms, sv->ev0, sv->ev1);
+  out->loop_ms = loop_ms;
   out->hist_len = hs.hist_len;
-  if (hs.breakdown == kBdNumericSweep) {
+  const long long hn = hs.hist_len < p.hist_cap ? hs.hist_len : p.hist_cap;
+  if (d_hist && hn > 0)
+    CK(cudaMemcpyAsync(d_hist, sv->hist, sizeof(double) * K * hn,
+                       cudaMemcpyDeviceToDevice, st));
+  auto sweep_fail = [&]() {
     out->iterations = 0;
     out->converged = 0;
     out->breakdown = kBdNumericSweep;
     out->half_exit = 0;
     out->relres = NAN;
     out->true_relres = NAN;
-    out->loop_ms = loop_ms;
+    out->launches = tl_launches - launches0;
     return 0;
-  }
-  sv.finish(hs, d_x);
+  };
+  if (hs.breakdown == kBdNumericSweep) return sweep_fail();
+  sv->finish(hs, d_x);
   int e_after = 0;
-  if (p.method == kGPBiCG && !(hs.iterations == 0 && hs.converged)) {
+  if (p.method == kGPBiCG && !(hs.iterations == 0 && hs.converged))
     CK(cudaMemcpyAsync(&e_after, A.err, sizeof(int), cudaMemcpyDeviceToHost, st));
-  }
-  relres_kernel<K><<<1, 1, 0, st>>>(sv.S);
-  sv.true_residual(d_x);
-  CK(cudaMemcpyAsync(&hs, sv.S, sizeof(State), cudaMemcpyDeviceToHost, st));
+  relres_kernel<K><<<1, 1, 0, st>>>(sv->S);
+  tl_launches += 2;  // relres + true-residual finalize
+  sv->true_residual(d_x);
+  CK(cudaMemcpyAsync(&hs, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
-  if (e_after) {
-    out->iterations = 0;
-    out->converged = 0;
-    out->breakdown = kBdNumericSweep;
-    out->half_exit = 0;
-    out->relres = NAN;
-    out->true_relres = NAN;
-    out->loop_ms = loop_ms;
-    return 0;
-  }
+  if (e_after) return sweep_fail();
   out->iterations = hs.iterations;
   out->converged = hs.converged;
   out->breakdown = hs.breakdown;
   out->half_exit = hs.half_exit;
   out->relres = hs.relres;
   out->true_relres = hs.true_relres;
-  out->loop_ms = loop_ms;
+  out->launches = tl_launches - launches0;
   return 0;
 }
 

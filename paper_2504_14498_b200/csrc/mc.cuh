@@ -17,10 +17,11 @@
 //    known to be zero (zero tails of promoted binary64 values) can be dropped
 //    at compile time: mul_lf / mul_rf / mul_ff below are the reference's
 //    mc_mul with a promoted binary64 operand, minus its zero terms.
-//  * TwoProd uses FMA: bit-identical to the reference's Dekker split for
-//    operands whose product neither overflows nor underflows (SURVEY.md
-//    finding 8).  All other binary64 operations use explicit _rn intrinsics,
-//    so no FMA contraction can occur regardless of compiler flags.
+//  * TwoProd uses FMA when both operands lie in [2^-480, 2^480] (then it is
+//    bit-identical to the reference's Dekker split, SURVEY.md finding 8) and
+//    the reference's Dekker split itself otherwise (underflowing errors
+//    differ between the two).  All other binary64 operations use explicit
+//    _rn intrinsics, so no FMA contraction can occur regardless of flags.
 //
 // Non-finite operands follow the reference's non-finite path (plain sum of
 // the terms in the head) except that products of a dropped zero term with
@@ -29,6 +30,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 
 #if defined(__CUDACC__)
 #define MPK_HD __host__ __device__ __forceinline__
@@ -105,18 +107,56 @@ MPK_HD void two_sum(double a, double b, double &s, double &e) {
   s = q;
 }
 
-// two_prod _mccore.py:40-51 (FMA form, see header)
+// Dekker split / two_prod exactly as the reference (_mccore.py:34-51)
+MPK_HD double dekker_err(double a, double b, double p) {
+  double t = dmul(134217729.0, a);
+  const double ah = dsub(t, dsub(t, a));
+  const double al = dsub(a, ah);
+  t = dmul(134217729.0, b);
+  const double bh = dsub(t, dsub(t, b));
+  const double bl = dsub(b, bh);
+  return dadd(dadd(dadd(dsub(dmul(ah, bh), p), dmul(ah, bl)), dmul(al, bh)),
+              dmul(al, bl));
+}
+
+// |x| in [2^-480, 2^480] or x == 0: every partial product of Dekker's
+// algorithm and the exact error of a*b are multiples of >= 2^-1064 below
+// 2^1000, hence representable, so fma(a,b,-p) == Dekker bit for bit.
+MPK_HD bool fma_safe(double x) {
+#ifdef __CUDA_ARCH__
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+#else
+  unsigned long long u;
+  std::memcpy(&u, &x, sizeof u);
+#endif
+  const unsigned ex = (unsigned)((u >> 52) & 0x7ffu);
+  return ((u << 1) == 0ull) || (ex - (1023u - 480u) <= 960u);
+}
+
+// two_prod _mccore.py:40-51: FMA form where provably identical (header)
 MPK_HD void two_prod(double a, double b, double &p, double &e) {
   p = dmul(a, b);
-  e = dfma(a, b, -p);
+  if (fma_safe(a) && fma_safe(b))
+    e = dfma(a, b, -p);
+  else
+    e = dekker_err(a, b, p);
 }
 
 // renorm_terms _mccore.py:90-116 on M register slots (holes = +0.0).
+// finite test on the exponent bits (2 integer ops, no branch)
+MPK_HD bool fin_bits(double x) {
+#ifdef __CUDA_ARCH__
+  return (__double2hiint(x) & 0x7ff00000) != 0x7ff00000;
+#else
+  return std::isfinite(x);
+#endif
+}
+
 template <int M, int K>
 MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
   bool fin = true;
 #pragma unroll
-  for (int i = 0; i < M; ++i) fin = fin && isfin(t[i]);
+  for (int i = 0; i < M; ++i) fin = fin & fin_bits(t[i]);
   if (!fin) {
     double s = 0.0;
 #pragma unroll
@@ -148,30 +188,30 @@ MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
       eps = em ? en : q;
     }
     t[M - 1] = eps;
+    // strictness over consecutive non-hole components (branch-free)
     bool ok = true;
     double prev = 0.0;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       const double c = t[i];
-      if (c != 0.0) {
-        if (prev != 0.0 && dadd(prev, c) != prev) ok = false;
-        prev = c;
-      }
+      const bool nz = (c != 0.0);
+      const bool viol = nz & (prev != 0.0) & (dadd(prev, c) != prev);
+      ok = ok & !viol;
+      prev = nz ? c : prev;
     }
     if (ok) break;
   }
+  // first K non-hole components (branch-free predicated selects)
 #pragma unroll
   for (int j = 0; j < K; ++j) out[j] = 0.0;
   int cnt = 0;
 #pragma unroll
   for (int i = 0; i < M; ++i) {
     const double c = t[i];
-    if (c != 0.0) {
+    const bool nz = (c != 0.0);
 #pragma unroll
-      for (int j = 0; j < K; ++j)
-        if (cnt == j) out[j] = c;
-      ++cnt;
-    }
+    for (int j = 0; j < K; ++j) out[j] = (nz & (cnt == j)) ? c : out[j];
+    cnt += nz ? 1 : 0;
   }
 }
 
@@ -332,13 +372,18 @@ MPK_HD void mul_rf(const double (&x)[K], double f, double (&out)[K]) {
 // finite (|e| <= ulp(p)/2 and fl(p+e) = p by round-to-nearest-even).
 MPK_HD void mul_ff2(double a, double f, double &h, double &l) {
   double p, e;
-  two_prod(a, f, p, e);
-  if (isfin(p)) {
+  if (fma_safe(a) && fma_safe(f)) {
+    p = dmul(a, f);
+    e = dfma(a, f, -p);
     h = dadd(p, 0.0);
     l = dadd(e, 0.0);
   } else {
-    h = dadd(dadd(0.0, p), e);
-    l = 0.0;
+    p = dmul(a, f);
+    e = dekker_err(a, f, p);
+    double t[2] = {p, e}, o[2];
+    renorm<2, 2>(t, o);
+    h = o[0];
+    l = o[1];
   }
 }
 
@@ -424,7 +469,7 @@ MPK_HD double div_by_zero(double x0, double y0) {
 
 // mc_div _mccore.py:222-237 (Newton reciprocal seeded by binary64 1/y0)
 template <int K>
-MPK_SCALAR void div(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
+MPK_HD void div_a(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
   if (K == 1) {
     out[0] = (y[0] == 0.0) ? div_by_zero(x[0], y[0]) : ddiv(x[0], y[0]);
     return;
@@ -459,7 +504,7 @@ MPK_SCALAR void div(const double (&x)[K], const double (&y)[K], double (&out)[K]
 
 // mc_sqrt _mccore.py:245-266 (Newton on rsqrt). Returns false if x0 < 0.
 template <int K>
-MPK_SCALAR bool sqrt_mc(const double (&x)[K], double (&out)[K]) {
+MPK_HD bool sqrt_a(const double (&x)[K], double (&out)[K]) {
   if (x[0] < 0.0) {
 #pragma unroll
     for (int i = 0; i < K; ++i) out[i] = NAN;
@@ -504,7 +549,7 @@ MPK_SCALAR bool sqrt_mc(const double (&x)[K], double (&out)[K]) {
 
 // mc_cmp _mccore.py:283-290
 template <int K>
-MPK_SCALAR int cmp(const double (&x)[K], const double (&y)[K]) {
+MPK_HD int cmp_a(const double (&x)[K], const double (&y)[K]) {
   double d[K];
   sub<K>(x, y, d);
   if (d[0] > 0.0) return 1;
@@ -512,9 +557,73 @@ MPK_SCALAR int cmp(const double (&x)[K], const double (&y)[K]) {
   return 0;
 }
 
+// Out-of-line scalar entry points.  They take and return small structs BY
+// VALUE (register ABI): passing references to a caller's register arrays
+// into a __noinline__ function is exactly what faulted on sm_100a, so no
+// pointer to a caller-local array ever crosses these call boundaries.
+template <int K>
+struct V {
+  double c[K];
+};
+template <int K>
+struct V2 {
+  double r[K];
+  double i[K];
+};
+
+template <int K>
+MPK_SCALAR V<K> div_v(V<K> x, V<K> y) {
+  V<K> o;
+  div_a<K>(x.c, y.c, o.c);
+  return o;
+}
+template <int K>
+MPK_SCALAR V<K> sqrt_v(V<K> x) {
+  V<K> o;
+  sqrt_a<K>(x.c, o.c);
+  return o;
+}
+template <int K>
+MPK_SCALAR int cmp_v(V<K> x, V<K> y) {
+  return cmp_a<K>(x.c, y.c);
+}
+
+template <int K>
+MPK_HD void div(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
+  V<K> a, b;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    a.c[i] = x[i];
+    b.c[i] = y[i];
+  }
+  const V<K> o = div_v<K>(a, b);
+#pragma unroll
+  for (int i = 0; i < K; ++i) out[i] = o.c[i];
+}
+template <int K>
+MPK_HD bool sqrt_mc(const double (&x)[K], double (&out)[K]) {
+  V<K> a;
+#pragma unroll
+  for (int i = 0; i < K; ++i) a.c[i] = x[i];
+  const V<K> o = sqrt_v<K>(a);
+#pragma unroll
+  for (int i = 0; i < K; ++i) out[i] = o.c[i];
+  return !(x[0] < 0.0);
+}
+template <int K>
+MPK_HD int cmp(const double (&x)[K], const double (&y)[K]) {
+  V<K> a, b;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    a.c[i] = x[i];
+    b.c[i] = y[i];
+  }
+  return cmp_v<K>(a, b);
+}
+
 // cx_div _mccore.py:328-347 (Smith)
 template <int K>
-MPK_SCALAR void cdiv(const double (&ar)[K], const double (&ai)[K],
+MPK_HD void cdiv_a(const double (&ar)[K], const double (&ai)[K],
                  const double (&br)[K], const double (&bi)[K],
                  double (&outr)[K], double (&outi)[K]) {
   double t[K], d[K], u[K], v[K], re[K], im[K];
@@ -550,6 +659,33 @@ MPK_SCALAR void cdiv(const double (&ar)[K], const double (&ai)[K],
   for (int i = 0; i < K; ++i) {
     outr[i] = re[i];
     outi[i] = im[i];
+  }
+}
+
+template <int K>
+MPK_SCALAR V2<K> cdiv_v(V2<K> a, V2<K> b) {
+  V2<K> o;
+  cdiv_a<K>(a.r, a.i, b.r, b.i, o.r, o.i);
+  return o;
+}
+
+template <int K>
+MPK_HD void cdiv(const double (&ar)[K], const double (&ai)[K],
+                 const double (&br)[K], const double (&bi)[K],
+                 double (&outr)[K], double (&outi)[K]) {
+  V2<K> a, b;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    a.r[i] = ar[i];
+    a.i[i] = ai[i];
+    b.r[i] = br[i];
+    b.i[i] = bi[i];
+  }
+  const V2<K> o = cdiv_v<K>(a, b);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    outr[i] = o.r[i];
+    outi[i] = o.i[i];
   }
 }
 

@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(kBlock)
 
 template <int K, bool CX, int NH, int NN, class F>
 void rows(long long n, const int *done, double *part, cudaStream_t st, F f) {
+  ++tl_launches;
   rows_kernel<K, CX, NH, NN, F><<<grid_for(n), kBlock, 0, st>>>(n, done, part, f);
 }
 
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kBlock)
 template <class F>
 void fin(State *S, const int *err, const double *part, int G, cudaStream_t st,
          F f) {
+  ++tl_launches;
   fin_kernel<F><<<1, kBlock, 0, st>>>(S, err, part, G, f);
 }
 

@@ -296,12 +296,14 @@ __global__ void from_planar_kernel(long long n, int k, const double *dev,
 void launch_to_planar(long long n, int k, const double *re, const double *im,
                       double *dev, cudaStream_t st) {
   if (n <= 0) return;
+  ++tl_launches;
   to_planar_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
       n, k, re, im, dev, plane_ld(n));
 }
 void launch_from_planar(long long n, int k, const double *dev, double *re,
                         double *im, cudaStream_t st) {
   if (n <= 0) return;
+  ++tl_launches;
   from_planar_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
       n, k, dev, plane_ld(n), re, im);
 }
