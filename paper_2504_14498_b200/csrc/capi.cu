@@ -1,4 +1,5 @@
 // capi.cu -- C ABI (include/mpk_b200.h) over the device hot path.
+#include <algorithm>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -113,6 +114,73 @@ static int level_order(int n, bool descending, const int *deps, Lo dlo, Hi dhi,
   return nlev;
 }
 
+__global__ void gather_phase_kernel(const double *lu, SweepPhase ph, int n,
+                                    int cx) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t < ph.nent) {
+    const int s = ph.src[t];  // -1: ELL padding
+    if (cx)
+      reinterpret_cast<double2 *>(ph.val)[t] =
+          s >= 0 ? reinterpret_cast<const double2 *>(lu)[s] : make_double2(0.0, 0.0);
+    else
+      ph.val[t] = s >= 0 ? lu[s] : 0.0;
+  }
+  if (t < n) {
+    const int s = ph.dsrc[t];
+    if (cx)
+      reinterpret_cast<double2 *>(ph.dval)[t] =
+          s >= 0 ? reinterpret_cast<const double2 *>(lu)[s] : make_double2(1.0, 0.0);
+    else
+      ph.dval[t] = s >= 0 ? lu[s] : 1.0;
+  }
+}
+
+// Build one phase: rows in level order `ord` (level pointers `lev`), row i's
+// entries (col, src) produced by `ent(i, cb)` in the reference's order and
+// its divisor source `div(i)` (-1 if none).
+template <class Ent, class Div>
+static void build_phase(SweepPhase &ph, int n, bool cx,
+                        const std::vector<int> &ord, const std::vector<int> &lev,
+                        int nlev, Ent ent, Div div, cudaStream_t st) {
+  std::vector<int4> desc(n);
+  std::vector<int> col, src, dsrc(n);
+  for (int r = 0; r < n; ++r) {
+    const int i = ord[r];
+    const int e0 = (int)col.size();
+    ent(i, [&](int c, int s) {
+      col.push_back(c);
+      src.push_back(s);
+    });
+    desc[r] = make_int4(i, e0, (int)col.size() - e0, 0);
+    dsrc[r] = div(i);
+  }
+  ph.nlev = nlev;
+  ph.nent = (long long)col.size();
+  upload(&ph.lev, lev, st);
+  upload(&ph.desc, desc, st);
+  upload(&ph.col, col, st);
+  upload(&ph.src, src, st);
+  upload(&ph.dsrc, dsrc, st);
+  const size_t w = cx ? 2 : 1;
+  cudaMalloc(&ph.val, sizeof(double) * w * (col.size() + 1));
+  cudaMalloc(&ph.dval, sizeof(double) * w * (n + 1));
+}
+
+static void gather_phase(const double *lu, const SweepPhase &ph, int n, bool cx,
+                         cudaStream_t st) {
+  const long long m = ph.nent > n ? ph.nent : n;
+  if (m <= 0) return;
+  ++tl_launches;
+  gather_phase_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(lu, ph, n,
+                                                                   cx ? 1 : 0);
+}
+
+static void free_phase(SweepPhase &ph) {
+  void *p[] = {ph.lev, ph.desc, ph.col, ph.src, ph.val, ph.dsrc, ph.dval};
+  for (void *q : p)
+    if (q) cudaFree(q);
+}
+
 }  // namespace
 
 namespace mpk {
@@ -177,6 +245,24 @@ void ensure_adjoint(DMat &A, cudaStream_t st) {
     upload(&A.ord_ba, ob, st);
     upload(&A.lev_fa, pf, st);
     upload(&A.lev_ba, pb, st);
+    if (sweep_uses_smem(n, cx)) {
+      // U^H forward: column c of U in ascending source rows, / conj(U_cc);
+      // L^H backward: column c of L in descending source rows
+      build_phase(
+          A.smat_adj.fwd, n, cx, of, pf, A.levels_fa,
+          [&](int c, auto cb) {
+            for (int q = ucnt[c]; q < ucnt[c + 1]; ++q) cb(ut_ci[q], ut_perm[q]);
+          },
+          [&](int c) { return dp[c]; }, st);
+      build_phase(
+          A.smat_adj.bwd, n, cx, ob, pb, A.levels_ba,
+          [&](int c, auto cb) {
+            for (int q = lcnt[c]; q < lcnt[c + 1]; ++q) cb(lt_ci[q], lt_perm[q]);
+          },
+          [&](int) { return -1; }, st);
+      A.smat_adj.conj = true;
+      A.smat_adj_built = true;
+    }
     const size_t w = cx ? 2 : 1;
     cudaMalloc(&A.at_val, sizeof(double) * w * (A.nnz ? A.nnz : 1));
     cudaMalloc(&A.ut_val, sizeof(double) * w * (ut_ci.size() + 1));
@@ -188,6 +274,10 @@ void ensure_adjoint(DMat &A, cudaStream_t st) {
   if (A.factored && !A.adj_ready) {
     gather(A.lu, A.ut_perm, A.ut_val, A.h_adj_sizes[0], cx, st);
     gather(A.lu, A.lt_perm, A.lt_val, A.h_adj_sizes[1], cx, st);
+    if (A.smat_adj_built) {
+      gather_phase(A.lu, A.smat_adj.fwd, n, cx, st);
+      gather_phase(A.lu, A.smat_adj.bwd, n, cx, st);
+    }
     A.adj_ready = true;
   }
 }
@@ -287,6 +377,24 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
     delete m;
     return fail(MPK_CUDA_ERROR, "allocation failed");
   }
+  if (sweep_uses_smem((int)n, A.cx)) {
+    const int *rp = A.h_rp.data(), *dp = A.h_dp.data(), *ci = A.h_ci.data();
+    build_phase(
+        A.smat.fwd, (int)n, A.cx, of, pf, A.levels_f,
+        [&](int i, auto cb) {
+          const int hi = dp[i] < 0 ? rp[i] : dp[i];
+          for (int p = rp[i]; p < hi; ++p) cb(ci[p], p);
+        },
+        [&](int) { return -1; }, st);
+    build_phase(
+        A.smat.bwd, (int)n, A.cx, ob, pb, A.levels_b,
+        [&](int i, auto cb) {
+          const int lo = dp[i] < 0 ? rp[i + 1] : dp[i] + 1;
+          for (int p = lo; p < rp[i + 1]; ++p) cb(ci[p], p);
+        },
+        [&](int i) { return dp[i]; }, st);
+    A.smat_built = true;
+  }
   const size_t w = A.cx ? 2 : 1;
   std::vector<double> vals(w * nnz);
   for (int64_t p = 0; p < nnz; ++p) {
@@ -327,6 +435,10 @@ void mpk_csr_free(mpk_matrix *m) {
                   A.ord_f,  A.ord_b,  A.ord_fa,  A.ord_ba,
                   A.lev_f,  A.lev_b,  A.lev_fa,  A.lev_ba,
                   A.err,    m->rowflag, m->fscratch};
+  free_phase(A.smat.fwd);
+  free_phase(A.smat.bwd);
+  free_phase(A.smat_adj.fwd);
+  free_phase(A.smat_adj.bwd);
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete m;
@@ -392,6 +504,10 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   }
   if (res[3]) return fail(MPK_NUMERIC_BREAKDOWN, "non-finite value in ILU(0) factors");
   A.factored = true;
+  if (A.smat_built) {
+    gather_phase(A.lu, A.smat.fwd, A.n, A.cx, m->ctx->stream);
+    gather_phase(A.lu, A.smat.bwd, A.n, A.cx, m->ctx->stream);
+  }
   return MPK_OK;
 }
 
@@ -448,7 +564,7 @@ static int apply_dev(mpk_matrix *m, int k, const double *in_mc, double *fz,
   a.tick = A.tick;
   a.err = A.err;
   a.done = nullptr;
-  if (A.n > 0) launch_sweep(a, A.cx, adjoint != 0, st);
+  if (A.n > 0) do_sweep(A, a, adjoint != 0, st);
   int err = 0;
   CKR(cudaMemcpyAsync(&err, A.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   CKR(cudaStreamSynchronize(st));
@@ -762,7 +878,7 @@ int mpk_bench_apply(mpk_matrix *m, int k, int reps, double *ms_avg) {
   for (int r = 0; r < reps; ++r) {
     launch_sweep_reset(A.sw_y, dz, A.n, A.cx, nullptr, st);
     cudaEventRecord(e0, st);
-    launch_sweep(a, A.cx, false, st);
+    do_sweep(A, a, false, st);
     cudaEventRecord(e1, st);
     CKR(cudaEventSynchronize(e1));
     float ms = 0.f;

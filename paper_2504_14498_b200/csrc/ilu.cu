@@ -445,6 +445,160 @@ __global__ void __launch_bounds__(kSmemThreads, 1)
   if (bad) atomicOr(a.err, 1);
 }
 
+// ---------------------------------------------------------------------
+// Prefetched single-CTA sweep over level-ordered sweep matrices.  Row
+// descriptors, the first kPE entries, the right-hand side and the divisor
+// of the NEXT level are loaded into registers before the current level is
+// computed, so a level's critical path is SMEM reads + the FP64 chain +
+// one __syncthreads, not a chain of dependent L2 loads.
+// ---------------------------------------------------------------------
+constexpr int kPE = 6;             // entries per row held in registers
+constexpr int kMatsThreads = 768;  // 85 registers/thread
+
+// Entries + divisor of one row, fetched one level ahead.
+template <bool CX>
+struct RowEnt {
+  int col[kPE];
+  double vr[kPE], vi[CX ? kPE : 1];
+  double dr, di[CX ? 1 : 1];
+};
+
+template <bool CX, bool ADJ>
+__device__ __forceinline__ void ent_load(RowEnt<CX> &E, const SweepPhase &ph,
+                                         const int4 d, int r, bool fwd) {
+#pragma unroll
+  for (int q = 0; q < kPE; ++q) {
+    int c = 0;
+    double lr = 0.0, li = 0.0;
+    if (q < d.z) {
+      c = ph.col[d.y + q];
+      ldval<CX>(ph.val, d.y + q, lr, li);
+    }
+    E.col[q] = c;
+    E.vr[q] = lr;
+    if constexpr (CX) E.vi[q] = li;
+  }
+  double d0 = 1.0, d1 = 0.0;
+  if (fwd == ADJ && r >= 0) ldval<CX>(ph.dval, r, d0, d1);
+  E.dr = d0;
+  E.di[0] = d1;
+}
+
+// Process one row: acc = (fwd ? rhs : y_i) - sum val*v[col] in order,
+// then the divisor (forward adjoint: conj(U_ii); backward plain: U_ii).
+template <bool CX, bool ADJ>
+__device__ __forceinline__ void row_run(const int4 d, const RowEnt<CX> &E,
+                                        const SweepPhase &ph,
+                                        const SweepArgs &a, double *sv,
+                                        bool fwd, bool &bad) {
+  const int i = d.x;
+  double ar, ai;
+  sm_ld<CX>(sv, i, ar, ai);  // forward: rhs preloaded; backward: y_i
+#pragma unroll
+  for (int q = 0; q < kPE; ++q) {
+    if (q < d.z) {
+      double vr, vi;
+      sm_ld<CX>(sv, E.col[q], vr, vi);
+      if constexpr (CX)
+        mulsub<CX, ADJ>(ar, ai, E.vr[q], E.vi[q], vr, vi);
+      else
+        mulsub<CX, ADJ>(ar, ai, E.vr[q], 0.0, vr, vi);
+    }
+  }
+  for (int e = d.y + kPE; e < d.y + d.z; ++e) {
+    double lr, li, vr, vi;
+    ldval<CX>(ph.val, e, lr, li);
+    sm_ld<CX>(sv, ph.col[e], vr, vi);
+    mulsub<CX, ADJ>(ar, ai, lr, li, vr, vi);
+  }
+  double qr = ar, qi = ai;
+  if (fwd == ADJ) {
+    if constexpr (CX) {
+      py_cdiv(ar, ai, E.dr, ADJ ? -E.di[0] : E.di[0], qr, qi);
+    } else {
+      qr = ddiv(ar, E.dr);
+    }
+  }
+  sm_st<CX>(sv, i, qr, qi);
+  if (!fwd) {
+    bad = bad || !isfin(qr) || !isfin(qi);
+    if constexpr (CX)
+      reinterpret_cast<double2 *>(a.z)[i] = make_double2(qr, qi);
+    else
+      a.z[i] = qr;
+  }
+}
+
+// global level index g -> (phase, level) helpers over [fwd levels | bwd levels]
+struct GLev {
+  const int *fl, *bl;
+  int nf, nb;
+  __device__ __forceinline__ bool fwd(int g) const { return g < nf; }
+  __device__ __forceinline__ int lo(int g) const {
+    return g < nf ? fl[g] : bl[g - nf];
+  }
+  __device__ __forceinline__ int hi(int g) const {
+    return g < nf ? fl[g + 1] : bl[g - nf + 1];
+  }
+};
+
+template <bool CX, bool ADJ>
+__global__ void __launch_bounds__(kMatsThreads, 1)
+    sweep_mats_kernel(SweepArgs a, SweepMats m) {
+  if (a.done && *a.done) return;
+  extern __shared__ double sv[];
+  const int tid = threadIdx.x;
+  const int n = a.n, nf = m.fwd.nlev, nb = m.bwd.nlev, nl = nf + nb;
+  int *fl = reinterpret_cast<int *>(sv + (size_t)n * (CX ? 2 : 1));
+  int *bl = fl + nf + 1;
+  for (int t = tid; t <= nf; t += kMatsThreads) fl[t] = m.fwd.lev[t];
+  for (int t = tid; t <= nb; t += kMatsThreads) bl[t] = m.bwd.lev[t];
+  // forward right-hand side (demoted input) preloaded into the vector slots
+  for (int i = tid; i < n; i += kMatsThreads) {
+    double r, mm;
+    load_in<CX>(a, i, r, mm);
+    sm_st<CX>(sv, i, r, mm);
+  }
+  __syncthreads();
+  const GLev gl{fl, bl, nf, nb};
+  bool bad = false;
+  // pipeline registers: descriptor of levels g+1, g+2 and entries of g, g+1
+  const int4 none = make_int4(0, 0, 0, -1);
+  auto desc_at = [&](int g) -> int4 {
+    if (g >= nl) return none;
+    const int r = gl.lo(g) + tid;
+    if (r >= gl.hi(g)) return none;
+    int4 d = (gl.fwd(g) ? m.fwd : m.bwd).desc[r];
+    d.w = r;
+    return d;
+  };
+  int4 d0 = desc_at(0), d1 = desc_at(1), d2;
+  RowEnt<CX> e0, e1;
+  if (d0.w >= 0) ent_load<CX, ADJ>(e0, gl.fwd(0) ? m.fwd : m.bwd, d0, d0.w, gl.fwd(0));
+  for (int g = 0; g < nl; ++g) {
+    const bool fwd = gl.fwd(g);
+    const SweepPhase &ph = fwd ? m.fwd : m.bwd;
+    // stage 1: descriptor two levels ahead; stage 2: entries one ahead
+    d2 = desc_at(g + 2);
+    if (d1.w >= 0)
+      ent_load<CX, ADJ>(e1, gl.fwd(g + 1) ? m.fwd : m.bwd, d1, d1.w,
+                        gl.fwd(g + 1));
+    if (d0.w >= 0) row_run<CX, ADJ>(d0, e0, ph, a, sv, fwd, bad);
+    const int s = gl.lo(g), e = gl.hi(g);
+    for (int r = s + tid + kMatsThreads; r < e; r += kMatsThreads) {
+      int4 dx = ph.desc[r];
+      RowEnt<CX> ex;
+      ent_load<CX, ADJ>(ex, ph, dx, r, fwd);
+      row_run<CX, ADJ>(dx, ex, ph, a, sv, fwd, bad);
+    }
+    __syncthreads();
+    d0 = d1;
+    e0 = e1;
+    d1 = d2;
+  }
+  if (bad) atomicOr(a.err, 1);
+}
+
 // Level-synchronous single-CTA factorization (small n): rows of one level
 // are independent; __syncthreads orders the global-memory factor values
 // between levels within the block, so no per-row flags are needed.
@@ -580,9 +734,33 @@ static void launch_sweep_smem(const SweepArgs &a, cudaStream_t st) {
   sweep_smem_kernel<CX, ADJ><<<1, kSmemThreads, bytes, st>>>(a);
 }
 
+template <bool CX, bool ADJ>
+static void launch_sweep_mats_t(const SweepArgs &a, const SweepMats &m,
+                                cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sweep_mats_kernel<CX, ADJ>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemMax);
+    attr = true;
+  }
+  const size_t bytes = (size_t)a.n * (CX ? 16 : 8) +
+                       sizeof(int) * (m.fwd.nlev + m.bwd.nlev + 2);
+  sweep_mats_kernel<CX, ADJ><<<1, kMatsThreads, bytes, st>>>(a, m);
+}
+
+void launch_sweep_mats(const SweepArgs &a, const SweepMats &m, bool cx,
+                       bool adjoint, cudaStream_t st) {
+  ++tl_launches;
+  if (!cx && !adjoint) launch_sweep_mats_t<false, false>(a, m, st);
+  if (!cx && adjoint) launch_sweep_mats_t<false, true>(a, m, st);
+  if (cx && !adjoint) launch_sweep_mats_t<true, false>(a, m, st);
+  if (cx && adjoint) launch_sweep_mats_t<true, true>(a, m, st);
+}
+
 bool sweep_uses_smem(int n, bool cx) {
   return env_on("MPK_SWEEP_SMEM", true) &&
-         (size_t)n * (cx ? 16 : 8) <= kSmemMax;
+         (size_t)n * (cx ? 16 : 8) + 16384 <= kSmemMax;
 }
 
 void launch_sweep(const SweepArgs &a, bool cx, bool adjoint,

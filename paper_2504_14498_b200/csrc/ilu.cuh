@@ -42,8 +42,34 @@ struct SweepArgs {
   const int *done; // solver done flag (skip when set), may be null
 };
 
+// Level-ordered copy of one sweep phase ("sweep matrix"): position r in
+// level order holds row row[r] whose entries are col/val[ptr[r]..ptr[r+1])
+// in the reference's per-row order; dval[r] is the divisor (backward plain
+// / forward adjoint phases).  Values are gathered from the factors (src,
+// dsrc) after every factorization.
+struct SweepPhase {
+  int nlev = 0;
+  int *lev = nullptr;   // nlev+1 level pointers into [0, n]
+  int4 *desc = nullptr; // n: {row, first entry, entry count, 0} per position
+  int *col = nullptr;   // entries, level order, reference order per row
+  int *src = nullptr;   // entry -> index into lu
+  double *val = nullptr;
+  int *dsrc = nullptr;  // n, -1 if no divisor
+  double *dval = nullptr;
+  long long nent = 0;
+};
+
+struct SweepMats {
+  SweepPhase fwd, bwd;
+  bool conj = false;  // adjoint: values are conjugated at use
+};
+
 void launch_sweep(const SweepArgs &a, bool cx, bool adjoint,
                   cudaStream_t st);
+// single-CTA prefetched sweep over prepared sweep matrices (small n)
+void launch_sweep_mats(const SweepArgs &a, const SweepMats &m, bool cx,
+                       bool adjoint, cudaStream_t st);
+bool sweep_uses_smem(int n, bool cx);
 void launch_sweep_reset(double *y, double *z, int n, bool cx,
                         const int *done, cudaStream_t st);
 

@@ -31,6 +31,7 @@ struct State {
   Sc rho, rho_old, alpha, omega, beta, sigma, nrm, nrm0, thr, zeta, eta;
   long long it, max_iter, iterations, hist_len, hist_cap;
   long long body_runs;  // executions of the captured iteration graph
+  int pending;          // end-of-iteration test deferred to the next body
   int done, converged, breakdown, half_exit, have_nrm, sweep_err;
   double eps_rel, eps_abs;
   double relres, true_relres;
@@ -68,11 +69,26 @@ struct DMat {
   int *ord_f = nullptr, *ord_b = nullptr, *ord_fa = nullptr, *ord_ba = nullptr;
   int *lev_f = nullptr, *lev_b = nullptr, *lev_fa = nullptr, *lev_ba = nullptr;
   int levels_f = 0, levels_b = 0, levels_fa = 0, levels_ba = 0;
+  // level-ordered sweep matrices (single-CTA path, small n)
+  SweepMats smat, smat_adj;
+  bool smat_built = false, smat_adj_built = false;
   int *tick = nullptr;  // 4 ints: [0..1] sweep A, [2..3] sweep B
   int *err = nullptr;
   // host copies of the pattern (for building transposes)
   std::vector<int> h_rp, h_ci, h_dp;
 };
+
+// ILU(0)-mixed apply dispatch: prefetched single-CTA sweep over the
+// level-ordered sweep matrices when they exist (small n), else the
+// sync-free multi-CTA kernel.
+inline void do_sweep(const DMat &A, const SweepArgs &a, bool adjoint,
+                     cudaStream_t st) {
+  const bool mats = adjoint ? A.smat_adj_built : A.smat_built;
+  if (mats)
+    launch_sweep_mats(a, adjoint ? A.smat_adj : A.smat, A.cx, adjoint, st);
+  else
+    launch_sweep(a, A.cx, adjoint, st);
+}
 
 struct SolveParams {
   int method, k;

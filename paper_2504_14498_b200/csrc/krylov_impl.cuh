@@ -173,6 +173,20 @@ struct Solver : PlanBase {
   long long body_nodes = 0;
   bool cond_graph = true;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // side branch of the captured iteration (convergence tests overlapped
+  // with the next sweep): its own stream, fork/join events, partials
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t evf = nullptr, evj = nullptr;
+  double *part2 = nullptr;
+
+  void fork() {
+    cudaEventRecord(evf, st);
+    cudaStreamWaitEvent(st2, evf, 0);
+  }
+  void join() {
+    cudaEventRecord(evj, st2);
+    cudaStreamWaitEvent(st, evj, 0);
+  }
 
   Solver(DMat &A_, const SolveParams &p_, cudaStream_t st_, char *eb)
       : A(A_), p(p_), st(st_), errbuf(eb) {
@@ -195,12 +209,19 @@ struct Solver : PlanBase {
     }
     cudaEventCreate(&ev0);
     cudaEventCreate(&ev1);
+    cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&evf, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evj, cudaEventDisableTiming);
+    part2 = (double *)dalloc(sizeof(double) * 2 * kMaxGrid * 8);
   }
   ~Solver() override {
     if (ge) cudaGraphExecDestroy(ge);
     if (g) cudaGraphDestroy(g);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (evf) cudaEventDestroy(evf);
+    if (evj) cudaEventDestroy(evj);
+    if (st2) cudaStreamDestroy(st2);
     for (void *q : allocs) cudaFree(q);
   }
   void zero_mc(double *q) {
@@ -250,7 +271,7 @@ struct Solver : PlanBase {
     a.tick = A.tick + 2 * which;
     a.err = A.err;
     a.done = after_loop ? nullptr : done;
-    launch_sweep(a, CX, adjoint, st);
+    do_sweep(A, a, adjoint, st);
   }
   const double *head_re(const double *v) const { return v; }
   const double *head_im(const double *v) const { return CX ? v + K * ld : nullptr; }
@@ -311,25 +332,52 @@ struct Solver : PlanBase {
     double *H = hist;
     const DA a = da;
     const long long L = ld;
-    // F1: rho, omega check, beta
+    // F5+F1: [end of the previous iteration, deferred: rho_old = rho,
+    // ||r|| record + tests, iteration count] then [this iteration: rho,
+    // rho/omega zero tests, beta = (rho/rho_old)*(alpha/omega)].  The norm
+    // test (warp 0) and the two quotients of beta (warps 1, 2) overlap; beta
+    // is committed only if the solve continues.
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
           const Sc rho = finalize_slot<K, CX>(pt_, 0, G_, sm);
+          const bool pend = S_->pending != 0;
+          Sc ss = sc_zero();
+          if (pend) ss = finalize_slot<K, false>(pt_, 1, G_, sm);
+          Sc *xs = reinterpret_cast<Sc *>(sm);
+          if (threadIdx.x == 0) xs[2] = rho;
+          __syncthreads();
+          const long long itn = pend ? S_->it + 1 : S_->it;
+          const Sc rold = pend ? S_->rho : S_->rho_old;
+          const bool spec = itn > 1 && !s_is_zero<K, CX>(xs[2]) &&
+                            !s_is_zero<K, CX>(S_->omega);
+          if (spec && threadIdx.x == 32) xs[0] = s_div<K, CX>(xs[2], rold);
+          if (spec && threadIdx.x == 64) xs[1] = s_div<K, CX>(S_->alpha, S_->omega);
+          int *go = reinterpret_cast<int *>(xs + 3);
           if (threadIdx.x == 0) {
-            S_->rho = rho;
-            if (s_is_zero<K, CX>(rho)) {
-              finish_state(S_, S_->it, 0, kBdRhoZero);
-              return;
-            }
-            if (S_->it > 1) {
-              if (s_is_zero<K, CX>(S_->omega)) {
-                finish_state(S_, S_->it, 0, kBdOmegaZero);
-                return;
+            *go = 0;
+            bool stop = false;
+            if (pend) {  // solvers.py:322-327
+              S_->pending = 0;
+              S_->rho_old = S_->rho;
+              stop = check_nrm<K>(S_, H, ss);
+              if (!stop) {
+                next_iter(S_);
+                stop = S_->done != 0;
               }
-              S_->beta = s_mul<K, CX>(s_div<K, CX>(rho, S_->rho_old),
-                                      s_div<K, CX>(S_->alpha, S_->omega));
+            }
+            if (!stop) {  // solvers.py:291-300
+              S_->rho = xs[2];
+              if (s_is_zero<K, CX>(xs[2])) {
+                finish_state(S_, S_->it, 0, kBdRhoZero);
+              } else if (S_->it > 1 && s_is_zero<K, CX>(S_->omega)) {
+                finish_state(S_, S_->it, 0, kBdOmegaZero);
+              } else if (S_->it > 1) {
+                *go = 1;
+              }
             }
           }
+          __syncthreads();
+          if (*go && threadIdx.x == 0) S_->beta = s_mul<K, CX>(xs[0], xs[1]);
         });
     // K2: p = r (it 1) | p = r + beta*(p - omega*v); reset sweep buffers
     rows<K, CX, 0, 0>(n, done, part, st,
@@ -373,8 +421,8 @@ struct Solver : PlanBase {
             S_->alpha = s_div<K, CX>(S_->rho, sg);
           }
         });
-    // K5: s = r - alpha v ; norm2(s)
-    rows<K, CX, 0, 1>(n, done, part, st,
+    // K5: s = r - alpha v ; norm2(s) (partials in part2 for the side branch)
+    rows<K, CX, 0, 1>(n, done, part2, st,
                       [=] __device__(long long i, Red<K, CX, 0, 1> &red) {
                         double rr[K], ri[K], vr[K], vi[K], sr[K], si[K];
                         Rr.load(i, rr, ri);
@@ -386,8 +434,12 @@ struct Solver : PlanBase {
                         Y.set_sent(i);
                         SH.set_sent(i);
                       });
-    // F3: half-step test
-    fin(S, err, part, G, st,
+    // F3: half-step test on a side branch, overlapped with the sweep of s
+    // and the SpMV that follow (they only touch shat / t / partials, which
+    // are dead if F3 stops the solve; F4 and K8 run after the join and exit
+    // on the done flag).  No sweep-error check here: that belongs to F4.
+    fork();
+    fin(S, nullptr, part2, G, st2,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
           const Sc ss = finalize_slot<K, false>(pt_, 0, G_, sm);
           if (threadIdx.x == 0) {
@@ -406,6 +458,7 @@ struct Solver : PlanBase {
                         acc_hdot<K, CX>(red.h[0], tr, ti, tr, ti);
                         acc_hdot<K, CX>(red.h[1], tr, ti, sr, si);
                       });
+    join();
     // F4: omega
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
@@ -417,6 +470,7 @@ struct Solver : PlanBase {
               return;
             }
             S_->omega = s_div<K, CX>(ts, tt);
+            S_->pending = 1;  // K8 runs; its norm test happens in next F5+F1
           }
         });
     // K8: x = (x + alpha phat) + omega shat ; r = s - omega t ;
@@ -440,16 +494,8 @@ struct Solver : PlanBase {
                         acc_hdot<K, CX>(red.h[0], qr, qi, rr, ri);
                         acc_sumsq<K, CX>(red.nr[0], rr, ri);
                       });
-    // F5
-    fin(S, err, part, G, st,
-        [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
-          const Sc ss = finalize_slot<K, false>(pt_, 1, G_, sm);
-          if (threadIdx.x == 0) {
-            S_->rho_old = S_->rho;
-            if (check_nrm<K>(S_, H, ss)) return;
-            next_iter(S_);
-          }
-        });
+    // F5 (norm of r, rho_old = rho, iteration count) is deferred into the
+    // next body's first finalize, where it runs concurrently with beta.
   }
 
   void bicgstab_finish(const State &hs) {
@@ -719,29 +765,60 @@ struct Solver : PlanBase {
             bty = finalize_slot<K, CX>(pt_, 4, G_, sm);
             yt = finalize_slot<K, CX>(pt_, 5, G_, sm);
           }
-          if (threadIdx.x == 0) {
-            if (!more) {
+          if (!more) {
+            if (threadIdx.x == 0) {
               if (s_is_zero<K, CX>(btbt)) {
                 finish_state(S_, S_->it, 0, kBdLs);
                 return;
               }
               S_->zeta = s_div<K, CX>(btt, btbt);
               S_->eta = sc_zero();
-            } else {
-              const Sc delta = s_sub<K, CX>(s_mul<K, CX>(yy, btbt),
-                                            s_mul<K, CX>(ybt, bty));
-              if (s_is_zero<K, CX>(delta)) {
-                finish_state(S_, S_->it, 0, kBdLs);
-                return;
-              }
-              S_->eta = s_div<K, CX>(s_sub<K, CX>(s_mul<K, CX>(btbt, yt),
-                                                  s_mul<K, CX>(ybt, btt)),
-                                     delta);
-              S_->zeta = s_div<K, CX>(s_sub<K, CX>(s_mul<K, CX>(yy, btt),
-                                                   s_mul<K, CX>(bty, yt)),
-                                      delta);
+            }
+            return;
+          }
+          // 2x2 least squares (solvers.py:384-392): the six products, the
+          // three differences and the two quotients each run on their own
+          // warp (independent MC operations -> latency of 1 mul + 1 sub +
+          // 1 div instead of 6 + 3 + 2)
+          Sc *xs = reinterpret_cast<Sc *>(sm);  // 6 slots (sm free here)
+          if (threadIdx.x == 0) {
+            xs[0] = yy;
+            xs[1] = btbt;
+            xs[2] = ybt;
+            xs[3] = bty;
+            xs[4] = yt;
+            xs[5] = btt;
+          }
+          __syncthreads();
+          Sc pr = sc_zero();
+          const int w = threadIdx.x >> 5, lane0 = (threadIdx.x & 31) == 0;
+          if (lane0 && w < 6) {
+            const Sc a0 = xs[0], a1 = xs[1], a2 = xs[2], a3 = xs[3],
+                     a4 = xs[4], a5 = xs[5];
+            switch (w) {
+              case 0: pr = s_mul<K, CX>(a0, a1); break;  // yy*btbt
+              case 1: pr = s_mul<K, CX>(a2, a3); break;  // ybt*bty
+              case 2: pr = s_mul<K, CX>(a1, a4); break;  // btbt*yt
+              case 3: pr = s_mul<K, CX>(a2, a5); break;  // ybt*btt
+              case 4: pr = s_mul<K, CX>(a0, a5); break;  // yy*btt
+              default: pr = s_mul<K, CX>(a3, a4); break; // bty*yt
             }
           }
+          __syncthreads();
+          if (lane0 && w < 6) xs[w] = pr;
+          __syncthreads();
+          Sc df = sc_zero();
+          if (lane0 && w < 3) df = s_sub<K, CX>(xs[2 * w], xs[2 * w + 1]);
+          __syncthreads();
+          if (lane0 && w < 3) xs[w] = df;  // delta, eta_num, zeta_num
+          __syncthreads();
+          const bool sing = s_is_zero<K, CX>(xs[0]);
+          if (sing) {
+            if (threadIdx.x == 0) finish_state(S_, S_->it, 0, kBdLs);
+            return;
+          }
+          if (threadIdx.x == 0) S_->eta = s_div<K, CX>(xs[1], xs[0]);
+          if (threadIdx.x == 32) S_->zeta = s_div<K, CX>(xs[2], xs[0]);
         });
     // K8: u, z, yhat, r updates ; norm2(r) [slot 1], rho_new [slot 0]
     rows<K, CX, 1, 1>(n, done, part, st,
@@ -790,18 +867,29 @@ struct Solver : PlanBase {
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
           const Sc rn = finalize_slot<K, CX>(pt_, 0, G_, sm);
           const Sc ss = finalize_slot<K, false>(pt_, 1, G_, sm);
+          // norm test (warp 0) and the two quotients of beta (warps 1, 2)
+          // run concurrently; beta is only committed if the test continues
+          Sc *xs = reinterpret_cast<Sc *>(sm);
+          if (threadIdx.x == 0) xs[2] = rn;
+          __syncthreads();
+          const bool zz = s_is_zero<K, CX>(S_->zeta), zr = s_is_zero<K, CX>(S_->rho);
+          if (threadIdx.x == 32 && !zz && !zr) xs[0] = s_div<K, CX>(S_->alpha, S_->zeta);
+          if (threadIdx.x == 64 && !zz && !zr) xs[1] = s_div<K, CX>(xs[2], S_->rho);
+          int *stop = reinterpret_cast<int *>(xs + 3);
           if (threadIdx.x == 0) {
-            if (check_nrm<K>(S_, H, ss)) return;
-            if (s_is_zero<K, CX>(S_->zeta)) {
+            *stop = 1;
+            if (check_nrm<K>(S_, H, ss)) {
+            } else if (zz) {
               finish_state(S_, S_->it, 0, kBdZetaZero);
-              return;
-            }
-            if (s_is_zero<K, CX>(S_->rho)) {
+            } else if (zr) {
               finish_state(S_, S_->it, 0, kBdRhoZero);
-              return;
+            } else {
+              *stop = 0;
             }
-            S_->beta = s_mul<K, CX>(s_div<K, CX>(S_->alpha, S_->zeta),
-                                    s_div<K, CX>(rn, S_->rho));
+          }
+          __syncthreads();
+          if (threadIdx.x == 0 && !*stop) {
+            S_->beta = s_mul<K, CX>(xs[0], xs[1]);
             S_->rho = rn;
             next_iter(S_);
           }

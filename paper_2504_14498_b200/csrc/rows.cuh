@@ -104,9 +104,23 @@ __global__ void __launch_bounds__(kBlock)
   if constexpr (NH + NN > 0) red.store(part, smem);
 }
 
+// Every kernel of the solver asks for the max-shared-memory carveout, so
+// SMs never have to be reconfigured between the SMEM-resident sweep and the
+// other kernels (which would serialise concurrent solves on other streams).
+template <class KFn>
+inline void prefer_max_smem(KFn kfn) {
+  static bool done_once = false;
+  if (!done_once) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    done_once = true;
+  }
+}
+
 template <int K, bool CX, int NH, int NN, class F>
 void rows(long long n, const int *done, double *part, cudaStream_t st, F f) {
   ++tl_launches;
+  prefer_max_smem(rows_kernel<K, CX, NH, NN, F>);
   rows_kernel<K, CX, NH, NN, F><<<grid_for(n), kBlock, 0, st>>>(n, done, part, f);
 }
 
@@ -132,6 +146,7 @@ template <class F>
 void fin(State *S, const int *err, const double *part, int G, cudaStream_t st,
          F f) {
   ++tl_launches;
+  prefer_max_smem(fin_kernel<F>);
   fin_kernel<F><<<1, kBlock, 0, st>>>(S, err, part, G, f);
 }
 
