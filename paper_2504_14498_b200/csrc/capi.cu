@@ -30,12 +30,22 @@ struct mpk_ctx {
   cudaStream_t stream;
 };
 
+// Per-k device I/O buffers of mpk_solve, kept across calls (no
+// cudaMalloc/cudaFree -- which synchronise the device -- on the call path).
+struct IoBufs {
+  double *b = nullptr, *x = nullptr, *stage = nullptr, *hist = nullptr;
+  long long hist_cap = 0;
+};
+
 struct mpk_matrix {
   mpk_ctx *ctx;
   DMat A;
   int *rowflag = nullptr;
   int *fscratch = nullptr;  // [0..1] ticket, [2] bad_row, [3] nonfinite
   float factor_ms = 0.f;
+  IoBufs io[5];
+  std::vector<double> h_vals;  // complex interleave staging
+  int *hres = nullptr;         // pinned factor init/result words
 };
 
 static thread_local std::string g_err;
@@ -155,6 +165,8 @@ static void build_phase(SweepPhase &ph, int n, bool cx,
     dsrc[r] = div(i);
   }
   ph.nlev = nlev;
+  ph.maxw = 0;
+  for (int L = 0; L < nlev; ++L) ph.maxw = std::max(ph.maxw, lev[L + 1] - lev[L]);
   ph.nent = (long long)col.size();
   upload(&ph.lev, lev, st);
   upload(&ph.desc, desc, st);
@@ -435,6 +447,12 @@ void mpk_csr_free(mpk_matrix *m) {
                   A.ord_f,  A.ord_b,  A.ord_fa,  A.ord_ba,
                   A.lev_f,  A.lev_b,  A.lev_fa,  A.lev_ba,
                   A.err,    m->rowflag, m->fscratch};
+  if (m->hres) cudaFreeHost(m->hres);
+  for (auto &B : m->io) {
+    void *q[] = {B.b, B.x, B.stage, B.hist};
+    for (void *v : q)
+      if (v) cudaFree(v);
+  }
   free_phase(A.smat.fwd);
   free_phase(A.smat.bwd);
   free_phase(A.smat_adj.fwd);
@@ -463,8 +481,13 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   CKR(cudaMemcpyAsync(A.lu, A.val, sizeof(double) * w * A.nnz,
                       cudaMemcpyDeviceToDevice, st));
   CKR(cudaMemsetAsync(m->rowflag, 0, sizeof(int) * (A.n + 1), st));
-  int init[4] = {0, 0, INT_MAX, 0};
-  CKR(cudaMemcpyAsync(m->fscratch, init, sizeof(init), cudaMemcpyHostToDevice,
+  if (!m->hres) CKR(cudaMallocHost(&m->hres, sizeof(int) * 8));
+  int *init = m->hres;  // pinned (pageable copies serialise concurrent solves)
+  init[0] = 0;
+  init[1] = 0;
+  init[2] = INT_MAX;
+  init[3] = 0;
+  CKR(cudaMemcpyAsync(m->fscratch, init, sizeof(int) * 4, cudaMemcpyHostToDevice,
                       st));
   FactorArgs fa{};
   fa.n = A.n;
@@ -485,8 +508,8 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   cudaEventRecord(e0, st);
   if (A.n > 0) launch_factor(fa, A.cx, st);
   cudaEventRecord(e1, st);
-  int res[4];
-  CKR(cudaMemcpyAsync(res, m->fscratch, sizeof(res), cudaMemcpyDeviceToHost,
+  int *res = m->hres + 4;
+  CKR(cudaMemcpyAsync(res, m->fscratch, sizeof(int) * 4, cudaMemcpyDeviceToHost,
                       st));
   CKR(cudaStreamSynchronize(st));
   CKR(cudaGetLastError());
@@ -964,32 +987,85 @@ int mpk_solve(mpk_matrix *m, int method, int k, double eps_rel,
   DMat &A = m->A;
   if (A.cx != (b_im != nullptr))
     return fail(MPK_INVALID, "matrix/vector field mismatch");
+  if (k < 2 || k > 4)
+    return fail(MPK_INVALID, "mixed SpMV needs a working precision above binary64");
   CKR(cudaSetDevice(m->ctx->device));
   cudaStream_t st = m->ctx->stream;
-  double *db = nullptr, *dx = nullptr, *dh = nullptr;
-  int rc = to_dev_planar(m->ctx, A.n, k, b_re, b_im, &db);
-  if (rc) return rc;
-  const long long L = plane_ld(A.n);
-  CKR(cudaMalloc(&dx, sizeof(double) * k * (A.cx ? 2 : 1) * L + 16));
-  CKR(cudaMemsetAsync(dx, 0, sizeof(double) * k * (A.cx ? 2 : 1) * L + 16, st));
+  const long long n = A.n, L = plane_ld(A.n);
+  const int c = A.cx ? 2 : 1;
+  IoBufs &B = m->io[k];
+  if (!B.b) {
+    CKR(cudaMalloc(&B.b, sizeof(double) * k * c * L + 16));
+    CKR(cudaMalloc(&B.x, sizeof(double) * k * c * L + 16));
+    CKR(cudaMalloc(&B.stage, sizeof(double) * k * c * (n ? n : 1)));
+  }
   const int64_t hc = hist && hist_cap > 0 ? hist_cap : 0;
-  CKR(cudaMalloc(&dh, sizeof(double) * k * (hc ? hc : 1)));
-  rc = solve_core(m, method, k, eps_rel, eps_abs, max_iter, db, dx, dh, hc, rep);
-  if (rc == MPK_OK && rep->has_x)
-    rc = from_dev_planar(m->ctx, A.n, k, dx, x_re, A.cx ? x_im : nullptr);
+  if (hc > B.hist_cap) {
+    if (B.hist) cudaFree(B.hist);
+    CKR(cudaMalloc(&B.hist, sizeof(double) * k * hc));
+    B.hist_cap = hc;
+  }
+  // H2D of b (the caller's buffer, pinned for full bandwidth) -> planar
+  CKR(cudaMemsetAsync(B.b, 0, sizeof(double) * k * c * L, st));
+  CKR(cudaMemsetAsync(B.x, 0, sizeof(double) * k * c * L, st));
+  if (n > 0) {
+    CKR(cudaMemcpyAsync(B.stage, b_re, sizeof(double) * n * k,
+                        cudaMemcpyHostToDevice, st));
+    if (A.cx)
+      CKR(cudaMemcpyAsync(B.stage + n * k, b_im, sizeof(double) * n * k,
+                          cudaMemcpyHostToDevice, st));
+    launch_to_planar(n, k, B.stage, A.cx ? B.stage + n * k : nullptr, B.b, st);
+  }
+  int rc = solve_core(m, method, k, eps_rel, eps_abs, max_iter, B.b, B.x,
+                      hc ? B.hist : nullptr, hc, rep);
+  if (rc == MPK_OK && rep->has_x && n > 0) {
+    launch_from_planar(n, k, B.x, B.stage, A.cx ? B.stage + n * k : nullptr, st);
+    CKR(cudaMemcpyAsync(x_re, B.stage, sizeof(double) * n * k,
+                        cudaMemcpyDeviceToHost, st));
+    if (A.cx)
+      CKR(cudaMemcpyAsync(x_im, B.stage + n * k, sizeof(double) * n * k,
+                          cudaMemcpyDeviceToHost, st));
+  }
   if (rc == MPK_OK && hc) {
     const int64_t cnt = rep->hist_len < hc ? rep->hist_len : hc;
     if (cnt > 0)
-      CKR(cudaMemcpy(hist, dh, sizeof(double) * k * cnt, cudaMemcpyDeviceToHost));
+      CKR(cudaMemcpyAsync(hist, B.hist, sizeof(double) * k * cnt,
+                          cudaMemcpyDeviceToHost, st));
   }
-  cudaFree(db);
-  cudaFree(dx);
-  cudaFree(dh);
+  CKR(cudaStreamSynchronize(st));
   rep->total_ms = std::chrono::duration<double, std::milli>(
                       std::chrono::steady_clock::now() - t0)
                       .count();
   rep->launches = tl_launches - l0;
   return rc;
+}
+
+int mpk_csr_set_values(mpk_matrix *m, const double *val_re,
+                       const double *val_im) {
+  DMat &A = m->A;
+  if (A.cx != (val_im != nullptr))
+    return fail(MPK_INVALID, "field mismatch: matrix/values");
+  CKR(cudaSetDevice(m->ctx->device));
+  cudaStream_t st = m->ctx->stream;
+  if (A.nnz > 0) {
+    if (!A.cx) {
+      CKR(cudaMemcpyAsync(A.val, val_re, sizeof(double) * A.nnz,
+                          cudaMemcpyHostToDevice, st));
+    } else {
+      m->h_vals.resize(2 * A.nnz);
+      for (long long p = 0; p < A.nnz; ++p) {
+        m->h_vals[2 * p] = val_re[p];
+        m->h_vals[2 * p + 1] = val_im[p];
+      }
+      CKR(cudaMemcpyAsync(A.val, m->h_vals.data(), sizeof(double) * 2 * A.nnz,
+                          cudaMemcpyHostToDevice, st));
+    }
+    if (A.at_rp) gather(A.val, A.at_perm, A.at_val, A.nnz, A.cx, st);
+  }
+  A.factored = false;
+  A.adj_ready = false;
+  CKR(cudaStreamSynchronize(st));
+  return MPK_OK;
 }
 
 int mpk_solve_batch(int nsys, mpk_matrix **ms, int method, int k,
@@ -1022,3 +1098,34 @@ int mpk_solve_batch(int nsys, mpk_matrix **ms, int method, int k,
 }
 
 }  // extern "C"
+
+extern "C" int mpk_run_jobs(mpk_job *jobs, int njobs, int device_resident) {
+  if (njobs <= 0) return MPK_OK;
+  auto run = [&](int j) {
+    mpk_job &J = jobs[j];
+    int rc = MPK_OK;
+    if (!device_resident && J.val_re)
+      rc = mpk_csr_set_values(J.m, J.val_re, J.val_im);
+    if (rc == MPK_OK) {
+      if (device_resident)
+        rc = mpk_solve_dev(J.m, J.method, J.k, J.eps_rel, J.eps_abs, J.max_iter,
+                           J.b_re, J.x_re, J.hist, J.hist_cap, &J.rep);
+      else
+        rc = mpk_solve(J.m, J.method, J.k, J.eps_rel, J.eps_abs, J.max_iter,
+                       J.b_re, J.b_im, J.x_re, J.x_im, J.hist, J.hist_cap,
+                       &J.rep);
+    }
+    J.rc = rc;
+  };
+  if (njobs == 1) {
+    run(0);
+  } else {
+    std::vector<std::thread> th;
+    th.reserve(njobs);
+    for (int j = 0; j < njobs; ++j) th.emplace_back(run, j);
+    for (auto &t : th) t.join();
+  }
+  for (int j = 0; j < njobs; ++j)
+    if (jobs[j].rc) return jobs[j].rc;
+  return MPK_OK;
+}

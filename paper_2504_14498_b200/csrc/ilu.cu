@@ -1,5 +1,6 @@
 // ilu.cu -- sync-free binary64 ILU(0) factorization and sweeps (see ilu.cuh)
 #include <climits>
+#include <algorithm>
 #include <cstdlib>
 
 #include "ilu.cuh"
@@ -551,10 +552,11 @@ __global__ void __launch_bounds__(kMatsThreads, 1)
   const int n = a.n, nf = m.fwd.nlev, nb = m.bwd.nlev, nl = nf + nb;
   int *fl = reinterpret_cast<int *>(sv + (size_t)n * (CX ? 2 : 1));
   int *bl = fl + nf + 1;
-  for (int t = tid; t <= nf; t += kMatsThreads) fl[t] = m.fwd.lev[t];
-  for (int t = tid; t <= nb; t += kMatsThreads) bl[t] = m.bwd.lev[t];
+  const int T = blockDim.x;  // sized to the widest level (<= kMatsThreads)
+  for (int t = tid; t <= nf; t += T) fl[t] = m.fwd.lev[t];
+  for (int t = tid; t <= nb; t += T) bl[t] = m.bwd.lev[t];
   // forward right-hand side (demoted input) preloaded into the vector slots
-  for (int i = tid; i < n; i += kMatsThreads) {
+  for (int i = tid; i < n; i += T) {
     double r, mm;
     load_in<CX>(a, i, r, mm);
     sm_st<CX>(sv, i, r, mm);
@@ -585,7 +587,7 @@ __global__ void __launch_bounds__(kMatsThreads, 1)
                         gl.fwd(g + 1));
     if (d0.w >= 0) row_run<CX, ADJ>(d0, e0, ph, a, sv, fwd, bad);
     const int s = gl.lo(g), e = gl.hi(g);
-    for (int r = s + tid + kMatsThreads; r < e; r += kMatsThreads) {
+    for (int r = s + tid + T; r < e; r += T) {
       int4 dx = ph.desc[r];
       RowEnt<CX> ex;
       ent_load<CX, ADJ>(ex, ph, dx, r, fwd);
@@ -746,7 +748,9 @@ static void launch_sweep_mats_t(const SweepArgs &a, const SweepMats &m,
   }
   const size_t bytes = (size_t)a.n * (CX ? 16 : 8) +
                        sizeof(int) * (m.fwd.nlev + m.bwd.nlev + 2);
-  sweep_mats_kernel<CX, ADJ><<<1, kMatsThreads, bytes, st>>>(a, m);
+  int T = ((std::max(m.fwd.maxw, m.bwd.maxw) + 31) / 32) * 32;
+  T = T < 32 ? 32 : (T > kMatsThreads ? kMatsThreads : T);
+  sweep_mats_kernel<CX, ADJ><<<1, T, bytes, st>>>(a, m);
 }
 
 void launch_sweep_mats(const SweepArgs &a, const SweepMats &m, bool cx,

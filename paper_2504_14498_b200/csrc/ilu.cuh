@@ -49,6 +49,7 @@ struct SweepArgs {
 // dsrc) after every factorization.
 struct SweepPhase {
   int nlev = 0;
+  int maxw = 0;         // widest level (rows)
   int *lev = nullptr;   // nlev+1 level pointers into [0, n]
   int4 *desc = nullptr; // n: {row, first entry, entry count, 0} per position
   int *col = nullptr;   // entries, level order, reference order per row

@@ -178,6 +178,8 @@ struct Solver : PlanBase {
   cudaStream_t st2 = nullptr;
   cudaEvent_t evf = nullptr, evj = nullptr;
   double *part2 = nullptr;
+  State *hp = nullptr;  // pinned host staging of the device State (x2)
+  int *hpi = nullptr;
 
   void fork() {
     cudaEventRecord(evf, st);
@@ -213,6 +215,9 @@ struct Solver : PlanBase {
     cudaEventCreateWithFlags(&evf, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&evj, cudaEventDisableTiming);
     part2 = (double *)dalloc(sizeof(double) * 2 * kMaxGrid * 8);
+    cudaMallocHost(&hp, sizeof(State) * 2);
+    cudaMallocHost(&hpi, sizeof(int) * 4);
+    *hpi = 0;
   }
   ~Solver() override {
     if (ge) cudaGraphExecDestroy(ge);
@@ -222,6 +227,8 @@ struct Solver : PlanBase {
     if (evf) cudaEventDestroy(evf);
     if (evj) cudaEventDestroy(evj);
     if (st2) cudaStreamDestroy(st2);
+    if (hp) cudaFreeHost(hp);
+    if (hpi) cudaFreeHost(hpi);
     for (void *q : allocs) cudaFree(q);
   }
   void zero_mc(double *q) {
@@ -1153,7 +1160,8 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   hs.eps_abs = p.eps_abs;
   hs.relres = NAN;
   hs.true_relres = NAN;
-  CK(cudaMemcpyAsync(sv->S, &hs, sizeof(State), cudaMemcpyHostToDevice, st));
+  *sv->hp = hs;  // pinned staging: pageable copies serialise concurrent solves
+  CK(cudaMemcpyAsync(sv->S, sv->hp, sizeof(State), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(A.err, 0, sizeof(int), st));
   sv->alloc_common(d_b);
   cudaEventRecord(sv->ev0, st);
@@ -1214,15 +1222,17 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
         CK(cudaGraphLaunch(sv->ge, st));
         tl_launches += sv->body_nodes;
       }
-      CK(cudaMemcpyAsync(&probe, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(sv->hp + 1, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      probe = sv->hp[1];
       if (probe.done) break;
       if (chunk < 64) chunk *= 2;
     }
   }
   cudaEventRecord(sv->ev1, st);
-  CK(cudaMemcpyAsync(&hs, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(sv->hp, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  hs = *sv->hp;
   if (use_cond) tl_launches += sv->body_nodes * hs.body_runs;
   if (!hs.done) {
     // loop ran out without a device-side stop (max_iter reached)
@@ -1251,13 +1261,16 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   if (hs.breakdown == kBdNumericSweep) return sweep_fail();
   sv->finish(hs, d_x);
   int e_after = 0;
-  if (p.method == kGPBiCG && !(hs.iterations == 0 && hs.converged))
-    CK(cudaMemcpyAsync(&e_after, A.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  const bool chk_after = p.method == kGPBiCG && !(hs.iterations == 0 && hs.converged);
+  if (chk_after)
+    CK(cudaMemcpyAsync(sv->hpi, A.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   relres_kernel<K><<<1, 1, 0, st>>>(sv->S);
   tl_launches += 2;  // relres + true-residual finalize
   sv->true_residual(d_x);
-  CK(cudaMemcpyAsync(&hs, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(sv->hp, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  hs = *sv->hp;
+  if (chk_after) e_after = *sv->hpi;
   CK(cudaGetLastError());
   if (e_after) return sweep_fail();
   out->iterations = hs.iterations;
