@@ -4,6 +4,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -128,7 +129,7 @@ __global__ void gather_phase_kernel(const double *lu, SweepPhase ph, int n,
                                     int cx) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t < ph.nent) {
-    const int s = ph.src[t];  // -1: ELL padding
+    const int s = ph.src[t];
     if (cx)
       reinterpret_cast<double2 *>(ph.val)[t] =
           s >= 0 ? reinterpret_cast<const double2 *>(lu)[s] : make_double2(0.0, 0.0);
@@ -145,37 +146,203 @@ __global__ void gather_phase_kernel(const double *lu, SweepPhase ph, int n,
   }
 }
 
-// Build one phase: rows in level order `ord` (level pointers `lev`), row i's
-// entries (col, src) produced by `ent(i, cb)` in the reference's order and
-// its divisor source `div(i)` (-1 if none).
+// Host copy of one phase: rows in level order `ord` (level pointers `lev`),
+// row i's entries (col, src) produced by `ent(i, cb)` in the reference's
+// order and its divisor source `div(i)` (-1 if none).
+struct HPhase {
+  int nlev = 0, maxw = 0;
+  std::vector<int> lev;
+  std::vector<int4> desc;  // per position {row, first entry, count, 0}
+  std::vector<int> col, src, dsrc;
+};
+
 template <class Ent, class Div>
-static void build_phase(SweepPhase &ph, int n, bool cx,
-                        const std::vector<int> &ord, const std::vector<int> &lev,
-                        int nlev, Ent ent, Div div, cudaStream_t st) {
-  std::vector<int4> desc(n);
-  std::vector<int> col, src, dsrc(n);
+static HPhase make_hphase(int n, const std::vector<int> &ord,
+                          const std::vector<int> &lev, int nlev, Ent ent,
+                          Div div) {
+  HPhase h;
+  h.nlev = nlev;
+  h.lev = lev;
+  h.desc.resize(n);
+  h.dsrc.resize(n);
   for (int r = 0; r < n; ++r) {
     const int i = ord[r];
-    const int e0 = (int)col.size();
+    const int e0 = (int)h.col.size();
     ent(i, [&](int c, int s) {
-      col.push_back(c);
-      src.push_back(s);
+      h.col.push_back(c);
+      h.src.push_back(s);
     });
-    desc[r] = make_int4(i, e0, (int)col.size() - e0, 0);
-    dsrc[r] = div(i);
+    h.desc[r] = make_int4(i, e0, (int)h.col.size() - e0, 0);
+    h.dsrc[r] = div(i);
   }
-  ph.nlev = nlev;
-  ph.maxw = 0;
-  for (int L = 0; L < nlev; ++L) ph.maxw = std::max(ph.maxw, lev[L + 1] - lev[L]);
-  ph.nent = (long long)col.size();
-  upload(&ph.lev, lev, st);
-  upload(&ph.desc, desc, st);
-  upload(&ph.col, col, st);
-  upload(&ph.src, src, st);
-  upload(&ph.dsrc, dsrc, st);
+  for (int L = 0; L < nlev; ++L) h.maxw = std::max(h.maxw, lev[L + 1] - lev[L]);
+  return h;
+}
+
+static void build_phase(SweepPhase &ph, int n, bool cx, const HPhase &h,
+                        cudaStream_t st) {
+  ph.nlev = h.nlev;
+  ph.maxw = h.maxw;
+  ph.nent = (long long)h.col.size();
+  upload(&ph.lev, h.lev, st);
+  upload(&ph.desc, h.desc, st);
+  upload(&ph.col, h.col, st);
+  upload(&ph.src, h.src, st);
+  upload(&ph.dsrc, h.dsrc, st);
   const size_t w = cx ? 2 : 1;
-  cudaMalloc(&ph.val, sizeof(double) * w * (col.size() + 1));
+  cudaMalloc(&ph.val, sizeof(double) * w * (h.col.size() + 1));
   cudaMalloc(&ph.dval, sizeof(double) * w * (n + 1));
+}
+
+static int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// Cluster sweep plan (ilu.cuh CSweep) for the phase pair (f, b).  Rows of a
+// level are split over the C CTAs in contiguous chunks of about equal work;
+// a row's storage slot is fixed by its forward-phase CTA.  Returns false if
+// the plan does not fit in shared memory.
+static bool build_cplan(CSweep &p, int n, bool cx, const HPhase &f,
+                        const HPhase &b, cudaStream_t st) {
+  const int cmax = env_int("MPK_CSWEEP_C", 8);
+  if (cmax <= 0 || n == 0) return false;
+  const int maxw = std::max(f.maxw, b.maxw);
+  int C = std::min(cmax, std::max(1, maxw / env_int("MPK_CSWEEP_ROWS", 24)));
+  if (C > 16) C = 16;
+  const int nl = f.nlev + b.nlev;
+  if (nl > 8192) return false;
+  // split of every level: cta[r] for each position of each phase
+  auto split = [&](const HPhase &h, std::vector<int> &cta) {
+    cta.assign(n, 0);
+    for (int L = 0; L < h.nlev; ++L) {
+      const int lo = h.lev[L], hi = h.lev[L + 1];
+      long long W = 0;
+      for (int r = lo; r < hi; ++r) W += h.desc[r].z + 4;
+      long long acc = 0;
+      for (int r = lo; r < hi; ++r) {
+        cta[r] = (int)std::min<long long>(C - 1, acc * C / W);
+        acc += h.desc[r].z + 4;
+      }
+    }
+  };
+  std::vector<int> cf, cb;
+  split(f, cf);
+  split(b, cb);
+  std::vector<int> pk(n), nslot(C, 0);
+  std::vector<std::vector<int>> srow(C);
+  for (int r = 0; r < n; ++r) {  // level order -> slots in compute order
+    const int i = f.desc[r].x, c = cf[r];
+    pk[i] = (c << 24) | nslot[c]++;
+    srow[c].push_back(i);
+  }
+  std::vector<int4> seg((size_t)nl * C);
+  std::vector<CDesc> desc;
+  std::vector<int> dsrc, esrc, epk;
+  desc.reserve(2 * (size_t)n);
+  int maxdesc = 0, maxent = 0;
+  for (int g = 0; g < nl; ++g) {
+    const bool fw = g < f.nlev;
+    const HPhase &h = fw ? f : b;
+    const std::vector<int> &cta = fw ? cf : cb;
+    const int L = fw ? g : g - f.nlev;
+    for (int c = 0; c < C; ++c) {
+      const int d0 = (int)desc.size(), x0 = (int)esrc.size();
+      for (int r = h.lev[L]; r < h.lev[L + 1]; ++r) {
+        if (cta[r] != c) continue;
+        const int4 hd = h.desc[r];
+        CDesc d{};
+        d.init = pk[hd.x];
+        d.out = pk[hd.x];
+        d.e0 = (int)esrc.size() - x0;
+        d.cnt = hd.z;
+        d.row = hd.x;
+        d.hasdiv = h.dsrc[r] >= 0 ? 1 : 0;
+        d.dr = 1.0;
+        d.di = 0.0;
+        desc.push_back(d);
+        dsrc.push_back(h.dsrc[r]);
+        for (int q = hd.y; q < hd.y + hd.z; ++q) {
+          esrc.push_back(h.src[q]);
+          epk.push_back(pk[h.col[q]]);
+        }
+      }
+      const int nd = (int)desc.size() - d0, ne = (int)esrc.size() - x0;
+      seg[(size_t)g * C + c] = make_int4(d0, nd, x0, ne);
+      maxdesc = std::max(maxdesc, nd);
+      maxent = std::max(maxent, ne);
+    }
+  }
+  int maxslots = 0;
+  for (int c = 0; c < C; ++c) maxslots = std::max(maxslots, nslot[c]);
+  const size_t esz = cx ? sizeof(CEntC) : sizeof(CEntR);
+  const size_t smem = 48 + (size_t)nl * 16 +
+                      ((size_t)maxslots * (cx ? 16 : 8) + 15) / 16 * 16 +
+                      3 * (size_t)maxdesc * sizeof(CDesc) + 3 * (size_t)maxent * esz;
+  if (smem > csweep_smem_limit()) return false;
+  p.C = C;
+  p.T = std::min(1024, std::max(64, (maxdesc + 31) / 32 * 32));
+  p.nl = nl;
+  p.nf = f.nlev;
+  p.ndesc = (long long)desc.size();
+  p.nent = (long long)esrc.size();
+  p.maxslots = maxslots;
+  p.maxdesc = maxdesc;
+  p.maxent = maxent;
+  p.smem = smem;
+  std::vector<int> slot_row, slot_off(C + 1, 0);
+  for (int c = 0; c < C; ++c) {
+    slot_off[c + 1] = slot_off[c] + nslot[c];
+    slot_row.insert(slot_row.end(), srow[c].begin(), srow[c].end());
+  }
+  upload(&p.seg, seg, st);
+  upload(&p.desc, desc, st);
+  upload(&p.dsrc, dsrc, st);
+  upload(&p.esrc, esrc, st);
+  upload(&p.slot_row, slot_row, st);
+  upload(&p.slot_off, slot_off, st);
+  if (cx) {
+    std::vector<CEntC> e(esrc.size());
+    for (size_t t = 0; t < e.size(); ++t) e[t] = CEntC{0.0, 0.0, epk[t], {0, 0, 0}};
+    CEntC *d = nullptr;
+    upload(&d, e, st);
+    p.ent = d;
+  } else {
+    std::vector<CEntR> e(esrc.size());
+    for (size_t t = 0; t < e.size(); ++t) e[t] = CEntR{0.0, epk[t], 0};
+    CEntR *d = nullptr;
+    upload(&d, e, st);
+    p.ent = d;
+  }
+  cudaStreamSynchronize(st);  // host staging vectors die here
+  return true;
+}
+
+static void free_cplan(CSweep &p) {
+  void *q[] = {p.seg, p.desc, p.dsrc, p.ent, p.esrc, p.slot_row, p.slot_off};
+  for (void *v : q)
+    if (v) cudaFree(v);
+  p = CSweep{};
+}
+
+// Sweep structures of one apply direction: the single-CTA sweep matrices
+// when the vector fits one SM, and the cluster plan when it fits a cluster.
+static bool build_sweeps(SweepMats &sm, int n, bool cx, const HPhase &f,
+                         const HPhase &b, cudaStream_t st) {
+  bool single = false;
+  if (sweep_uses_smem(n, cx)) {
+    build_phase(sm.fwd, n, cx, f, st);
+    build_phase(sm.bwd, n, cx, b, st);
+    single = true;
+  }
+  if (env_int("MPK_CSWEEP", 1)) build_cplan(sm.cs, n, cx, f, b, st);
+  return single;
+}
+
+static bool csweep_candidate(int n, bool cx) {
+  // vector spread over at most 16 SMs with room for staging
+  return env_int("MPK_CSWEEP", 1) &&
+         (size_t)n * (cx ? 16 : 8) <= 16 * (size_t)160 * 1024;
 }
 
 static void gather_phase(const double *lu, const SweepPhase &ph, int n, bool cx,
@@ -191,6 +358,12 @@ static void free_phase(SweepPhase &ph) {
   void *p[] = {ph.lev, ph.desc, ph.col, ph.src, ph.val, ph.dsrc, ph.dval};
   for (void *q : p)
     if (q) cudaFree(q);
+}
+
+static void free_sweeps(SweepMats &sm) {
+  free_phase(sm.fwd);
+  free_phase(sm.bwd);
+  free_cplan(sm.cs);
 }
 
 }  // namespace
@@ -257,23 +430,23 @@ void ensure_adjoint(DMat &A, cudaStream_t st) {
     upload(&A.ord_ba, ob, st);
     upload(&A.lev_fa, pf, st);
     upload(&A.lev_ba, pb, st);
-    if (sweep_uses_smem(n, cx)) {
+    if (sweep_uses_smem(n, cx) || csweep_candidate(n, cx)) {
       // U^H forward: column c of U in ascending source rows, / conj(U_cc);
       // L^H backward: column c of L in descending source rows
-      build_phase(
-          A.smat_adj.fwd, n, cx, of, pf, A.levels_fa,
+      const HPhase hf = make_hphase(
+          n, of, pf, A.levels_fa,
           [&](int c, auto cb) {
             for (int q = ucnt[c]; q < ucnt[c + 1]; ++q) cb(ut_ci[q], ut_perm[q]);
           },
-          [&](int c) { return dp[c]; }, st);
-      build_phase(
-          A.smat_adj.bwd, n, cx, ob, pb, A.levels_ba,
+          [&](int c) { return dp[c]; });
+      const HPhase hb = make_hphase(
+          n, ob, pb, A.levels_ba,
           [&](int c, auto cb) {
             for (int q = lcnt[c]; q < lcnt[c + 1]; ++q) cb(lt_ci[q], lt_perm[q]);
           },
-          [&](int) { return -1; }, st);
+          [&](int) { return -1; });
+      A.smat_adj_built = build_sweeps(A.smat_adj, n, cx, hf, hb, st);
       A.smat_adj.conj = true;
-      A.smat_adj_built = true;
     }
     const size_t w = cx ? 2 : 1;
     cudaMalloc(&A.at_val, sizeof(double) * w * (A.nnz ? A.nnz : 1));
@@ -290,6 +463,7 @@ void ensure_adjoint(DMat &A, cudaStream_t st) {
       gather_phase(A.lu, A.smat_adj.fwd, n, cx, st);
       gather_phase(A.lu, A.smat_adj.bwd, n, cx, st);
     }
+    gather_csweep(A.lu, A.smat_adj.cs, cx, st);
     A.adj_ready = true;
   }
 }
@@ -389,23 +563,23 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
     delete m;
     return fail(MPK_CUDA_ERROR, "allocation failed");
   }
-  if (sweep_uses_smem((int)n, A.cx)) {
+  if (sweep_uses_smem((int)n, A.cx) || csweep_candidate((int)n, A.cx)) {
     const int *rp = A.h_rp.data(), *dp = A.h_dp.data(), *ci = A.h_ci.data();
-    build_phase(
-        A.smat.fwd, (int)n, A.cx, of, pf, A.levels_f,
+    const HPhase hf = make_hphase(
+        (int)n, of, pf, A.levels_f,
         [&](int i, auto cb) {
           const int hi = dp[i] < 0 ? rp[i] : dp[i];
           for (int p = rp[i]; p < hi; ++p) cb(ci[p], p);
         },
-        [&](int) { return -1; }, st);
-    build_phase(
-        A.smat.bwd, (int)n, A.cx, ob, pb, A.levels_b,
+        [&](int) { return -1; });
+    const HPhase hb = make_hphase(
+        (int)n, ob, pb, A.levels_b,
         [&](int i, auto cb) {
           const int lo = dp[i] < 0 ? rp[i + 1] : dp[i] + 1;
           for (int p = lo; p < rp[i + 1]; ++p) cb(ci[p], p);
         },
-        [&](int i) { return dp[i]; }, st);
-    A.smat_built = true;
+        [&](int i) { return dp[i]; });
+    A.smat_built = build_sweeps(A.smat, (int)n, A.cx, hf, hb, st);
   }
   const size_t w = A.cx ? 2 : 1;
   std::vector<double> vals(w * nnz);
@@ -453,10 +627,8 @@ void mpk_csr_free(mpk_matrix *m) {
     for (void *v : q)
       if (v) cudaFree(v);
   }
-  free_phase(A.smat.fwd);
-  free_phase(A.smat.bwd);
-  free_phase(A.smat_adj.fwd);
-  free_phase(A.smat_adj.bwd);
+  free_sweeps(A.smat);
+  free_sweeps(A.smat_adj);
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete m;
@@ -531,6 +703,7 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
     gather_phase(A.lu, A.smat.fwd, A.n, A.cx, m->ctx->stream);
     gather_phase(A.lu, A.smat.bwd, A.n, A.cx, m->ctx->stream);
   }
+  gather_csweep(A.lu, A.smat.cs, A.cx, m->ctx->stream);
   return MPK_OK;
 }
 

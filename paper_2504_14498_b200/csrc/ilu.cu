@@ -681,6 +681,245 @@ __global__ void sweep_reset_kernel(double *y, double *z, int n,
   }
 }
 
+// ---------------------------------------------------------------------
+// cluster sweep (ilu.cuh CSweep): DSMEM-resident vector, TMA-bulk staged
+// entries, one cluster barrier per level
+// ---------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_map(uint32_t a, uint32_t rank) {
+  uint32_t o;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(rank));
+  return o;
+}
+__device__ __forceinline__ void cl_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cl_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// values of earlier levels are immutable within a level: plain (reorderable)
+// loads; the barrier asm above carries the memory clobber
+__device__ __forceinline__ double cl_ld1(uint32_t a) {
+  double v;
+  asm("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void cl_ld2(uint32_t a, double &x, double &y) {
+  asm("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+__device__ __forceinline__ void cl_st1(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st2(uint32_t a, double x, double y) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x),
+               "d"(y)
+               : "memory");
+}
+__device__ __forceinline__ int cl_ldi(uint32_t a) {
+  int v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, int cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(cnt)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "CSW_WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra CSW_WAIT%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src,
+                                         uint32_t bytes, uint64_t *b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+constexpr int kCsBatch = 8;  // entries whose loads are issued together
+
+template <bool CX, bool ADJ>
+__global__ void __launch_bounds__(1024, 1)
+    csweep_kernel(SweepArgs a, CSweep p) {
+  using Ent = typename std::conditional<CX, CEntC, CEntR>::type;
+  constexpr int ESZ = CX ? 16 : 8;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int tid = threadIdx.x, T = blockDim.x;
+  const uint32_t rank = cl_rank();
+  const int C = p.C, nl = p.nl, nf = p.nf;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smraw);  // 3 mbarriers
+  int *flag = reinterpret_cast<int *>(smraw + 32);
+  int4 *seg = reinterpret_cast<int4 *>(smraw + 48);     // nl own segments
+  unsigned char *q = smraw + 48 + (size_t)nl * 16;
+  double *vec = reinterpret_cast<double *>(q);
+  q += ((size_t)p.maxslots * ESZ + 15) / 16 * 16;
+  CDesc *dbuf = reinterpret_cast<CDesc *>(q);
+  Ent *ebuf = reinterpret_cast<Ent *>(dbuf + 3 * p.maxdesc);
+  const uint32_t vbase = smem_u32(vec);
+
+  if (tid == 0) {
+    for (int b = 0; b < 3; ++b) mbar_init(&bar[b], 1);
+    flag[0] = (a.done && *a.done) ? 1 : 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  for (int g = tid; g < nl; g += T) seg[g] = p.seg[(size_t)g * C + rank];
+  // forward right-hand side (demoted input) preloaded into the own slots
+  const int s0 = p.slot_off[rank], s1 = p.slot_off[rank + 1];
+  for (int s = s0 + tid; s < s1; s += T) {
+    double r, m;
+    load_in<CX>(a, p.slot_row[s], r, m);
+    vec[(s - s0) * (CX ? 2 : 1)] = r;
+    if constexpr (CX) vec[(s - s0) * 2 + 1] = m;
+  }
+  __syncthreads();
+  // every CTA of the cluster is running and initialised; one uniform
+  // decision on the solver's done flag (rank 0's read)
+  cl_arrive();
+  cl_wait();
+  const bool skip = cl_ldi(cl_map(smem_u32(flag), 0)) != 0;
+  if (skip) {
+    cl_arrive();  // rank 0's flag must outlive the readers
+    cl_wait();
+    return;
+  }
+  const CDesc *gdesc = p.desc;
+  const Ent *gent = reinterpret_cast<const Ent *>(p.ent);
+  auto issue = [&](int g) {
+    const int b = g % 3;
+    const int4 sg = seg[g];
+    const uint32_t bytes = (uint32_t)sg.y * sizeof(CDesc) + (uint32_t)sg.w * sizeof(Ent);
+    if (bytes == 0) {
+      mbar_arrive(&bar[b]);
+      return;
+    }
+    mbar_arrive_tx(&bar[b], bytes);
+    if (sg.y) bulk_g2s(dbuf + b * p.maxdesc, gdesc + sg.x, sg.y * sizeof(CDesc), &bar[b]);
+    if (sg.w) bulk_g2s(ebuf + b * p.maxent, gent + sg.z, sg.w * sizeof(Ent), &bar[b]);
+  };
+  if (tid == 0) {
+    issue(0);
+    if (nl > 1) issue(1);
+  }
+  auto addr = [&](int pk) -> uint32_t {
+    return cl_map(vbase + (uint32_t)(pk & 0xFFFFFF) * ESZ, (uint32_t)pk >> 24);
+  };
+  bool bad = false;
+  for (int g = 0; g < nl; ++g) {
+    const int b = g % 3;
+    const bool fwd = g < nf;
+    mbar_wait(&bar[b], (uint32_t)((g / 3) & 1));
+    const int nd = seg[g].y;
+    const CDesc *D = dbuf + b * p.maxdesc;
+    const Ent *E = ebuf + b * p.maxent;
+    for (int r = tid; r < nd; r += T) {
+      const CDesc d = D[r];
+      double ar, ai = 0.0;
+      if constexpr (CX)
+        cl_ld2(addr(d.init), ar, ai);
+      else
+        ar = cl_ld1(addr(d.init));
+      for (int e = 0; e < d.cnt; e += kCsBatch) {
+        double lr[kCsBatch], li[kCsBatch], vr[kCsBatch], vi[kCsBatch];
+#pragma unroll
+        for (int t = 0; t < kCsBatch; ++t) {
+          vr[t] = vi[t] = lr[t] = li[t] = 0.0;
+          if (e + t < d.cnt) {
+            const Ent &x = E[d.e0 + e + t];
+            if constexpr (CX) {
+              lr[t] = x.vr;
+              li[t] = x.vi;
+              cl_ld2(addr(x.pk), vr[t], vi[t]);
+            } else {
+              lr[t] = x.v;
+              vr[t] = cl_ld1(addr(x.pk));
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < kCsBatch; ++t)
+          if (e + t < d.cnt) mulsub<CX, ADJ>(ar, ai, lr[t], li[t], vr[t], vi[t]);
+      }
+      double qr = ar, qi = ai;
+      if (d.hasdiv) {
+        if constexpr (CX)
+          py_cdiv(ar, ai, d.dr, ADJ ? -d.di : d.di, qr, qi);
+        else
+          qr = ddiv(ar, d.dr);
+      }
+      if constexpr (CX)
+        cl_st2(addr(d.out), qr, qi);
+      else
+        cl_st1(addr(d.out), qr);
+      if (!fwd) {
+        bad = bad || !isfin(qr) || !isfin(qi);
+        if constexpr (CX)
+          reinterpret_cast<double2 *>(a.z)[d.row] = make_double2(qr, qi);
+        else
+          a.z[d.row] = qr;
+      }
+    }
+    cl_arrive();
+    // buffer (g+2)%3 was last read at level g-1, which every CTA finished
+    if (tid == 0 && g + 2 < nl) issue(g + 2);
+    cl_wait();
+  }
+  if (bad) atomicOr(a.err, 1);
+}
+
+__global__ void gather_csweep_kernel(const double *lu, CSweep p, int cx) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t < p.nent) {
+    const int s = p.esrc[t];
+    if (cx) {
+      CEntC &e = reinterpret_cast<CEntC *>(p.ent)[t];
+      const double2 v = reinterpret_cast<const double2 *>(lu)[s];
+      e.vr = v.x;
+      e.vi = v.y;
+    } else {
+      reinterpret_cast<CEntR *>(p.ent)[t].v = lu[s];
+    }
+  }
+  if (t < p.ndesc) {
+    const int s = p.dsrc[t];
+    CDesc &d = p.desc[t];
+    if (s >= 0) {
+      if (cx) {
+        const double2 v = reinterpret_cast<const double2 *>(lu)[s];
+        d.dr = v.x;
+        d.di = v.y;
+      } else {
+        d.dr = lu[s];
+        d.di = 0.0;
+      }
+    }
+  }
+}
+
 int sweep_grid(int n) {
   // enough resident warps to expose the DAG's width; extra warps idle out
   long long warps = (2LL * n + 31) / 32;
@@ -760,6 +999,56 @@ void launch_sweep_mats(const SweepArgs &a, const SweepMats &m, bool cx,
   if (!cx && adjoint) launch_sweep_mats_t<false, true>(a, m, st);
   if (cx && !adjoint) launch_sweep_mats_t<true, false>(a, m, st);
   if (cx && adjoint) launch_sweep_mats_t<true, true>(a, m, st);
+}
+
+size_t csweep_smem_limit() { return kSmemMax; }
+
+template <bool CX, bool ADJ>
+static void launch_csweep_t(const SweepArgs &a, const CSweep &p,
+                            cudaStream_t st) {
+  static size_t attr_smem = 0;
+  static bool nonport = false;
+  auto kfn = csweep_kernel<CX, ADJ>;
+  if (attr_smem < p.smem) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemMax);
+    attr_smem = kSmemMax;
+  }
+  if (p.C > 8 && !nonport) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    nonport = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.C);
+  cfg.blockDim = dim3(p.T);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kfn, a, p);
+}
+
+void launch_csweep(const SweepArgs &a, const CSweep &p, bool cx, bool adjoint,
+                   cudaStream_t st) {
+  ++tl_launches;
+  if (!cx && !adjoint) launch_csweep_t<false, false>(a, p, st);
+  if (!cx && adjoint) launch_csweep_t<false, true>(a, p, st);
+  if (cx && !adjoint) launch_csweep_t<true, false>(a, p, st);
+  if (cx && adjoint) launch_csweep_t<true, true>(a, p, st);
+}
+
+void gather_csweep(const double *lu, const CSweep &p, bool cx,
+                   cudaStream_t st) {
+  const long long m = p.nent > p.ndesc ? p.nent : p.ndesc;
+  if (p.C == 0 || m <= 0) return;
+  ++tl_launches;
+  gather_csweep_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(lu, p,
+                                                                    cx ? 1 : 0);
 }
 
 bool sweep_uses_smem(int n, bool cx) {

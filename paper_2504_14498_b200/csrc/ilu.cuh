@@ -60,10 +60,58 @@ struct SweepPhase {
   long long nent = 0;
 };
 
+// Cluster sweep plan: both phases of one apply split over the C CTAs of a
+// thread-block cluster (one SM each).  Row i's value lives in the shared
+// memory of the CTA that computes it in the forward phase ("owner", slot s);
+// every reference to it is a packed address pk = owner << 24 | s read with
+// ld.shared::cluster (DSMEM).  Per (level, CTA) the row descriptors and
+// entries are contiguous ("segments"), staged into shared memory by bulk
+// async copies two levels ahead; levels are separated by a cluster barrier.
+struct __align__(16) CDesc {
+  int init;   // pk of the initial value (forward: rhs in own slot; backward: y_i)
+  int out;    // pk the result is stored to (row's owner slot)
+  int e0;     // first entry, relative to the segment
+  int cnt;    // entries
+  int row;    // global row (z output, rhs)
+  int hasdiv; // divide by d at the end
+  int pad0, pad1;
+  double dr, di;  // divisor (gathered from the factors)
+};
+struct __align__(16) CEntR {
+  double v;
+  int pk;
+  int pad;
+};
+struct __align__(16) CEntC {
+  double vr, vi;
+  int pk;
+  int pad[3];
+};
+struct CSweep {
+  int C = 0, T = 0;   // cluster size, threads per CTA (0: no plan)
+  int nl = 0, nf = 0; // levels (forward + backward), forward levels
+  int4 *seg = nullptr;        // [nl][C] {desc_off, ndesc, ent_off, nent}
+  CDesc *desc = nullptr;
+  int *dsrc = nullptr;        // per descriptor: lu index of divisor or -1
+  void *ent = nullptr;        // CEntR / CEntC
+  int *esrc = nullptr;        // per entry: lu index
+  int *slot_row = nullptr;    // [C][..] global row held in each slot
+  int *slot_off = nullptr;    // C+1 offsets into slot_row
+  long long ndesc = 0, nent = 0;
+  int maxslots = 0, maxdesc = 0, maxent = 0;
+  size_t smem = 0;            // dynamic shared memory per CTA
+};
+
 struct SweepMats {
   SweepPhase fwd, bwd;
   bool conj = false;  // adjoint: values are conjugated at use
+  CSweep cs;          // cluster plan (cs.C > 0 when built)
 };
+// cluster sweep over a plan (values gathered); cfg: env MPK_CSWEEP_C
+void launch_csweep(const SweepArgs &a, const CSweep &p, bool cx, bool adjoint,
+                   cudaStream_t st);
+void gather_csweep(const double *lu, const CSweep &p, bool cx, cudaStream_t st);
+size_t csweep_smem_limit();
 
 void launch_sweep(const SweepArgs &a, bool cx, bool adjoint,
                   cudaStream_t st);

@@ -78,13 +78,16 @@ struct DMat {
   std::vector<int> h_rp, h_ci, h_dp;
 };
 
-// ILU(0)-mixed apply dispatch: prefetched single-CTA sweep over the
-// level-ordered sweep matrices when they exist (small n), else the
-// sync-free multi-CTA kernel.
+// ILU(0)-mixed apply dispatch: cluster sweep when its plan exists, else the
+// prefetched single-CTA sweep over the level-ordered sweep matrices (small
+// n), else the sync-free multi-CTA kernel.
 inline void do_sweep(const DMat &A, const SweepArgs &a, bool adjoint,
                      cudaStream_t st) {
   const bool mats = adjoint ? A.smat_adj_built : A.smat_built;
-  if (mats)
+  const CSweep &cs = adjoint ? A.smat_adj.cs : A.smat.cs;
+  if (cs.C > 0)
+    launch_csweep(a, cs, A.cx, adjoint, st);
+  else if (mats)
     launch_sweep_mats(a, adjoint ? A.smat_adj : A.smat, A.cx, adjoint, st);
   else
     launch_sweep(a, A.cx, adjoint, st);

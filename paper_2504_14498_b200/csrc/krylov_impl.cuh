@@ -253,6 +253,11 @@ struct Solver : PlanBase {
   // ILU(0)-mixed apply: z = promote(U^-1 L^-1 demote(in)).
   void sweep(const double *in_re, const double *in_im, double *y, double *z,
              bool adjoint, int which, bool after_loop = false) {
+    sweep_on(st, in_re, in_im, y, z, adjoint, which, after_loop);
+  }
+  void sweep_on(cudaStream_t s_, const double *in_re, const double *in_im,
+                double *y, double *z, bool adjoint, int which,
+                bool after_loop = false) {
     SweepArgs a{};
     a.n = n;
     a.rp = A.rp;
@@ -278,7 +283,7 @@ struct Solver : PlanBase {
     a.tick = A.tick + 2 * which;
     a.err = A.err;
     a.done = after_loop ? nullptr : done;
-    do_sweep(A, a, adjoint, st);
+    do_sweep(A, a, adjoint, s_);
   }
   const double *head_re(const double *v) const { return v; }
   const double *head_im(const double *v) const { return CX ? v + K * ld : nullptr; }
@@ -998,21 +1003,27 @@ struct Solver : PlanBase {
                         Y2.set_sent(i);
                         ZT.set_sent(i);
                       });
+    // the two preconditioner applies are independent: the adjoint one (and
+    // hdot(zt, r), partials in part2) runs on the side branch, overlapped
+    // with the norm test and the forward apply.  Work done after a stop is
+    // dead (the next finalize exits on the done flag).
+    fork();
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
           const Sc ss = finalize_slot<K, false>(pt_, 0, G_, sm);
           if (threadIdx.x == 0) check_nrm<K>(S_, H, ss);
         });
     sweep(head_re(r), head_im(r), A.sw_y, zf, false, 0);
-    sweep(head_re(rt), head_im(rt), A.sw_y2, ztf, true, 1);
-    rows<K, CX, 1, 0>(n, done, part, st,
+    sweep_on(st2, head_re(rt), head_im(rt), A.sw_y2, ztf, true, 1);
+    rows<K, CX, 1, 0>(n, done, part2, st2,
                       [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
                         double wr[K], wi[K], rr[K], ri[K];
                         ZT.template load_mc<K>(i, wr, wi);
                         Rr.load(i, rr, ri);
                         acc_hdot<K, CX>(red.h[0], wr, wi, rr, ri);
                       });
-    fin(S, err, part, G, st,
+    join();
+    fin(S, err, part2, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
           const Sc rn = finalize_slot<K, CX>(pt_, 0, G_, sm);
           if (threadIdx.x == 0) {

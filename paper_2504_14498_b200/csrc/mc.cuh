@@ -152,20 +152,33 @@ MPK_HD bool fin_bits(double x) {
 #endif
 }
 
-template <int M, int K>
-MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
-  bool fin = true;
-#pragma unroll
-  for (int i = 0; i < M; ++i) fin = fin & fin_bits(t[i]);
-  if (!fin) {
-    double s = 0.0;
-#pragma unroll
-    for (int i = 0; i < M; ++i) s = dadd(s, t[i]);
-    out[0] = s;
-#pragma unroll
-    for (int i = 1; i < K; ++i) out[i] = 0.0;
-    return;
-  }
+// Exact error of q = fl(a + b) by Fast2Sum on the larger-magnitude operand
+// (Dekker: exact for finite a, b when a + b does not overflow).  The error
+// of an addition is unique, so this equals TwoSum's value -- up to the sign
+// of a zero error, which renorm's second sweep never observes (it only
+// tests en != 0).  Critical path: 2 DADDs after q instead of 4.
+MPK_HD double fast_err(double a, double b, double q) {
+  const bool ab = dabs(a) >= dabs(b);
+  const double big = ab ? a : b, sml = ab ? b : a;
+  return dsub(sml, dsub(q, big));
+}
+
+// |x| < 2^1000 (or zero): no partial sum of <= 16 such terms can overflow
+MPK_HD bool no_ovf(double x) {
+#ifdef __CUDA_ARCH__
+  return (__double2hiint(x) & 0x7ff00000) < ((1023 + 1000) << 20);
+#else
+  return std::fabs(x) < 0x1p1000;
+#endif
+}
+
+#ifdef MPK_COUNT_PASSES
+__device__ unsigned long long g_pass_hist[20][8];
+#endif
+// The pass loop of renorm_terms (_mccore.py:90-116).  fast: the Fast2Sum
+// error in the second sweep (valid when no partial sum can overflow).
+template <int M, bool fast>
+MPK_HD void renorm_passes(double (&t)[M]) {
 #pragma unroll 1
   for (int pass = 0; pass < 8; ++pass) {
     double e[M];
@@ -179,13 +192,24 @@ MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
     }
     e[0] = s;
     double eps = e[0];
+    if constexpr (fast) {
 #pragma unroll
-    for (int i = 1; i < M; ++i) {
-      double q, en;
-      two_sum(eps, e[i], q, en);
-      const bool em = (en != 0.0);
-      t[i - 1] = em ? q : 0.0;
-      eps = em ? en : q;
+      for (int i = 1; i < M; ++i) {
+        const double q = dadd(eps, e[i]);
+        const double en = fast_err(eps, e[i], q);
+        const bool em = (en != 0.0);
+        t[i - 1] = em ? q : 0.0;
+        eps = em ? en : q;
+      }
+    } else {
+#pragma unroll
+      for (int i = 1; i < M; ++i) {
+        double q, en;
+        two_sum(eps, e[i], q, en);
+        const bool em = (en != 0.0);
+        t[i - 1] = em ? q : 0.0;
+        eps = em ? en : q;
+      }
     }
     t[M - 1] = eps;
     // strictness over consecutive non-hole components (branch-free)
@@ -199,8 +223,36 @@ MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
       ok = ok & !viol;
       prev = nz ? c : prev;
     }
+#if defined(MPK_COUNT_PASSES) && defined(__CUDA_ARCH__)
+    atomicAdd(&g_pass_hist[M][pass], 1ull);
+#endif
     if (ok) break;
   }
+}
+
+template <int M, int K>
+MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
+  bool fin = true, small = true;
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    fin = fin & fin_bits(t[i]);
+    small = small & no_ovf(t[i]);
+  }
+  if (!fin) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) s = dadd(s, t[i]);
+    out[0] = s;
+#pragma unroll
+    for (int i = 1; i < K; ++i) out[i] = 0.0;
+    return;
+  }
+  // both pass loops inline: a call on the fast path costs more than the
+  // code (the branch is uniform in practice)
+  if (small)
+    renorm_passes<M, true>(t);
+  else
+    renorm_passes<M, false>(t);
   // first K non-hole components (branch-free predicated selects)
 #pragma unroll
   for (int j = 0; j < K; ++j) out[j] = 0.0;
@@ -217,23 +269,29 @@ MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
 
 // Reference merge of two component lists by magnitude, ties prefer x
 // (_mccore.py:134-154), for arbitrary (not necessarily sorted) inputs.
+// The two inputs are consumed as shift registers (heads xq[0] / yq[0]) so
+// every index is static: a dynamically indexed x[i] is lowered to local
+// memory, which put an L1 round trip on each merge step.
 template <int KX, int KY>
 MPK_HD void merge(const double (&x)[KX], const double (&y)[KY],
                   double (&buf)[KX + KY]) {
-  int i = 0;
+  double xq[KX], yq[KY];
+#pragma unroll
+  for (int a = 0; a < KX; ++a) xq[a] = x[a];
+#pragma unroll
+  for (int a = 0; a < KY; ++a) yq[a] = y[a];
+  int nx = KX, ny = KY;  // remaining
 #pragma unroll
   for (int t = 0; t < KX + KY; ++t) {
-    double xi = 0.0, yj = 0.0;
+    const bool xv = nx > 0, yv = ny > 0;
+    const bool tx = xv && (!yv || dabs(xq[0]) >= dabs(yq[0]));
+    buf[t] = tx ? xq[0] : yq[0];
 #pragma unroll
-    for (int a = 0; a < KX; ++a)
-      if (i == a) xi = x[a];
+    for (int a = 0; a + 1 < KX; ++a) xq[a] = tx ? xq[a + 1] : xq[a];
 #pragma unroll
-    for (int a = 0; a < KY; ++a)
-      if (t - i == a) yj = y[a];
-    const bool xv = i < KX, yv = (t - i) < KY;
-    const bool tx = xv && (!yv || dabs(xi) >= dabs(yj));
-    buf[t] = tx ? xi : yj;
-    i += tx ? 1 : 0;
+    for (int a = 0; a + 1 < KY; ++a) yq[a] = tx ? yq[a] : yq[a + 1];
+    nx -= tx ? 1 : 0;
+    ny -= tx ? 0 : 1;
   }
 }
 
@@ -461,6 +519,66 @@ MPK_HD bool is_finite(const double (&x)[K]) {
   return f;
 }
 
+// Out-of-line MC operations for the scalar recurrences.  They take and
+// return small structs BY VALUE (register ABI): passing references to a
+// caller's register arrays into a __noinline__ function is exactly what
+// faulted on sm_100a, so no pointer to a caller-local array ever crosses
+// these call boundaries.  Division / sqrt call them instead of inlining 13
+// full operations: the inlined bodies overflowed the instruction cache
+// (a single-thread division streamed ~100 KB of code per call).
+template <int K>
+struct V {
+  double c[K];
+};
+template <int K>
+struct V2 {
+  double r[K];
+  double i[K];
+};
+template <int K>
+MPK_SCALAR V<K> mul_v(V<K> x, V<K> y) {
+  V<K> o;
+  mul<K>(x.c, y.c, o.c);
+  return o;
+}
+template <int K>
+MPK_SCALAR V<K> add_v(V<K> x, V<K> y) {
+  V<K> o;
+  add<K>(x.c, y.c, o.c);
+  return o;
+}
+template <int K>
+MPK_HD void mul_o(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
+  V<K> a, b;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    a.c[i] = x[i];
+    b.c[i] = y[i];
+  }
+  const V<K> o = mul_v<K>(a, b);
+#pragma unroll
+  for (int i = 0; i < K; ++i) out[i] = o.c[i];
+}
+template <int K>
+MPK_HD void add_o(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
+  V<K> a, b;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    a.c[i] = x[i];
+    b.c[i] = y[i];
+  }
+  const V<K> o = add_v<K>(a, b);
+#pragma unroll
+  for (int i = 0; i < K; ++i) out[i] = o.c[i];
+}
+template <int K>
+MPK_HD void sub_o(const double (&x)[K], const double (&y)[K], double (&out)[K]) {
+  double ny[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) ny[i] = -y[i];
+  add_o<K>(x, ny, out);
+}
+
 // _div_by_zero _mccore.py:216-219
 MPK_HD double div_by_zero(double x0, double y0) {
   if (x0 == 0.0) return NAN;
@@ -487,19 +605,19 @@ MPK_HD void div_a(const double (&x)[K], const double (&y)[K], double (&out)[K]) 
   w[0] = ddiv(1.0, y[0]);
   const int iters = (K == 2) ? 1 : 2;
   for (int it = 0; it < iters; ++it) {
-    mul<K>(y, w, t1);
-    sub<K>(one, t1, t2);
-    mul<K>(w, t2, t1);
-    add<K>(w, t1, t2);
+    mul_o<K>(y, w, t1);
+    sub_o<K>(one, t1, t2);
+    mul_o<K>(w, t2, t1);
+    add_o<K>(w, t1, t2);
 #pragma unroll
     for (int i = 0; i < K; ++i) w[i] = t2[i];
   }
   double q[K], r[K];
-  mul<K>(x, w, q);
-  mul<K>(q, y, t1);
-  sub<K>(x, t1, r);
-  mul<K>(r, w, t2);
-  add<K>(q, t2, out);
+  mul_o<K>(x, w, q);
+  mul_o<K>(q, y, t1);
+  sub_o<K>(x, t1, r);
+  mul_o<K>(r, w, t2);
+  add_o<K>(q, t2, out);
 }
 
 // mc_sqrt _mccore.py:245-266 (Newton on rsqrt). Returns false if x0 < 0.
@@ -526,24 +644,24 @@ MPK_HD bool sqrt_a(const double (&x)[K], double (&out)[K]) {
   z[0] = ddiv(1.0, dsqrt(x[0]));
   const int iters = (K == 2) ? 1 : 2;
   for (int it = 0; it < iters; ++it) {
-    mul<K>(z, z, a);
-    mul<K>(x, a, b);
-    sub<K>(one, b, t);
-    mul<K>(z, t, a);
+    mul_o<K>(z, z, a);
+    mul_o<K>(x, a, b);
+    sub_o<K>(one, b, t);
+    mul_o<K>(z, t, a);
 #pragma unroll
     for (int i = 0; i < K; ++i) a[i] = dmul(a[i], 0.5);
-    add<K>(z, a, b);
+    add_o<K>(z, a, b);
 #pragma unroll
     for (int i = 0; i < K; ++i) z[i] = b[i];
   }
   double r[K];
-  mul<K>(x, z, r);
-  mul<K>(r, r, a);
-  sub<K>(x, a, t);
+  mul_o<K>(x, z, r);
+  mul_o<K>(r, r, a);
+  sub_o<K>(x, a, t);
 #pragma unroll
   for (int i = 0; i < K; ++i) b[i] = dmul(z[i], 0.5);
-  mul<K>(t, b, a);
-  add<K>(r, a, out);
+  mul_o<K>(t, b, a);
+  add_o<K>(r, a, out);
   return true;
 }
 
@@ -551,25 +669,13 @@ MPK_HD bool sqrt_a(const double (&x)[K], double (&out)[K]) {
 template <int K>
 MPK_HD int cmp_a(const double (&x)[K], const double (&y)[K]) {
   double d[K];
-  sub<K>(x, y, d);
+  sub_o<K>(x, y, d);
   if (d[0] > 0.0) return 1;
   if (d[0] < 0.0) return -1;
   return 0;
 }
 
-// Out-of-line scalar entry points.  They take and return small structs BY
-// VALUE (register ABI): passing references to a caller's register arrays
-// into a __noinline__ function is exactly what faulted on sm_100a, so no
-// pointer to a caller-local array ever crosses these call boundaries.
-template <int K>
-struct V {
-  double c[K];
-};
-template <int K>
-struct V2 {
-  double r[K];
-  double i[K];
-};
+// Out-of-line scalar entry points (by-value structs, see V above).
 
 template <int K>
 MPK_SCALAR V<K> div_v(V<K> x, V<K> y) {
@@ -636,23 +742,23 @@ MPK_HD void cdiv_a(const double (&ar)[K], const double (&ai)[K],
       return;
     }
     div<K>(bi, br, t);
-    mul<K>(bi, t, u);
-    add<K>(br, u, d);
-    mul<K>(ai, t, u);
-    add<K>(ar, u, v);
+    mul_o<K>(bi, t, u);
+    add_o<K>(br, u, d);
+    mul_o<K>(ai, t, u);
+    add_o<K>(ar, u, v);
     div<K>(v, d, re);
-    mul<K>(ar, t, u);
-    sub<K>(ai, u, v);
+    mul_o<K>(ar, t, u);
+    sub_o<K>(ai, u, v);
     div<K>(v, d, im);
   } else {
     div<K>(br, bi, t);
-    mul<K>(br, t, u);
-    add<K>(u, bi, d);
-    mul<K>(ar, t, u);
-    add<K>(u, ai, v);
+    mul_o<K>(br, t, u);
+    add_o<K>(u, bi, d);
+    mul_o<K>(ar, t, u);
+    add_o<K>(u, ai, v);
     div<K>(v, d, re);
-    mul<K>(ai, t, u);
-    sub<K>(u, ar, v);
+    mul_o<K>(ai, t, u);
+    sub_o<K>(u, ar, v);
     div<K>(v, d, im);
   }
 #pragma unroll

@@ -332,3 +332,46 @@ def test_device_edge_cases(pkg):
     Ab = pkg.CsrMatrix(n, rp, ci, vre, None, P)
     with pytest.raises(ValueError, match="binary64-representable"):
         pkg.solve(Ab, b, cfg)
+
+
+SWEEP_PATHS = {
+    "global": {"MPK_CSWEEP": "0", "MPK_SWEEP_SMEM": "0"},
+    "single": {"MPK_CSWEEP": "0"},
+    "cluster1": {"MPK_CSWEEP_C": "1"},
+    "cluster2": {"MPK_CSWEEP_C": "2", "MPK_CSWEEP_ROWS": "1"},
+    "cluster8": {"MPK_CSWEEP_C": "8", "MPK_CSWEEP_ROWS": "1"},
+    "cluster16": {"MPK_CSWEEP_C": "16", "MPK_CSWEEP_ROWS": "1"},
+}
+
+
+@pytest.mark.parametrize("path", list(SWEEP_PATHS))
+@pytest.mark.parametrize("mat", ["cfg1", "cfg2", "helm_c"])
+def test_device_sweep_paths_bitwise(pkg, monkeypatch, path, mat):
+    """Every sweep implementation (sync-free global, single-CTA, cluster of
+    1/2/8/16 CTAs) gives the oracle's binary64 ILU(0) apply bit for bit,
+    plain and adjoint (ilu.py:410-470)."""
+    import oracle.oracle as orc
+    from paper_2504_14498_b200 import problems
+
+    for k_, v_ in SWEEP_PATHS[path].items():
+        monkeypatch.setenv(k_, v_)
+    if mat == "helm_c":
+        rp, ci, vre, vim = problems.helmholtz7(20, 7)[:4]
+        n = len(rp) - 1
+    else:
+        p = getattr(problems, mat)()
+        n, rp, ci, vre, vim = p.n, p.row_ptr, p.col_idx, p.val_re, p.val_im
+    A = _csr(pkg, rp, ci, vre, vim)
+    F = pkg.ilu0_factorize_demoted(A)
+    rc, lre, lim = orc.ilu0_factor(n, rp, ci, vre, vim)[:3]
+    assert rc == 0
+    rng = np.random.default_rng(11)
+    r_re = rng.standard_normal((n, 2))
+    r_im = rng.standard_normal((n, 2)) if vim is not None else None
+    r = pkg.DenseVector(r_re.copy(), None if r_im is None else r_im.copy(), pkg.Precision.DD)
+    for adj in (False, True):
+        z = (pkg.ilu0_apply_adjoint_mixed if adj else pkg.ilu0_apply_mixed)(F, r)
+        _, zr, zi = orc.ilu0_apply_mixed(n, rp, ci, lre, lim, r_re, r_im, adjoint=adj)
+        assert bits_equal(z.re, zr), (path, mat, adj)
+        if vim is not None:
+            assert bits_equal(z.im, zi), (path, mat, adj)
