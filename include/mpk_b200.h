@@ -78,6 +78,15 @@ void mpk_ctx_destroy(mpk_ctx *ctx);
 int mpk_ctx_synchronize(mpk_ctx *ctx);
 /* the context's cudaStream_t (for event timing by the caller) */
 void *mpk_ctx_stream(mpk_ctx *ctx);
+/* Context options.  MPK_OPT_REDUCTION selects how dot products / norms are
+ * reduced in mpk_hdot, mpk_norm2 and the solvers: MPK_REDUCE_TREE (default,
+ * fixed-shape parallel tree) or MPK_REDUCE_SEQUENTIAL (the reference's
+ * ascending accumulation, _kernels.py:487-552, bit-identical to it and
+ * slow: one dependent chain of n MC additions per reduction). */
+#define MPK_OPT_REDUCTION 1
+#define MPK_REDUCE_TREE 0
+#define MPK_REDUCE_SEQUENTIAL 1
+int mpk_ctx_set_option(mpk_ctx *ctx, int option, int64_t value);
 
 /* CsrMatrix.demoted() upload (sparse.py:192-249): binary64 values, val_im
  * NULL for the real field.  Columns must be strictly increasing per row. */
@@ -86,6 +95,10 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
                    const double *val_re, const double *val_im,
                    mpk_matrix **out);
 void mpk_csr_free(mpk_matrix *m);
+/* New binary64 values on the uploaded pattern (numeric phase; the pattern
+ * analysis -- level sets, sweep matrices, solver plans -- is kept). */
+int mpk_csr_set_values(mpk_matrix *m, const double *val_re,
+                       const double *val_im);
 
 /* ilu0_factorize_demoted (ilu.py:284-286 -> _factorize_tuples :178-276).
  * Returns MPK_SINGULAR_PIVOT with *bad_row / *structural, or
@@ -162,6 +175,27 @@ int mpk_from_planar(mpk_ctx *ctx, int64_t n, int k, const double *dev,
  * context stream) of one ILU(0)-mixed apply (forward + backward sweep
  * kernel) of a k-component input, over reps launches.  Needs factors. */
 int mpk_bench_apply(mpk_matrix *m, int k, int reps, double *ms_avg);
+
+/* A batch of independent solves run concurrently, one native thread per
+ * job, each on its matrix's own context/stream (the reference harness runs
+ * cells in a thread pool, bench.py:179-216).  device_resident = 0: b/x are
+ * host (n,k) arrays as in mpk_solve, and val_re/val_im (optional) are new
+ * matrix values copied in first (mpk_csr_set_values); device_resident = 1:
+ * b/x are planar device buffers as in mpk_solve_dev. */
+typedef struct {
+  mpk_matrix *m;
+  int32_t method, k;
+  double eps_rel, eps_abs;
+  int64_t max_iter;
+  const double *b_re, *b_im;
+  double *x_re, *x_im;
+  const double *val_re, *val_im;
+  double *hist;
+  int64_t hist_cap;
+  mpk_report rep; /* out */
+  int32_t rc;     /* out */
+} mpk_job;
+int mpk_run_jobs(mpk_job *jobs, int njobs, int device_resident);
 
 /* Independent systems (cfg5 batch): matrices[i] already uploaded, each
  * solved on its own stream of the context's device.  b/x host (n_i,k). */

@@ -47,7 +47,11 @@ EXPORTS = (
     "mpk_spmv_mixed", "mpk_hdot", "mpk_norm2", "mpk_axpy", "mpk_mc_elementwise",
     "mpk_mc_host", "mpk_solve", "mpk_plane_ld", "mpk_solve_dev", "mpk_to_planar",
     "mpk_from_planar", "mpk_solve_batch", "mpk_ctx_stream", "mpk_bench_apply",
+    "mpk_csr_set_values", "mpk_run_jobs", "mpk_ctx_set_option",
 )
+
+MPK_OPT_REDUCTION = 1
+REDUCTION_MODE = {"tree": 0, "sequential": 1}
 
 
 class MpkReport(ctypes.Structure):
@@ -65,6 +69,27 @@ class MpkReport(ctypes.Structure):
         ("solve_ms", ctypes.c_double),
         ("total_ms", ctypes.c_double),
         ("launches", ctypes.c_int64),
+    ]
+
+
+class MpkJob(ctypes.Structure):
+    _fields_ = [
+        ("m", ctypes.c_void_p),
+        ("method", ctypes.c_int32),
+        ("k", ctypes.c_int32),
+        ("eps_rel", ctypes.c_double),
+        ("eps_abs", ctypes.c_double),
+        ("max_iter", ctypes.c_int64),
+        ("b_re", ctypes.c_void_p),
+        ("b_im", ctypes.c_void_p),
+        ("x_re", ctypes.c_void_p),
+        ("x_im", ctypes.c_void_p),
+        ("val_re", ctypes.c_void_p),
+        ("val_im", ctypes.c_void_p),
+        ("hist", ctypes.c_void_p),
+        ("hist_cap", ctypes.c_int64),
+        ("rep", MpkReport),
+        ("rc", ctypes.c_int32),
     ]
 
 
@@ -140,3 +165,30 @@ def i64(a):
 
 def plane_ld(n: int) -> int:
     return int(lib().mpk_plane_ld(ctypes.c_int64(n)))
+
+
+def set_reduction(mode: str, device: int = 0) -> None:
+    """Reduction order of hdot/norm2 and of the solvers' dot products:
+    "tree" (default, fixed-shape parallel tree) or "sequential" (the
+    reference's ascending accumulation, _kernels.py:487-552 -- bit-identical
+    to it, one dependent chain of n MC additions per reduction)."""
+    if mode not in REDUCTION_MODE:
+        raise ValueError(f"unknown reduction mode {mode!r} (tree | sequential)")
+    check(lib().mpk_ctx_set_option(context(device), ctypes.c_int(MPK_OPT_REDUCTION),
+                                   ctypes.c_int64(REDUCTION_MODE[mode])),
+          "mpk_ctx_set_option")
+
+
+class reduction_mode:
+    """Context manager: `with reduction_mode("sequential"): ...`"""
+
+    def __init__(self, mode: str, device: int = 0):
+        self.mode, self.device = mode, device
+
+    def __enter__(self):
+        set_reduction(self.mode, self.device)
+        return self
+
+    def __exit__(self, *exc):
+        set_reduction("tree", self.device)
+        return False

@@ -29,6 +29,7 @@ using namespace mpk;
 struct mpk_ctx {
   int device;
   cudaStream_t stream;
+  int reduce_seq = 0;  // MPK_OPT_REDUCTION
 };
 
 // Per-k device I/O buffers of mpk_solve, kept across calls (no
@@ -503,6 +504,19 @@ int mpk_ctx_synchronize(mpk_ctx *ctx) {
 
 void *mpk_ctx_stream(mpk_ctx *ctx) { return (void *)ctx->stream; }
 
+int mpk_ctx_set_option(mpk_ctx *ctx, int option, int64_t value) {
+  if (!ctx) return fail(MPK_INVALID, "null context");
+  switch (option) {
+    case MPK_OPT_REDUCTION:
+      if (value != MPK_REDUCE_TREE && value != MPK_REDUCE_SEQUENTIAL)
+        return fail(MPK_INVALID, "reduction mode must be 0 (tree) or 1 (sequential)");
+      ctx->reduce_seq = (int)value;
+      return MPK_OK;
+    default:
+      return fail(MPK_INVALID, "unknown option");
+  }
+}
+
 int64_t mpk_plane_ld(int64_t n) { return plane_ld(n); }
 
 int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
@@ -936,7 +950,7 @@ int mpk_hdot(mpk_ctx *ctx, int64_t n, int k, const double *x_re,
   rc = to_dev_planar(ctx, n, k, y_re, y_im, &dy);
   if (rc) return rc;
   double out[8];
-  rc = unit_reduce(k, x_im != nullptr, 0, n, dx, dy, out, ctx->stream);
+  rc = unit_reduce(k, x_im != nullptr, 0, n, dx, dy, out, ctx->stream, ctx->reduce_seq);
   for (int c = 0; c < k; ++c) {
     out_re[c] = out[c];
     if (out_im) out_im[c] = out[4 + c];
@@ -954,7 +968,7 @@ int mpk_norm2(mpk_ctx *ctx, int64_t n, int k, const double *x_re,
   int rc = to_dev_planar(ctx, n, k, x_re, x_im, &dx);
   if (rc) return rc;
   double o[8];
-  rc = unit_reduce(k, x_im != nullptr, 1, n, dx, dx, o, ctx->stream);
+  rc = unit_reduce(k, x_im != nullptr, 1, n, dx, dx, o, ctx->stream, ctx->reduce_seq);
   for (int c = 0; c < k; ++c) out[c] = o[c];
   cudaFree(dx);
   return rc ? fail(rc, "norm2 failed") : MPK_OK;
@@ -1127,6 +1141,7 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   p.max_iter = max_iter < 0 ? 3LL * m->A.n : max_iter;
   p.precond_ilu = 1;
   p.hist_cap = hist_cap;
+  p.reduce_seq = m->ctx->reduce_seq;
   SolveOut o{};
   char eb[256] = {0};
   rc = run_solve(m->A, p, d_b, d_x, d_hist, &o, m->ctx->stream, eb);

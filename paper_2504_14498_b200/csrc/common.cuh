@@ -24,6 +24,11 @@ constexpr int kWarpsPerBlock = kBlock / 32;
 // Host-side count of kernels launched (or captured) by this thread; the
 // C ABI reports per-call deltas (mpk_report.launches).
 inline thread_local long long tl_launches = 0;
+// Sequential-reduction twin mode (set by the solver while it builds its
+// graphs): row kernels write every element's reduction term here instead of
+// accumulating, and a chain kernel folds them in the reference's ascending
+// order.  nullptr: fixed-shape tree reductions.
+inline thread_local double *tl_seq = nullptr;
 
 // Sentinel for sync-free triangular sweeps: a signalling NaN payload that no
 // binary64 operation produces (hardware NaNs are quiet).
@@ -313,9 +318,11 @@ template <int K, bool CX>
 struct Acc {
   double re[K];
   double im[K];
+  double *seq;  // twin mode: this element's term slot (2K doubles), else null
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int c = 0; c < K; ++c) re[c] = im[c] = 0.0;
+    seq = nullptr;
   }
 };
 
@@ -330,11 +337,24 @@ __device__ __forceinline__ void acc_hdot(Acc<K, CX> &a, const double (&xr)[K],
 #pragma unroll
     for (int c = 0; c < K; ++c) cj[c] = -xi[c];
     cmul<K>(xr, cj, yr, yi, pr, pi);
+    if (a.seq) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        a.seq[c] = pr[c];
+        a.seq[K + c] = pi[c];
+      }
+      return;
+    }
     add<K>(a.re, pr, a.re);
     add<K>(a.im, pi, a.im);
   } else {
     double t[K];
     mul<K>(xr, yr, t);
+    if (a.seq) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) a.seq[c] = t[c];
+      return;
+    }
     add<K>(a.re, t, a.re);
   }
 }
@@ -345,6 +365,16 @@ __device__ __forceinline__ void acc_sumsq(Acc<K, false> &a,
                                           const double (&xi)[K]) {
   double t[K];
   mul<K>(xr, xr, t);
+  if (a.seq) {  // complex: two terms (re^2, im^2) in the reference order
+#pragma unroll
+    for (int c = 0; c < K; ++c) a.seq[c] = t[c];
+    if constexpr (CX) {
+      mul<K>(xi, xi, t);
+#pragma unroll
+      for (int c = 0; c < K; ++c) a.seq[K + c] = t[c];
+    }
+    return;
+  }
   add<K>(a.re, t, a.re);
   if constexpr (CX) {
     mul<K>(xi, xi, t);

@@ -99,6 +99,7 @@ struct SolveParams {
   long long max_iter;
   int precond_ilu;  // 1: ILU(0)-mixed, 0: identity
   long long hist_cap;
+  int reduce_seq;   // 1: sequential-order (bit-identical twin) reductions
 };
 
 struct SolveOut {
@@ -120,7 +121,7 @@ int run_solve(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
 int unit_spmv(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
               double *d_y, cudaStream_t st);
 int unit_reduce(int k, bool cx, int op, long long n, const double *d_x,
-                const double *d_y, double *h_out, cudaStream_t st);
+                const double *d_y, double *h_out, cudaStream_t st, int seq);
 int unit_axpy(int k, bool cx, long long n, const double *alpha_re,
               const double *alpha_im, const double *d_x, const double *d_y,
               double *d_out, cudaStream_t st);

@@ -178,6 +178,7 @@ struct Solver : PlanBase {
   cudaStream_t st2 = nullptr;
   cudaEvent_t evf = nullptr, evj = nullptr;
   double *part2 = nullptr;
+  double *seqbuf = nullptr;  // twin-mode element terms [slot][i][2K]
   State *hp = nullptr;  // pinned host staging of the device State (x2)
   int *hpi = nullptr;
 
@@ -194,7 +195,10 @@ struct Solver : PlanBase {
       : A(A_), p(p_), st(st_), errbuf(eb) {
     n = A.n;
     ld = plane_ld(n);
-    G = grid_for(n);
+    // twin mode: element terms + ascending chains; finalize over 1 partial
+    G = p.reduce_seq ? 1 : grid_for(n);
+    if (p.reduce_seq)
+      seqbuf = (double *)dalloc(sizeof(double) * 8 * 2 * K * (size_t)(n > 0 ? n : 1));
     da = DA{A.n, A.rp, A.ci, A.val, A.at_rp, A.at_ci, A.at_val};
     S = (State *)dalloc(sizeof(State));
     part = (double *)dalloc(sizeof(double) * 6 * kMaxGrid * 8);
@@ -1139,7 +1143,7 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   const char *nocond = getenv("MPK_NO_COND_GRAPH");
   const bool use_cond = !nocond || nocond[0] == '0';
   // plan cache: one workspace + graph per (method, K, field) on this matrix
-  const int key = p.method * 100 + K * 10 + (CX ? 1 : 0);
+  const int key = p.reduce_seq * 1000 + p.method * 100 + K * 10 + (CX ? 1 : 0);
   Solver<K, CX> *sv = nullptr;
   auto it = A.plans.find(key);
   if (it != A.plans.end()) {
@@ -1163,6 +1167,10 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   }
   sv->p = p;
   sv->errbuf = errbuf;
+  struct SeqScope {  // every row kernel of this solve (eager or captured)
+    explicit SeqScope(double *s) { tl_seq = s; }
+    ~SeqScope() { tl_seq = nullptr; }
+  } seq_scope(sv->seqbuf);
   const long long launches0 = tl_launches;
   State hs{};
   hs.max_iter = p.max_iter;

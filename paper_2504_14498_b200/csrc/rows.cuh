@@ -93,15 +93,77 @@ struct Red {
 
 template <int K, bool CX, int NH, int NN, class F>
 __global__ void __launch_bounds__(kBlock)
-    rows_kernel(long long n, const int *done, double *part, F f) {
+    rows_kernel(long long n, const int *done, double *part, double *seq, F f) {
   if (done && *done) return;
   __shared__ double smem[kWarpsPerBlock * 8];
   Red<K, CX, NH, NN> red;
   red.zero();
   for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < n;
-       i += (long long)gridDim.x * kBlock)
+       i += (long long)gridDim.x * kBlock) {
+    if (seq) {  // twin mode: element i's terms -> seq[slot][i]
+#pragma unroll
+      for (int s = 0; s < NH; ++s) red.h[s].seq = seq + ((size_t)s * n + i) * 2 * K;
+#pragma unroll
+      for (int s = 0; s < NN; ++s)
+        red.nr[s].seq = seq + ((size_t)(NH + s) * n + i) * 2 * K;
+    }
     f(i, red);
-  if constexpr (NH + NN > 0) red.store(part, smem);
+  }
+  if constexpr (NH + NN > 0)
+    if (!seq) red.store(part, smem);
+}
+
+// Twin mode: one lane per chain folds the element terms in ascending order
+// exactly like dot_real / hdot_cx / sumsq_* (_kernels.py:487-552), and
+// stores the sum as block partial 0 of its slot (the finalize then runs
+// with G = 1; adding the zero lanes of its tree is exact for a renormalised
+// value).  Chains: hdot slots 1 (real) or 2 (re, im); norm slots 1, with
+// two terms per element for the complex field.
+template <int K, bool CX, int NH, int NN>
+__global__ void seq_chain_kernel(long long n, const int *done,
+                                 const double *seq, double *part) {
+  if (done && *done) return;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) != 0) return;
+  constexpr int NHC = NH * (CX ? 2 : 1);
+  int slot, off, per;
+  if (w < NHC) {
+    slot = CX ? w / 2 : w;
+    off = CX ? (w % 2) * K : 0;
+    per = 1;
+  } else if (w < NHC + NN) {
+    slot = NH + (w - NHC);
+    off = 0;
+    per = CX ? 2 : 1;
+  } else {
+    return;
+  }
+  const double *b = seq + (size_t)slot * n * 2 * K;
+  double acc[K], t[K], nx[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) acc[c] = 0.0;
+  const long long m = n * per;
+  auto term = [&](long long j, double(&o)[K]) {
+    const long long i = per == 2 ? j >> 1 : j;
+    const int o2 = per == 2 ? (int)(j & 1) * K : off;
+#pragma unroll
+    for (int c = 0; c < K; ++c) o[c] = b[(size_t)i * 2 * K + o2 + c];
+  };
+  if (m > 0) term(0, nx);
+  for (long long j = 0; j < m; ++j) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) t[c] = nx[c];
+    if (j + 1 < m) term(j + 1, nx);  // prefetch overlaps the add
+    add<K>(acc, t, acc);
+  }
+  double *q = part + ((size_t)slot * kMaxGrid) * 8;
+  const int base = (CX && w < NHC && (w % 2)) ? 4 : 0;
+#pragma unroll
+  for (int c = 0; c < K; ++c) q[base + c] = acc[c];
+  if (!CX || w >= NHC) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) q[4 + c] = 0.0;
+  }
 }
 
 // Every kernel of the solver asks for the max-shared-memory carveout, so
@@ -121,7 +183,14 @@ template <int K, bool CX, int NH, int NN, class F>
 void rows(long long n, const int *done, double *part, cudaStream_t st, F f) {
   ++tl_launches;
   prefer_max_smem(rows_kernel<K, CX, NH, NN, F>);
-  rows_kernel<K, CX, NH, NN, F><<<grid_for(n), kBlock, 0, st>>>(n, done, part, f);
+  double *seq = (NH + NN > 0) ? tl_seq : nullptr;
+  rows_kernel<K, CX, NH, NN, F><<<grid_for(n), kBlock, 0, st>>>(n, done, part,
+                                                                 seq, f);
+  if (seq) {
+    ++tl_launches;
+    constexpr int chains = NH * (CX ? 2 : 1) + NN;
+    seq_chain_kernel<K, CX, NH, NN><<<1, 32 * chains, 0, st>>>(n, done, seq, part);
+  }
 }
 
 template <class F>

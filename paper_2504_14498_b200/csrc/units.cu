@@ -85,13 +85,16 @@ __global__ void unit_fin_kernel(const double *part, int G, int op,
 
 template <int K, bool CX>
 static int reduce_typed(int op, long long n, const double *d_x,
-                        const double *d_y, double *h_out, cudaStream_t st) {
+                        const double *d_y, double *h_out, cudaStream_t st,
+                        int seq_mode) {
   const long long L = plane_ld(n);
   const MV<K, CX> X{const_cast<double *>(d_x), L},
       Y{const_cast<double *>(d_y), L};
-  double *part = nullptr, *out = nullptr;
+  double *part = nullptr, *out = nullptr, *seq = nullptr;
   cudaMalloc(&part, sizeof(double) * kMaxGrid * 8);
   cudaMalloc(&out, sizeof(double) * 8);
+  if (seq_mode) cudaMalloc(&seq, sizeof(double) * 2 * K * (size_t)(n > 0 ? n : 1));
+  tl_seq = seq;  // twin mode: ascending chain instead of the tree
   if (op == 0)
     rows<K, CX, 1, 0>(n, nullptr, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
@@ -107,20 +110,22 @@ static int reduce_typed(int op, long long n, const double *d_x,
                         X.load(i, xr, xi);
                         acc_sumsq<K, CX>(red.nr[0], xr, xi);
                       });
-  unit_fin_kernel<K, CX><<<1, kBlock, 0, st>>>(part, grid_for(n), op, out);
+  tl_seq = nullptr;
+  unit_fin_kernel<K, CX><<<1, kBlock, 0, st>>>(part, seq ? 1 : grid_for(n), op, out);
   cudaMemcpyAsync(h_out, out, sizeof(double) * 8, cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   cudaFree(part);
   cudaFree(out);
+  if (seq) cudaFree(seq);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
 int unit_reduce(int k, bool cx, int op, long long n, const double *d_x,
-                const double *d_y, double *h_out, cudaStream_t st) {
-#define DISPATCH(KK)                                                 \
-  if (k == KK)                                                       \
-    return cx ? reduce_typed<KK, true>(op, n, d_x, d_y, h_out, st)   \
-              : reduce_typed<KK, false>(op, n, d_x, d_y, h_out, st);
+                const double *d_y, double *h_out, cudaStream_t st, int seq) {
+#define DISPATCH(KK)                                                      \
+  if (k == KK)                                                            \
+    return cx ? reduce_typed<KK, true>(op, n, d_x, d_y, h_out, st, seq)   \
+              : reduce_typed<KK, false>(op, n, d_x, d_y, h_out, st, seq);
   DISPATCH(2)
   DISPATCH(3)
   DISPATCH(4)
