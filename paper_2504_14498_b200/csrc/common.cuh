@@ -487,6 +487,99 @@ __device__ __forceinline__ Sc finalize_slot(const double *part, int slot,
   return s;  // valid in thread 0
 }
 
+// Reduce the G block partials of NS slots AT ONCE (slot s complex iff the
+// s-th template flag): slot s gets W = kWarpsPerBlock / NS warps, each lane
+// folds a strided subset of the partials, then a lane tree and a tree over
+// the W warps -- the slots' trees run side by side instead of one after the
+// other.  Fixed shape for a given (G, NS): deterministic.  Results are
+// returned in out[] for every thread.  Uses smem[0, 8 * kWarpsPerBlock +
+// 8 * NS) doubles.  All threads must call.
+template <int K, bool C>
+__device__ __forceinline__ void fin_slot_warp(const double *part, int slot, int G,
+                                              int wi, int W, int lane,
+                                              double *wsm) {
+  Acc<K, C> a;
+  a.zero();
+  for (int b = wi * 32 + lane; b < G; b += 32 * W) {
+    Acc<K, C> v;
+    const double *q = part + ((size_t)slot * kMaxGrid + b) * 8;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      v.re[c] = q[c];
+      v.im[c] = q[4 + c];
+    }
+    acc_combine<K, C>(a, v);
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    Acc<K, C> o;
+    acc_shfl_down<K, C>(o, a, off);
+    if (lane < off) acc_combine<K, C>(a, o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      wsm[c] = a.re[c];
+      wsm[4 + c] = C ? a.im[c] : 0.0;
+    }
+  }
+}
+
+template <int K, bool C>
+__device__ __forceinline__ void fin_slot_cross(const double *wsm0, int W,
+                                               int lane, Sc *dst) {
+  Acc<K, C> b;
+  b.zero();
+  if (lane < W) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      b.re[c] = wsm0[lane * 8 + c];
+      b.im[c] = wsm0[lane * 8 + 4 + c];
+    }
+  }
+  for (int off = kWarpsPerBlock / 2; off >= 1; off >>= 1) {
+    if (off >= W) continue;  // uniform
+    Acc<K, C> o;
+    acc_shfl_down<K, C>(o, b, off);
+    if (lane < off) acc_combine<K, C>(b, o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      dst->re[c] = c < K ? b.re[c] : 0.0;
+      dst->im[c] = (C && c < K) ? b.im[c] : 0.0;
+    }
+  }
+}
+
+template <int K, bool... CXS>
+__device__ __forceinline__ void finalize_slots(const double *part, int G,
+                                               double *smem, Sc *out) {
+  constexpr int NS = sizeof...(CXS);
+  static_assert(NS >= 1 && NS <= kWarpsPerBlock, "slots per finalize");
+  constexpr bool cxs[NS] = {CXS...};
+  constexpr int W = kWarpsPerBlock / NS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = warp / W, wi = warp % W;
+  Sc *res = reinterpret_cast<Sc *>(smem + 8 * kWarpsPerBlock);
+  if (s < NS) {
+    if (cxs[s])
+      fin_slot_warp<K, true>(part, s, G, wi, W, lane, smem + 8 * warp);
+    else
+      fin_slot_warp<K, false>(part, s, G, wi, W, lane, smem + 8 * warp);
+  }
+  __syncthreads();
+  if (s < NS && wi == 0) {
+    if (cxs[s])
+      fin_slot_cross<K, true>(smem + 8 * warp, W, lane, res + s);
+    else
+      fin_slot_cross<K, false>(smem + 8 * warp, W, lane, res + s);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < NS; ++t) out[t] = res[t];
+}
+
 inline int grid_for(int64_t n) {
   int64_t g = (n + kBlock - 1) / kBlock;
   if (g < 1) g = 1;

@@ -760,7 +760,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src,
       : "memory");
 }
 
-constexpr int kCsBatch = 8;  // entries whose loads are issued together
+constexpr int kCsBatch = 16;  // entries whose loads are issued together
 
 template <bool CX, bool ADJ>
 __global__ void __launch_bounds__(1024, 1)
@@ -828,10 +828,8 @@ __global__ void __launch_bounds__(1024, 1)
   auto addr = [&](int pk) -> uint32_t {
     return cl_map(vbase + (uint32_t)(pk & 0xFFFFFF) * ESZ, (uint32_t)pk >> 24);
   };
-  bool bad = false;
   for (int g = 0; g < nl; ++g) {
     const int b = g % 3;
-    const bool fwd = g < nf;
     mbar_wait(&bar[b], (uint32_t)((g / 3) & 1));
     const int nd = seg[g].y;
     const CDesc *D = dbuf + b * p.maxdesc;
@@ -875,18 +873,28 @@ __global__ void __launch_bounds__(1024, 1)
         cl_st2(addr(d.out), qr, qi);
       else
         cl_st1(addr(d.out), qr);
-      if (!fwd) {
-        bad = bad || !isfin(qr) || !isfin(qi);
-        if constexpr (CX)
-          reinterpret_cast<double2 *>(a.z)[d.row] = make_double2(qr, qi);
-        else
-          a.z[d.row] = qr;
-      }
     }
+    // no global stores inside the level loop: the release of the cluster
+    // barrier would have to wait for their acknowledgements
     cl_arrive();
     // buffer (g+2)%3 was last read at level g-1, which every CTA finished
     if (tid == 0 && g + 2 < nl) issue(g + 2);
     cl_wait();
+  }
+  // every slot now holds the backward result z of its row: write out the
+  // own slots (coalesced over slots) and check them (NumericBreakdownError)
+  bool bad = false;
+  for (int s = s0 + tid; s < s1; s += T) {
+    const int i = p.slot_row[s];
+    if constexpr (CX) {
+      const double qr = vec[(s - s0) * 2], qi = vec[(s - s0) * 2 + 1];
+      bad = bad || !isfin(qr) || !isfin(qi);
+      reinterpret_cast<double2 *>(a.z)[i] = make_double2(qr, qi);
+    } else {
+      const double qr = vec[s - s0];
+      bad = bad || !isfin(qr);
+      a.z[i] = qr;
+    }
   }
   if (bad) atomicOr(a.err, 1);
 }

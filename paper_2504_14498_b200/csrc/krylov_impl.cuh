@@ -124,9 +124,10 @@ __global__ void relres_kernel(State *S) {
 
 template <int K, bool CX>
 __global__ void true_res_kernel_impl(State *S_, const double *pt_, int G_) {
-  __shared__ double sm[kWarpsPerBlock * 8];
-  const Sc rr = finalize_slot<K, false>(pt_, 0, G_, sm);
-  const Sc bb = finalize_slot<K, false>(pt_, 1, G_, sm);
+  __shared__ double sm[kWarpsPerBlock * 16];
+  Sc o[2];
+  finalize_slots<K, false, false>(pt_, G_, sm, o);
+  const Sc rr = o[0], bb = o[1];
   if (threadIdx.x == 0) {
     S_->true_relres = NAN;
     const Sc nb = sqrt_sc<K>(bb);
@@ -322,8 +323,9 @@ struct Solver : PlanBase {
     double *H = hist;
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
-          const Sc rho = finalize_slot<K, CX>(pt_, 0, G_, sm);
-          const Sc ss = finalize_slot<K, false>(pt_, 1, G_, sm);
+          Sc o[2];
+          finalize_slots<K, CX, false>(pt_, G_, sm, o);
+          const Sc rho = o[0], ss = o[1];
           if (threadIdx.x == 0) {
             S_->rho = rho;
             setup_norm0<K>(S_, H, ss);
@@ -355,10 +357,10 @@ struct Solver : PlanBase {
     // is committed only if the solve continues.
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
-          const Sc rho = finalize_slot<K, CX>(pt_, 0, G_, sm);
           const bool pend = S_->pending != 0;
-          Sc ss = sc_zero();
-          if (pend) ss = finalize_slot<K, false>(pt_, 1, G_, sm);
+          Sc o[2];  // slot 1 (||r||) is only meaningful when pend
+          finalize_slots<K, CX, false>(pt_, G_, sm, o);
+          const Sc rho = o[0], ss = o[1];
           Sc *xs = reinterpret_cast<Sc *>(sm);
           if (threadIdx.x == 0) xs[2] = rho;
           __syncthreads();
@@ -478,8 +480,9 @@ struct Solver : PlanBase {
     // F4: omega
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
-          const Sc tt = finalize_slot<K, CX>(pt_, 0, G_, sm);
-          const Sc ts = finalize_slot<K, CX>(pt_, 1, G_, sm);
+          Sc o[2];
+          finalize_slots<K, CX, CX>(pt_, G_, sm, o);
+          const Sc tt = o[0], ts = o[1];
           if (threadIdx.x == 0) {
             if (s_is_zero<K, CX>(tt)) {
               finish_state(S_, S_->it, 0, kBdOmegaZero);
@@ -771,15 +774,17 @@ struct Solver : PlanBase {
                       });
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
-          const Sc btbt = finalize_slot<K, CX>(pt_, 0, G_, sm);
-          const Sc btt = finalize_slot<K, CX>(pt_, 1, G_, sm);
           const bool more = S_->it > 1;  // uniform
+          // all six slots side by side (slots 2-5 are stale when !more)
+          Sc o[6];
+          finalize_slots<K, CX, CX, CX, CX, CX, CX>(pt_, G_, sm, o);
+          const Sc btbt = o[0], btt = o[1];
           Sc yy = sc_zero(), ybt = sc_zero(), bty = sc_zero(), yt = sc_zero();
           if (more) {
-            yy = finalize_slot<K, CX>(pt_, 2, G_, sm);
-            ybt = finalize_slot<K, CX>(pt_, 3, G_, sm);
-            bty = finalize_slot<K, CX>(pt_, 4, G_, sm);
-            yt = finalize_slot<K, CX>(pt_, 5, G_, sm);
+            yy = o[2];
+            ybt = o[3];
+            bty = o[4];
+            yt = o[5];
           }
           if (!more) {
             if (threadIdx.x == 0) {
@@ -881,8 +886,9 @@ struct Solver : PlanBase {
                       });
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
-          const Sc rn = finalize_slot<K, CX>(pt_, 0, G_, sm);
-          const Sc ss = finalize_slot<K, false>(pt_, 1, G_, sm);
+          Sc o[2];
+          finalize_slots<K, CX, false>(pt_, G_, sm, o);
+          const Sc rn = o[0], ss = o[1];
           // norm test (warp 0) and the two quotients of beta (warps 1, 2)
           // run concurrently; beta is only committed if the test continues
           Sc *xs = reinterpret_cast<Sc *>(sm);

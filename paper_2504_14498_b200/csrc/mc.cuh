@@ -98,6 +98,13 @@ MPK_HD bool isfin(double a) {
 #endif
 }
 MPK_HD double dabs(double a) { return fabs(a); }
+MPK_HD int __builtin_ctz_dev(unsigned m) {
+#ifdef __CUDA_ARCH__
+  return __ffs((int)m) - 1;
+#else
+  return __builtin_ctz(m);
+#endif
+}
 
 // two_sum _mccore.py:19-24
 MPK_HD void two_sum(double a, double b, double &s, double &e) {
@@ -142,7 +149,6 @@ MPK_HD void two_prod(double a, double b, double &p, double &e) {
     e = dekker_err(a, b, p);
 }
 
-// renorm_terms _mccore.py:90-116 on M register slots (holes = +0.0).
 // finite test on the exponent bits (2 integer ops, no branch)
 MPK_HD bool fin_bits(double x) {
 #ifdef __CUDA_ARCH__
@@ -152,31 +158,57 @@ MPK_HD bool fin_bits(double x) {
 #endif
 }
 
-// Exact error of q = fl(a + b) by Fast2Sum on the larger-magnitude operand
-// (Dekker: exact for finite a, b when a + b does not overflow).  The error
-// of an addition is unique, so this equals TwoSum's value -- up to the sign
-// of a zero error, which renorm's second sweep never observes (it only
-// tests en != 0).  Critical path: 2 DADDs after q instead of 4.
-MPK_HD double fast_err(double a, double b, double q) {
-  const bool ab = dabs(a) >= dabs(b);
-  const double big = ab ? a : b, sml = ab ? b : a;
-  return dsub(sml, dsub(q, big));
-}
-
-// |x| < 2^1000 (or zero): no partial sum of <= 16 such terms can overflow
-MPK_HD bool no_ovf(double x) {
+// Bit-level helpers (integer pipe): for finite values, |a| >= |b| iff the
+// sign-cleared bit patterns compare so as unsigned integers, and x != 0.0
+// iff its sign-cleared pattern is nonzero (NaN also counts as nonzero).
+MPK_HD unsigned long long dbits(double x) {
 #ifdef __CUDA_ARCH__
-  return (__double2hiint(x) & 0x7ff00000) < ((1023 + 1000) << 20);
+  return (unsigned long long)__double_as_longlong(x);
 #else
-  return std::fabs(x) < 0x1p1000;
+  unsigned long long u;
+  std::memcpy(&u, &x, sizeof u);
+  return u;
 #endif
 }
+MPK_HD unsigned long long mag(double x) { return dbits(x) & 0x7FFFFFFFFFFFFFFFull; }
+MPK_HD bool nzb(double x) { return mag(x) != 0ull; }
 
+// |x| < 2^1000 (and finite): no partial sum of <= 16 such terms can overflow
+MPK_HD bool no_ovf(double x) {
+  return mag(x) < ((unsigned long long)(1023 + 1000) << 52);
+}
+
+// implementation knobs (A/B-measured, see tools/ubench/mclat.cu)
+#ifndef MPK_RN_COMPACT
+#define MPK_RN_COMPACT 0  // 0: select chain, 1: local-array gather
+#endif
+#ifndef MPK_RN_INTCMP
+#define MPK_RN_INTCMP 0   // magnitude / zero tests: 0 FP64 pipe, 1 integer pipe
+#endif
+#ifndef MPK_RN_S1FAST
+#define MPK_RN_S1FAST 0   // sweep 1 errors by Fast2Sum (1) or TwoSum (0)
+#endif
 #ifdef MPK_COUNT_PASSES
 __device__ unsigned long long g_pass_hist[20][8];
 #endif
-// The pass loop of renorm_terms (_mccore.py:90-116).  fast: the Fast2Sum
-// error in the second sweep (valid when no partial sum can overflow).
+#ifdef MPK_RENORM_TIMING
+__device__ long long g_rt[16];
+#endif
+#if defined(MPK_RENORM_TIMING) && defined(__CUDA_ARCH__)
+#define MPK_RT(k) (g_rt[k] = clock64())
+#else
+#define MPK_RT(k) ((void)0)
+#endif
+
+// The pass loop of renorm_terms (_mccore.py:90-116).
+//
+// fast (all terms finite and below 2^1000, so no partial sum overflows):
+// every TwoSum error is computed by Fast2Sum on the larger-magnitude
+// operand, chosen by an integer compare beside the sum.  The error of an
+// addition is unique, so the value equals TwoSum's; a zero error is forced
+// to +0.0, which is what TwoSum yields for an exact sum (x - x = +0 in
+// round-to-nearest), so even the signs of zeros agree.  In sweep 2 the sign
+// of a zero error is never observed (only en != 0 is tested).
 template <int M, bool fast>
 MPK_HD void renorm_passes(double (&t)[M]) {
 #pragma unroll 1
@@ -186,73 +218,91 @@ MPK_HD void renorm_passes(double (&t)[M]) {
 #pragma unroll
     for (int i = M - 2; i >= 0; --i) {
       double q, err;
-      two_sum(t[i], s, q, err);
+      if constexpr (fast && MPK_RN_S1FAST) {
+        const double a = t[i];
+        q = dadd(a, s);
+        const bool ge = MPK_RN_INTCMP ? (mag(a) >= mag(s)) : (dabs(a) >= dabs(s));
+        const double big = ge ? a : s, sml = ge ? s : a;
+        err = dsub(sml, dsub(q, big));
+        err = (MPK_RN_INTCMP ? nzb(err) : (err != 0.0)) ? err : 0.0;
+      } else {
+        two_sum(t[i], s, q, err);
+      }
       e[i + 1] = err;
       s = q;
     }
     e[0] = s;
+    MPK_RT(2);
     double eps = e[0];
-    if constexpr (fast) {
 #pragma unroll
-      for (int i = 1; i < M; ++i) {
-        const double q = dadd(eps, e[i]);
-        const double en = fast_err(eps, e[i], q);
-        const bool em = (en != 0.0);
-        t[i - 1] = em ? q : 0.0;
-        eps = em ? en : q;
-      }
-    } else {
-#pragma unroll
-      for (int i = 1; i < M; ++i) {
-        double q, en;
+    for (int i = 1; i < M; ++i) {
+      double q, en;
+      if constexpr (fast) {
+        const double ei = e[i];
+        q = dadd(eps, ei);
+        const bool ge = MPK_RN_INTCMP ? (mag(eps) >= mag(ei)) : (dabs(eps) >= dabs(ei));
+        const double big = ge ? eps : ei, sml = ge ? ei : eps;
+        en = dsub(sml, dsub(q, big));
+      } else {
         two_sum(eps, e[i], q, en);
-        const bool em = (en != 0.0);
-        t[i - 1] = em ? q : 0.0;
-        eps = em ? en : q;
       }
+      const bool em = MPK_RN_INTCMP ? nzb(en) : (en != 0.0);
+      t[i - 1] = em ? q : 0.0;
+      eps = em ? en : q;
     }
     t[M - 1] = eps;
-    // strictness over consecutive non-hole components (branch-free)
+    MPK_RT(3);
+    // strictness over consecutive non-hole components (branch-free); for a
+    // nonzero finite prev, fl(prev + c) != prev iff the bit patterns differ
     bool ok = true;
     double prev = 0.0;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       const double c = t[i];
+#if MPK_RN_INTCMP
+      const bool nz = nzb(c);
+      const bool viol = nz & nzb(prev) & (dbits(dadd(prev, c)) != dbits(prev));
+#else
       const bool nz = (c != 0.0);
       const bool viol = nz & (prev != 0.0) & (dadd(prev, c) != prev);
+#endif
       ok = ok & !viol;
       prev = nz ? c : prev;
     }
 #if defined(MPK_COUNT_PASSES) && defined(__CUDA_ARCH__)
     atomicAdd(&g_pass_hist[M][pass], 1ull);
 #endif
+    MPK_RT(4);
     if (ok) break;
   }
 }
 
 template <int M, int K>
 MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
-  bool fin = true, small = true;
+  MPK_RT(0);
+  bool small = true;
 #pragma unroll
-  for (int i = 0; i < M; ++i) {
-    fin = fin & fin_bits(t[i]);
-    small = small & no_ovf(t[i]);
-  }
-  if (!fin) {
-    double s = 0.0;
+  for (int i = 0; i < M; ++i) small = small & no_ovf(t[i]);
+  if (!small) {
+    bool fin = true;
 #pragma unroll
-    for (int i = 0; i < M; ++i) s = dadd(s, t[i]);
-    out[0] = s;
+    for (int i = 0; i < M; ++i) fin = fin & fin_bits(t[i]);
+    if (!fin) {
+      double s = 0.0;
 #pragma unroll
-    for (int i = 1; i < K; ++i) out[i] = 0.0;
-    return;
-  }
-  // both pass loops inline: a call on the fast path costs more than the
-  // code (the branch is uniform in practice)
-  if (small)
-    renorm_passes<M, true>(t);
-  else
+      for (int i = 0; i < M; ++i) s = dadd(s, t[i]);
+      out[0] = s;
+#pragma unroll
+      for (int i = 1; i < K; ++i) out[i] = 0.0;
+      return;
+    }
     renorm_passes<M, false>(t);
+  } else {
+    MPK_RT(1);
+    renorm_passes<M, true>(t);
+    MPK_RT(5);
+  }
+#if MPK_RN_COMPACT == 0
   // first K non-hole components (branch-free predicated selects)
 #pragma unroll
   for (int j = 0; j < K; ++j) out[j] = 0.0;
@@ -265,6 +315,24 @@ MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
     for (int j = 0; j < K; ++j) out[j] = (nz & (cnt == j)) ? c : out[j];
     cnt += nz ? 1 : 0;
   }
+#else
+  // first K non-hole components: positions by clearing the lowest set bit
+  // of the nonzero mask, values gathered from a local copy (independent
+  // loads instead of a select chain through a running count)
+  unsigned mask = 0u;
+#pragma unroll
+  for (int i = 0; i < M; ++i) mask |= nzb(t[i]) ? (1u << i) : 0u;
+  double tl[M];
+#pragma unroll
+  for (int i = 0; i < M; ++i) tl[i] = t[i];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int p = mask ? (__builtin_ctz_dev(mask)) : 0;
+    out[j] = mask ? tl[p] : 0.0;
+    mask &= mask - 1u;
+  }
+#endif
+  MPK_RT(6);
 }
 
 // Reference merge of two component lists by magnitude, ties prefer x
@@ -272,9 +340,9 @@ MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
 // The two inputs are consumed as shift registers (heads xq[0] / yq[0]) so
 // every index is static: a dynamically indexed x[i] is lowered to local
 // memory, which put an L1 round trip on each merge step.
-template <int KX, int KY>
-MPK_HD void merge(const double (&x)[KX], const double (&y)[KY],
-                  double (&buf)[KX + KY]) {
+template <int KX, int KY, bool INTCMP>
+MPK_HD void merge_q(const double (&x)[KX], const double (&y)[KY],
+                    double (&buf)[KX + KY]) {
   double xq[KX], yq[KY];
 #pragma unroll
   for (int a = 0; a < KX; ++a) xq[a] = x[a];
@@ -284,7 +352,9 @@ MPK_HD void merge(const double (&x)[KX], const double (&y)[KY],
 #pragma unroll
   for (int t = 0; t < KX + KY; ++t) {
     const bool xv = nx > 0, yv = ny > 0;
-    const bool tx = xv && (!yv || dabs(xq[0]) >= dabs(yq[0]));
+    const bool ge = (INTCMP && MPK_RN_INTCMP) ? (mag(xq[0]) >= mag(yq[0]))
+                                              : (dabs(xq[0]) >= dabs(yq[0]));
+    const bool tx = xv && (!yv || ge);
     buf[t] = tx ? xq[0] : yq[0];
 #pragma unroll
     for (int a = 0; a + 1 < KX; ++a) xq[a] = tx ? xq[a + 1] : xq[a];
@@ -293,6 +363,22 @@ MPK_HD void merge(const double (&x)[KX], const double (&y)[KY],
     nx -= tx ? 1 : 0;
     ny -= tx ? 0 : 1;
   }
+}
+
+// magnitude compares on the integer pipe when every input is finite (for
+// NaN the IEEE compare is false, which the integer one would not reproduce)
+template <int KX, int KY>
+MPK_HD void merge(const double (&x)[KX], const double (&y)[KY],
+                  double (&buf)[KX + KY]) {
+  bool fin = true;
+#pragma unroll
+  for (int a = 0; a < KX; ++a) fin = fin & fin_bits(x[a]);
+#pragma unroll
+  for (int a = 0; a < KY; ++a) fin = fin & fin_bits(y[a]);
+  if (fin)
+    merge_q<KX, KY, true>(x, y, buf);
+  else
+    merge_q<KX, KY, false>(x, y, buf);
 }
 
 // mc_add _mccore.py:129-155

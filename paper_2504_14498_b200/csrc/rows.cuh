@@ -91,8 +91,14 @@ struct Red {
   }
 };
 
+// at least kRowsMinBlocks blocks per SM: caps registers so more warps stay
+// resident (the row kernels are latency-bound chains of MC operations, and
+// concurrent solves compete for warp slots)
+#ifndef MPK_ROWS_MIN_BLOCKS
+#define MPK_ROWS_MIN_BLOCKS 3
+#endif
 template <int K, bool CX, int NH, int NN, class F>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, MPK_ROWS_MIN_BLOCKS)
     rows_kernel(long long n, const int *done, double *part, double *seq, F f) {
   if (done && *done) return;
   __shared__ double smem[kWarpsPerBlock * 8];
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(kBlock)
     }
     return;
   }
-  __shared__ double smem[kWarpsPerBlock * 8];
+  __shared__ double smem[kWarpsPerBlock * 16];  // finalize_slots scratch
   f(S, part, G, smem);
 }
 
