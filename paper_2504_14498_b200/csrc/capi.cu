@@ -201,19 +201,16 @@ static int env_int(const char *name, int dflt) {
 }
 
 // Cluster sweep plan (ilu.cuh CSweep) for the phase pair (f, b).  Rows of a
-// level are split over the C CTAs in contiguous chunks of about equal work;
-// a row's storage slot is fixed by its forward-phase CTA.  Returns false if
-// the plan does not fit in shared memory.
-static bool build_cplan(CSweep &p, int n, bool cx, const HPhase &f,
-                        const HPhase &b, cudaStream_t st) {
-  const int cmax = env_int("MPK_CSWEEP_C", 8);
-  if (cmax <= 0 || n == 0) return false;
-  const int maxw = std::max(f.maxw, b.maxw);
-  int C = std::min(cmax, std::max(1, maxw / env_int("MPK_CSWEEP_ROWS", 24)));
-  if (C > 16) C = 16;
+// level are split over the C CTAs in contiguous chunks of about equal work.
+// Replicated vector when it fits next to the staging buffers (smallest such
+// C from 2 up, or MPK_CSWEEP_C), else the distributed layout.  Returns false
+// if no layout fits in shared memory.
+static bool build_cplan_c(CSweep &p, int n, bool cx, const HPhase &f,
+                          const HPhase &b, int C, bool repl, bool commit,
+                          cudaStream_t st) {
   const int nl = f.nlev + b.nlev;
   if (nl > 8192) return false;
-  // split of every level: cta[r] for each position of each phase
+  const size_t esz = cx ? 16 : 8;
   auto split = [&](const HPhase &h, std::vector<int> &cta) {
     cta.assign(n, 0);
     for (int L = 0; L < h.nlev; ++L) {
@@ -234,93 +231,256 @@ static bool build_cplan(CSweep &p, int n, bool cx, const HPhase &f,
   std::vector<std::vector<int>> srow(C);
   for (int r = 0; r < n; ++r) {  // level order -> slots in compute order
     const int i = f.desc[r].x, c = cf[r];
-    pk[i] = (c << 24) | nslot[c]++;
-    srow[c].push_back(i);
+    pk[i] = repl ? i : ((c << 24) | nslot[c]++);
+    if (!repl) srow[c].push_back(i);
   }
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  // sizes first (cheap), then the stream only when committing
   std::vector<int4> seg((size_t)nl * C);
-  std::vector<CDesc> desc;
-  std::vector<int> dsrc, esrc, epk;
-  desc.reserve(2 * (size_t)n);
-  int maxdesc = 0, maxent = 0;
+  size_t total = 0, maxseg = 0;
+  int maxnd = 0;
+  std::vector<std::vector<int>> rows_of(C);
   for (int g = 0; g < nl; ++g) {
     const bool fw = g < f.nlev;
     const HPhase &h = fw ? f : b;
     const std::vector<int> &cta = fw ? cf : cb;
     const int L = fw ? g : g - f.nlev;
+    for (int c = 0; c < C; ++c) rows_of[c].clear();
+    for (int r = h.lev[L]; r < h.lev[L + 1]; ++r) rows_of[cta[r]].push_back(r);
     for (int c = 0; c < C; ++c) {
-      const int d0 = (int)desc.size(), x0 = (int)esrc.size();
-      for (int r = h.lev[L]; r < h.lev[L + 1]; ++r) {
-        if (cta[r] != c) continue;
-        const int4 hd = h.desc[r];
-        CDesc d{};
-        d.init = pk[hd.x];
-        d.out = pk[hd.x];
-        d.e0 = (int)esrc.size() - x0;
-        d.cnt = hd.z;
-        d.row = hd.x;
-        d.hasdiv = h.dsrc[r] >= 0 ? 1 : 0;
-        d.dr = 1.0;
-        d.di = 0.0;
-        desc.push_back(d);
-        dsrc.push_back(h.dsrc[r]);
-        for (int q = hd.y; q < hd.y + hd.z; ++q) {
-          esrc.push_back(h.src[q]);
-          epk.push_back(pk[h.col[q]]);
-        }
-      }
-      const int nd = (int)desc.size() - d0, ne = (int)esrc.size() - x0;
-      seg[(size_t)g * C + c] = make_int4(d0, nd, x0, ne);
-      maxdesc = std::max(maxdesc, nd);
-      maxent = std::max(maxent, ne);
+      int nd = (int)rows_of[c].size(), ne = 0;
+      for (int r : rows_of[c]) ne += h.desc[r].z + (h.dsrc[r] >= 0 ? 1 : 0);
+      const size_t bytes = nd ? a16(16 * (size_t)nd + a16(4 * (size_t)ne) + esz * ne) : 0;
+      seg[(size_t)g * C + c] = make_int4((int)(total >> 4), (int)bytes, nd, ne);
+      total += bytes;
+      maxseg = std::max(maxseg, bytes);
+      maxnd = std::max(maxnd, nd);
     }
   }
   int maxslots = 0;
   for (int c = 0; c < C; ++c) maxslots = std::max(maxslots, nslot[c]);
-  const size_t esz = cx ? sizeof(CEntC) : sizeof(CEntR);
-  const size_t smem = 48 + (size_t)nl * 16 +
-                      ((size_t)maxslots * (cx ? 16 : 8) + 15) / 16 * 16 +
-                      3 * (size_t)maxdesc * sizeof(CDesc) + 3 * (size_t)maxent * esz;
-  if (smem > csweep_smem_limit()) return false;
+  if (repl) maxslots = n;
+  if ((total >> 4) > (size_t)INT_MAX) return false;
+  auto smem_for = [&](int nb) {
+    return 80 + (size_t)nl * 16 + a16((size_t)maxslots * esz) + nb * maxseg;
+  };
+  int nb = std::min(8, std::max(3, env_int("MPK_CSWEEP_NBUF", 4)));
+  while (nb > 3 && smem_for(nb) > csweep_smem_limit()) --nb;
+  if (smem_for(nb) > csweep_smem_limit()) return false;
+  if (!commit) return true;
+  std::vector<unsigned char> stream(total, 0);
+  std::vector<long long> eoff;
+  std::vector<int> esrc;
+  for (int g = 0; g < nl; ++g) {
+    const bool fw = g < f.nlev;
+    const HPhase &h = fw ? f : b;
+    const std::vector<int> &cta = fw ? cf : cb;
+    const int L = fw ? g : g - f.nlev;
+    for (int c = 0; c < C; ++c) rows_of[c].clear();
+    for (int r = h.lev[L]; r < h.lev[L + 1]; ++r) rows_of[cta[r]].push_back(r);
+    for (int c = 0; c < C; ++c) {
+      const int4 sg = seg[(size_t)g * C + c];
+      if (!sg.z) continue;
+      const size_t off = (size_t)sg.x << 4;
+      unsigned char *q = stream.data() + off;
+      const size_t refs_off = 16 * (size_t)sg.z;
+      const size_t vals_off = refs_off + a16(4 * (size_t)sg.w);
+      int e = 0, k = 0;
+      for (int r : rows_of[c]) {
+        const int4 hd = h.desc[r];
+        const bool dv = h.dsrc[r] >= 0;
+        CSDesc d{pk[hd.x], e, hd.z, dv ? 1 : 0};
+        std::memcpy(q + 16 * (size_t)k++, &d, sizeof d);
+        const double one = 1.0;  // placeholder until the first gather
+        for (int t = hd.y; t < hd.y + hd.z; ++t, ++e) {
+          const int ref = pk[h.col[t]];
+          std::memcpy(q + refs_off + 4 * (size_t)e, &ref, 4);
+          std::memcpy(q + vals_off + esz * (size_t)e, &one, 8);
+          eoff.push_back((long long)((off + vals_off + esz * (size_t)e) / 8));
+          esrc.push_back(h.src[t]);
+        }
+        if (dv) {
+          std::memcpy(q + vals_off + esz * (size_t)e, &one, 8);
+          eoff.push_back((long long)((off + vals_off + esz * (size_t)e) / 8));
+          esrc.push_back(h.dsrc[r]);
+          ++e;
+        }
+      }
+    }
+  }
   p.C = C;
-  p.T = std::min(1024, std::max(64, (maxdesc + 31) / 32 * 32));
+  p.T = std::min(1024, std::max(64, (maxnd + 31) / 32 * 32));
   p.nl = nl;
   p.nf = f.nlev;
-  p.ndesc = (long long)desc.size();
-  p.nent = (long long)esrc.size();
+  p.repl = repl ? 1 : 0;
+  p.nbuf = nb;
+  p.nval = (long long)esrc.size();
   p.maxslots = maxslots;
-  p.maxdesc = maxdesc;
-  p.maxent = maxent;
-  p.smem = smem;
+  p.maxseg = (int)maxseg;
+  p.smem = smem_for(nb);
   std::vector<int> slot_row, slot_off(C + 1, 0);
   for (int c = 0; c < C; ++c) {
-    slot_off[c + 1] = slot_off[c] + nslot[c];
+    slot_off[c + 1] = slot_off[c] + (int)srow[c].size();
     slot_row.insert(slot_row.end(), srow[c].begin(), srow[c].end());
   }
   upload(&p.seg, seg, st);
-  upload(&p.desc, desc, st);
-  upload(&p.dsrc, dsrc, st);
+  upload(&p.stream, stream, st);
+  upload(&p.eoff, eoff, st);
   upload(&p.esrc, esrc, st);
   upload(&p.slot_row, slot_row, st);
   upload(&p.slot_off, slot_off, st);
-  if (cx) {
-    std::vector<CEntC> e(esrc.size());
-    for (size_t t = 0; t < e.size(); ++t) e[t] = CEntC{0.0, 0.0, epk[t], {0, 0, 0}};
-    CEntC *d = nullptr;
-    upload(&d, e, st);
-    p.ent = d;
-  } else {
-    std::vector<CEntR> e(esrc.size());
-    for (size_t t = 0; t < e.size(); ++t) e[t] = CEntR{0.0, epk[t], 0};
-    CEntR *d = nullptr;
-    upload(&d, e, st);
-    p.ent = d;
-  }
   cudaStreamSynchronize(st);  // host staging vectors die here
   return true;
 }
 
+static bool build_cplan(CSweep &p, int n, bool cx, const HPhase &f,
+                        const HPhase &b, cudaStream_t st) {
+  if (n == 0) return false;
+  const int cenv = env_int("MPK_CSWEEP_C", 0);
+  const int renv = env_int("MPK_CSWEEP_REPL", -1);
+  const int cs[] = {2, 4, 8, 16};
+  if (renv != 0) {  // replicated: smallest C that fits (or the forced one)
+    for (int C : cs) {
+      if (cenv && C != cenv) continue;
+      if (build_cplan_c(p, n, cx, f, b, C, true, false, st))
+        return build_cplan_c(p, n, cx, f, b, C, true, true, st);
+    }
+    if (cenv == 1 && build_cplan_c(p, n, cx, f, b, 1, true, false, st))
+      return build_cplan_c(p, n, cx, f, b, 1, true, true, st);
+  }
+  if (renv == 1) return false;
+  const int maxw = std::max(f.maxw, b.maxw);
+  int C = cenv ? cenv : std::min(8, std::max(1, maxw / env_int("MPK_CSWEEP_ROWS", 24)));
+  if (C > 16) C = 16;
+  if (build_cplan_c(p, n, cx, f, b, C, false, false, st))
+    return build_cplan_c(p, n, cx, f, b, C, false, true, st);
+  return false;
+}
+
+// Ring sweep plan (ilu.cuh RSweep) for the phase pair (f, b): the stream of
+// chunks (rows of one level, at most `slot` bytes each) in forward-then-
+// backward level order.  Returns false when the vector plus a useful ring
+// does not fit in one SM's shared memory.
+static bool build_rplan(RSweep &p, int n, bool cx, const HPhase &f,
+                        const HPhase &b, cudaStream_t st) {
+  if (n == 0) return false;
+  const size_t esz = cx ? 16 : 8, vsz = cx ? 16 : 8;
+  const size_t vec = ((size_t)n * esz + 15) / 16 * 16;
+  const size_t limit = csweep_smem_limit();
+  const int S = 4;
+  // chunk table <= 8 B per chunk; bound the count by rows + levels
+  const size_t tab_max = 8 * (size_t)(2 * n + f.nlev + b.nlev + 64);
+  const size_t fixed = ((16 * S + 16 + 15) / 16) * 16 + vec;
+  if (fixed + 4 * 4096 > limit) return false;
+  size_t slot = std::min<size_t>(48 * 1024, (limit - fixed - std::min(tab_max, (size_t)16384)) / S);
+  slot = slot / 16 * 16;
+  if (slot < 4096) return false;
+  struct Row { int row, cnt, dsrc, e0; };
+  std::vector<unsigned char> stream;
+  std::vector<RChunk> chunks;
+  std::vector<long long> eoff, doff;
+  std::vector<int> esrc, dsrcv;
+  int maxrows = 0;
+  bool fits = true;
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  auto emit = [&](const HPhase &h, bool fw, int lo, int hi, bool end) {
+    // rows [lo, hi) of phase h (positions in its level order)
+    int nent = 0;
+    for (int r = lo; r < hi; ++r) nent += h.desc[r].z;
+    const int nr = hi - lo;
+    const size_t cols_off = 16 + 32 * (size_t)nr;
+    const size_t vals_off = cols_off + a16((size_t)nent * 4);
+    const size_t bytes = a16(vals_off + (size_t)nent * vsz);
+    if (bytes > slot) fits = false;  // one row larger than a ring slot
+    const size_t off = stream.size();
+    stream.resize(off + bytes, 0);
+    unsigned char *q = stream.data() + off;
+    const int hdr[4] = {nr, nent, end ? 1 : 0, fw ? 1 : 0};
+    std::memcpy(q, hdr, 16);
+    int e = 0;
+    for (int r = lo; r < hi; ++r) {
+      const int4 hd = h.desc[r];
+      RDesc d{};
+      d.row = hd.x;
+      d.e0 = e;
+      d.cnt = hd.z;
+      d.hasdiv = h.dsrc[r] >= 0 ? 1 : 0;
+      d.dr = 1.0;
+      d.di = 0.0;
+      std::memcpy(q + 16 + 32 * (size_t)(r - lo), &d, sizeof d);
+      doff.push_back((long long)((off + 16 + 32 * (size_t)(r - lo) + 16) / 8));
+      dsrcv.push_back(h.dsrc[r]);
+      for (int t = hd.y; t < hd.y + hd.z; ++t, ++e) {
+        const int c = h.col[t];
+        std::memcpy(q + cols_off + 4 * (size_t)e, &c, 4);
+        const double one = 1.0;  // placeholder until the first gather
+        std::memcpy(q + vals_off + vsz * (size_t)e, &one, 8);
+        eoff.push_back((long long)((off + vals_off + vsz * (size_t)e) / 8));
+        esrc.push_back(h.src[t]);
+      }
+    }
+    RChunk ch{};
+    ch.off = (long long)off;
+    ch.bytes = (int)bytes;
+    ch.nrows = nr;
+    ch.nent = nent;
+    ch.level_end = end ? 1 : 0;
+    ch.fwd = fw ? 1 : 0;
+    chunks.push_back(ch);
+    maxrows = std::max(maxrows, nr);
+    return true;
+  };
+  auto phase = [&](const HPhase &h, bool fw) -> bool {
+    for (int L = 0; L < h.nlev; ++L) {
+      int lo = h.lev[L];
+      int ne = 0;
+      for (int r = h.lev[L]; r < h.lev[L + 1]; ++r) {
+        const int c = h.desc[r].z;
+        const size_t nb = a16(16 + 32 * (size_t)(r - lo + 1)) + a16((size_t)(ne + c) * 4) +
+                          a16((size_t)(ne + c) * vsz);
+        if (nb > slot) {
+          if (r == lo) return false;  // a single row exceeds the slot
+          emit(h, fw, lo, r, false);
+          lo = r;
+          ne = 0;
+        }
+        ne += c;
+      }
+      emit(h, fw, lo, h.lev[L + 1], true);
+    }
+    return true;
+  };
+  if (!phase(f, true) || !phase(b, false) || !fits) return false;
+  const size_t tab = ((8 * chunks.size() + 15) / 16) * 16;
+  const size_t smem = fixed + tab + S * slot;
+  if (smem > limit) return false;
+  p.nchunks = (int)chunks.size();
+  p.S = S;
+  p.slot = (int)slot;
+  const int nc = std::min(992, std::max(32, (maxrows + 31) / 32 * 32));
+  p.T = nc + 32;
+  p.nent = (long long)esrc.size();
+  p.ndesc = (long long)dsrcv.size();
+  p.smem = smem;
+  upload(&p.stream, stream, st);
+  upload(&p.chunks, chunks, st);
+  upload(&p.eoff, eoff, st);
+  upload(&p.esrc, esrc, st);
+  upload(&p.doff, doff, st);
+  upload(&p.dsrc, dsrcv, st);
+  cudaStreamSynchronize(st);  // host staging vectors die here
+  return true;
+}
+
+static void free_rplan(RSweep &p) {
+  void *q[] = {p.stream, p.chunks, p.eoff, p.esrc, p.doff, p.dsrc};
+  for (void *v : q)
+    if (v) cudaFree(v);
+  p = RSweep{};
+}
+
 static void free_cplan(CSweep &p) {
-  void *q[] = {p.seg, p.desc, p.dsrc, p.ent, p.esrc, p.slot_row, p.slot_off};
+  void *q[] = {p.seg, p.stream, p.eoff, p.esrc, p.slot_row, p.slot_off};
   for (void *v : q)
     if (v) cudaFree(v);
   p = CSweep{};
@@ -328,15 +488,82 @@ static void free_cplan(CSweep &p) {
 
 // Sweep structures of one apply direction: the single-CTA sweep matrices
 // when the vector fits one SM, and the cluster plan when it fits a cluster.
+// Average device time of `reps` applies through one sweep plan (dummy input;
+// the plans hold placeholder values before the first factorization).
+static float time_plan(SweepMats &sm, int n, bool cx, bool adjoint, int which,
+                       cudaStream_t st) {
+  double *in = nullptr, *z = nullptr;
+  int *err = nullptr;
+  const size_t w = cx ? 2 : 1;
+  cudaMalloc(&in, sizeof(double) * w * n + 16);
+  cudaMalloc(&z, sizeof(double) * w * n + 16);
+  cudaMalloc(&err, sizeof(int) * 4);
+  cudaMemsetAsync(in, 0, sizeof(double) * w * n + 16, st);
+  SweepArgs a{};
+  a.n = n;
+  a.in_re = in;
+  a.in_im = cx ? in + n : nullptr;
+  a.z = z;
+  a.y = z;
+  a.err = err;
+  a.done = nullptr;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const long long l0 = tl_launches;
+  auto go = [&]() {
+    if (which == 0)
+      launch_rsweep(a, sm.rs, cx, adjoint, st);
+    else
+      launch_csweep(a, sm.cs, cx, adjoint, st);
+  };
+  go();  // warm-up (attributes, code)
+  cudaEventRecord(e0, st);
+  const int reps = 3;
+  for (int r = 0; r < reps; ++r) go();
+  cudaEventRecord(e1, st);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  tl_launches = l0;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(in);
+  cudaFree(z);
+  cudaFree(err);
+  if (cudaGetLastError() != cudaSuccess) return 1e30f;
+  return ms / reps;
+}
+
+// Sweep structures of one apply direction: the single-CTA sweep matrices
+// when the vector fits one SM, the ring plan (one SM, vector + streamed
+// entries in shared memory) and the cluster plan; when both of the latter
+// exist, the faster one on this device is kept (timed here, once per
+// pattern; MPK_SWEEP_PICK=ring|cluster overrides).
 static bool build_sweeps(SweepMats &sm, int n, bool cx, const HPhase &f,
-                         const HPhase &b, cudaStream_t st) {
+                         const HPhase &b, bool adjoint, cudaStream_t st) {
   bool single = false;
   if (sweep_uses_smem(n, cx)) {
     build_phase(sm.fwd, n, cx, f, st);
     build_phase(sm.bwd, n, cx, b, st);
     single = true;
   }
+  if (env_int("MPK_RSWEEP", 1)) build_rplan(sm.rs, n, cx, f, b, st);
   if (env_int("MPK_CSWEEP", 1)) build_cplan(sm.cs, n, cx, f, b, st);
+  if (sm.rs.nchunks > 0 && sm.cs.C > 0) {
+    const char *pick = getenv("MPK_SWEEP_PICK");
+    int keep;
+    if (pick && !strcmp(pick, "ring"))
+      keep = 0;
+    else if (pick && !strcmp(pick, "cluster"))
+      keep = 1;
+    else
+      keep = time_plan(sm, n, cx, adjoint, 0, st) <= time_plan(sm, n, cx, adjoint, 1, st) ? 0 : 1;
+    if (keep == 0)
+      free_cplan(sm.cs);
+    else
+      free_rplan(sm.rs);
+  }
   return single;
 }
 
@@ -365,6 +592,7 @@ static void free_sweeps(SweepMats &sm) {
   free_phase(sm.fwd);
   free_phase(sm.bwd);
   free_cplan(sm.cs);
+  free_rplan(sm.rs);
 }
 
 }  // namespace
@@ -446,7 +674,7 @@ void ensure_adjoint(DMat &A, cudaStream_t st) {
             for (int q = lcnt[c]; q < lcnt[c + 1]; ++q) cb(lt_ci[q], lt_perm[q]);
           },
           [&](int) { return -1; });
-      A.smat_adj_built = build_sweeps(A.smat_adj, n, cx, hf, hb, st);
+      A.smat_adj_built = build_sweeps(A.smat_adj, n, cx, hf, hb, true, st);
       A.smat_adj.conj = true;
     }
     const size_t w = cx ? 2 : 1;
@@ -465,6 +693,7 @@ void ensure_adjoint(DMat &A, cudaStream_t st) {
       gather_phase(A.lu, A.smat_adj.bwd, n, cx, st);
     }
     gather_csweep(A.lu, A.smat_adj.cs, cx, st);
+    gather_rsweep(A.lu, A.smat_adj.rs, cx, st);
     A.adj_ready = true;
   }
 }
@@ -593,7 +822,7 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
           for (int p = lo; p < rp[i + 1]; ++p) cb(ci[p], p);
         },
         [&](int i) { return dp[i]; });
-    A.smat_built = build_sweeps(A.smat, (int)n, A.cx, hf, hb, st);
+    A.smat_built = build_sweeps(A.smat, (int)n, A.cx, hf, hb, false, st);
   }
   const size_t w = A.cx ? 2 : 1;
   std::vector<double> vals(w * nnz);
@@ -718,6 +947,7 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
     gather_phase(A.lu, A.smat.bwd, A.n, A.cx, m->ctx->stream);
   }
   gather_csweep(A.lu, A.smat.cs, A.cx, m->ctx->stream);
+  gather_rsweep(A.lu, A.smat.rs, A.cx, m->ctx->stream);
   return MPK_OK;
 }
 
@@ -1120,7 +1350,9 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   // reference's total_seconds includes the factorization (solvers.py:426)
   int64_t bad = -1;
   int32_t structural = 0;
+  tl_phase[0] = host_ms();
   int rc = mpk_ilu0_factor(m, &bad, &structural);
+  tl_phase[1] = host_ms();
   if (rc == MPK_SINGULAR_PIVOT || rc == MPK_NUMERIC_BREAKDOWN) {
     rep->iterations = 0;
     rep->converged = 0;
@@ -1163,6 +1395,14 @@ int mpk_solve_dev(mpk_matrix *m, int method, int k, double eps_rel,
                       std::chrono::steady_clock::now() - t0)
                       .count();
   rep->launches = tl_launches - l0;
+  static const bool phases = getenv("MPK_PHASE_TIMES") != nullptr;
+  if (phases)
+    fprintf(stderr,
+            "[mpk] factor %.3f | setup+capture %.3f | loop %.3f | finish %.3f | "
+            "tail %.3f ms\n",
+            tl_phase[1] - tl_phase[0], tl_phase[2] - tl_phase[1],
+            tl_phase[3] - tl_phase[2], tl_phase[4] - tl_phase[3],
+            host_ms() - tl_phase[4]);
   return rc;
 }
 

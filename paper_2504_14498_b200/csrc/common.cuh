@@ -10,6 +10,8 @@
 //     double2[n] (re, im interleaved, one 16-byte load per element).
 #pragma once
 
+#include <chrono>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -29,6 +31,13 @@ inline thread_local long long tl_launches = 0;
 // accumulating, and a chain kernel folds them in the reference's ascending
 // order.  nullptr: fixed-shape tree reductions.
 inline thread_local double *tl_seq = nullptr;
+// host-side phase marks of the current solve (MPK_PHASE_TIMES diagnostics)
+inline thread_local double tl_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+inline double host_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
 
 // Sentinel for sync-free triangular sweeps: a signalling NaN payload that no
 // binary64 operation produces (hardware NaNs are quiet).

@@ -1,6 +1,7 @@
 // ilu.cu -- sync-free binary64 ILU(0) factorization and sweeps (see ilu.cuh)
 #include <climits>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "ilu.cuh"
@@ -765,34 +766,35 @@ constexpr int kCsBatch = 16;  // entries whose loads are issued together
 template <bool CX, bool ADJ>
 __global__ void __launch_bounds__(1024, 1)
     csweep_kernel(SweepArgs a, CSweep p) {
-  using Ent = typename std::conditional<CX, CEntC, CEntR>::type;
   constexpr int ESZ = CX ? 16 : 8;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int tid = threadIdx.x, T = blockDim.x;
   const uint32_t rank = cl_rank();
-  const int C = p.C, nl = p.nl, nf = p.nf;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smraw);  // 3 mbarriers
-  int *flag = reinterpret_cast<int *>(smraw + 32);
-  int4 *seg = reinterpret_cast<int4 *>(smraw + 48);     // nl own segments
-  unsigned char *q = smraw + 48 + (size_t)nl * 16;
+  const int C = p.C, nl = p.nl, nf = p.nf, NB = p.nbuf;
+  const bool repl = p.repl != 0;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smraw);  // NB <= 8 mbarriers
+  int *flag = reinterpret_cast<int *>(smraw + 64);
+  int4 *seg = reinterpret_cast<int4 *>(smraw + 80);     // nl own segments
+  unsigned char *q = smraw + 80 + (size_t)nl * 16;
   double *vec = reinterpret_cast<double *>(q);
   q += ((size_t)p.maxslots * ESZ + 15) / 16 * 16;
-  CDesc *dbuf = reinterpret_cast<CDesc *>(q);
-  Ent *ebuf = reinterpret_cast<Ent *>(dbuf + 3 * p.maxdesc);
+  unsigned char *stage = q;  // NB x maxseg
   const uint32_t vbase = smem_u32(vec);
 
   if (tid == 0) {
-    for (int b = 0; b < 3; ++b) mbar_init(&bar[b], 1);
+    for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
     flag[0] = (a.done && *a.done) ? 1 : 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   for (int g = tid; g < nl; g += T) seg[g] = p.seg[(size_t)g * C + rank];
-  // forward right-hand side (demoted input) preloaded into the own slots
-  const int s0 = p.slot_off[rank], s1 = p.slot_off[rank + 1];
+  // forward right-hand side (demoted input) preloaded into the slots: all
+  // rows (replicated) or the own slots (distributed)
+  const int s0 = repl ? 0 : p.slot_off[rank];
+  const int s1 = repl ? a.n : p.slot_off[rank + 1];
   for (int s = s0 + tid; s < s1; s += T) {
     double r, m;
-    load_in<CX>(a, p.slot_row[s], r, m);
+    load_in<CX>(a, repl ? s : p.slot_row[s], r, m);
     vec[(s - s0) * (CX ? 2 : 1)] = r;
     if constexpr (CX) vec[(s - s0) * 2 + 1] = m;
   }
@@ -807,59 +809,242 @@ __global__ void __launch_bounds__(1024, 1)
     cl_wait();
     return;
   }
-  const CDesc *gdesc = p.desc;
-  const Ent *gent = reinterpret_cast<const Ent *>(p.ent);
   auto issue = [&](int g) {
-    const int b = g % 3;
+    const int b = g % NB;
     const int4 sg = seg[g];
-    const uint32_t bytes = (uint32_t)sg.y * sizeof(CDesc) + (uint32_t)sg.w * sizeof(Ent);
-    if (bytes == 0) {
+    if (sg.y == 0) {
       mbar_arrive(&bar[b]);
       return;
     }
-    mbar_arrive_tx(&bar[b], bytes);
-    if (sg.y) bulk_g2s(dbuf + b * p.maxdesc, gdesc + sg.x, sg.y * sizeof(CDesc), &bar[b]);
-    if (sg.w) bulk_g2s(ebuf + b * p.maxent, gent + sg.z, sg.w * sizeof(Ent), &bar[b]);
+    mbar_arrive_tx(&bar[b], (uint32_t)sg.y);
+    bulk_g2s(stage + (size_t)b * p.maxseg, p.stream + ((size_t)sg.x << 4),
+             (uint32_t)sg.y, &bar[b]);
   };
-  if (tid == 0) {
-    issue(0);
-    if (nl > 1) issue(1);
-  }
+  if (tid == 0)
+    for (int g = 0; g < NB - 1 && g < nl; ++g) issue(g);
+  // distributed: DSMEM address of a packed slot reference
   auto addr = [&](int pk) -> uint32_t {
     return cl_map(vbase + (uint32_t)(pk & 0xFFFFFF) * ESZ, (uint32_t)pk >> 24);
   };
+  auto ldv = [&](int ref, double &r, double &m) {
+    if (repl) {
+      r = vec[ref * (CX ? 2 : 1)];
+      m = CX ? vec[ref * 2 + 1] : 0.0;
+    } else if constexpr (CX) {
+      cl_ld2(addr(ref), r, m);
+    } else {
+      r = cl_ld1(addr(ref));
+      m = 0.0;
+    }
+  };
   for (int g = 0; g < nl; ++g) {
-    const int b = g % 3;
-    mbar_wait(&bar[b], (uint32_t)((g / 3) & 1));
-    const int nd = seg[g].y;
-    const CDesc *D = dbuf + b * p.maxdesc;
-    const Ent *E = ebuf + b * p.maxent;
-    for (int r = tid; r < nd; r += T) {
-      const CDesc d = D[r];
-      double ar, ai = 0.0;
-      if constexpr (CX)
-        cl_ld2(addr(d.init), ar, ai);
-      else
-        ar = cl_ld1(addr(d.init));
+    const int b = g % NB;
+    mbar_wait(&bar[b], (uint32_t)((g / NB) & 1));
+    const int4 sg = seg[g];
+    const unsigned char *base = stage + (size_t)b * p.maxseg;
+    const CSDesc *D = reinterpret_cast<const CSDesc *>(base);
+    const int *refs = reinterpret_cast<const int *>(base + 16 * (size_t)sg.z);
+    const double *vals = reinterpret_cast<const double *>(
+        base + 16 * (size_t)sg.z + (((size_t)sg.w * 4 + 15) / 16) * 16);
+    for (int r = tid; r < sg.z; r += T) {
+      const CSDesc d = D[r];
+      double ar, ai;
+      ldv(d.row, ar, ai);
       for (int e = 0; e < d.cnt; e += kCsBatch) {
         double lr[kCsBatch], li[kCsBatch], vr[kCsBatch], vi[kCsBatch];
 #pragma unroll
         for (int t = 0; t < kCsBatch; ++t) {
           vr[t] = vi[t] = lr[t] = li[t] = 0.0;
           if (e + t < d.cnt) {
-            const Ent &x = E[d.e0 + e + t];
-            if constexpr (CX) {
-              lr[t] = x.vr;
-              li[t] = x.vi;
-              cl_ld2(addr(x.pk), vr[t], vi[t]);
-            } else {
-              lr[t] = x.v;
-              vr[t] = cl_ld1(addr(x.pk));
-            }
+            const int x = d.e0 + e + t;
+            lr[t] = vals[x * (CX ? 2 : 1)];
+            if constexpr (CX) li[t] = vals[2 * x + 1];
+            ldv(refs[x], vr[t], vi[t]);
           }
         }
 #pragma unroll
         for (int t = 0; t < kCsBatch; ++t)
+          if (e + t < d.cnt) mulsub<CX, ADJ>(ar, ai, lr[t], li[t], vr[t], vi[t]);
+      }
+      double qr = ar, qi = ai;
+      if (d.hasdiv) {
+        const int x = d.e0 + d.cnt;
+        if constexpr (CX)
+          py_cdiv(ar, ai, vals[2 * x], ADJ ? -vals[2 * x + 1] : vals[2 * x + 1], qr, qi);
+        else
+          qr = ddiv(ar, vals[x]);
+      }
+      if (repl) {
+        // own copy + every peer's copy
+        const uint32_t la = vbase + (uint32_t)d.row * ESZ;
+        if constexpr (CX) {
+          vec[2 * d.row] = qr;
+          vec[2 * d.row + 1] = qi;
+        } else {
+          vec[d.row] = qr;
+        }
+        for (int k = 1; k < C; ++k) {
+          const uint32_t rr = (rank + (uint32_t)k) % (uint32_t)C;
+          if constexpr (CX)
+            cl_st2(cl_map(la, rr), qr, qi);
+          else
+            cl_st1(cl_map(la, rr), qr);
+        }
+      } else if constexpr (CX) {
+        cl_st2(addr(d.row), qr, qi);
+      } else {
+        cl_st1(addr(d.row), qr);
+      }
+    }
+    // no global stores inside the level loop: the release of the cluster
+    // barrier would have to wait for their acknowledgements
+    cl_arrive();
+    // buffer (g+NB-1)%NB was last read at level g-1, which every CTA finished
+    if (tid == 0 && g + NB - 1 < nl) issue(g + NB - 1);
+    cl_wait();
+  }
+  // every slot now holds the backward result z of its row: write out (the
+  // replicated layout splits the rows over the CTAs) and check them
+  bool bad = false;
+  const int w0 = repl ? (int)rank : s0, w1 = repl ? a.n : s1, ws = repl ? C : 1;
+  for (int s = w0 + tid * ws; s < w1; s += T * ws) {
+    const int i = repl ? s : p.slot_row[s];
+    const int v = repl ? s : s - s0;
+    if constexpr (CX) {
+      const double qr = vec[2 * v], qi = vec[2 * v + 1];
+      bad = bad || !isfin(qr) || !isfin(qi);
+      reinterpret_cast<double2 *>(a.z)[i] = make_double2(qr, qi);
+    } else {
+      const double qr = vec[v];
+      bad = bad || !isfin(qr);
+      a.z[i] = qr;
+    }
+  }
+  if (bad) atomicOr(a.err, 1);
+  // peers may still be pushing into this CTA's vector until they pass here
+  cl_arrive();
+  cl_wait();
+}
+
+__global__ void gather_csweep_kernel(const double *lu, CSweep p, int cx) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= p.nval) return;
+  double *st = reinterpret_cast<double *>(p.stream);
+  const int s = p.esrc[t];
+  const long long o = p.eoff[t];
+  if (cx) {
+    const double2 v = reinterpret_cast<const double2 *>(lu)[s];
+    st[o] = v.x;
+    st[o + 1] = v.y;
+  } else {
+    st[o] = lu[s];
+  }
+}
+
+// ---------------------------------------------------------------------
+// ring sweep (ilu.cuh RSweep): vector resident in shared memory, rows and
+// entries streamed by a producer warp through a ring of TMA-filled slots
+// ---------------------------------------------------------------------
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <bool CX, bool ADJ>
+__global__ void __launch_bounds__(1024, 1) rsweep_kernel(SweepArgs a, RSweep p) {
+  constexpr int ESZ = CX ? 16 : 8;
+  constexpr int kRsBatch = CX ? 4 : 8;  // entries whose loads issue together
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int tid = threadIdx.x, T = blockDim.x, NC = T - 32;
+  const int S = p.S, nch = p.nchunks, n = a.n;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  uint64_t *empty = full + S;
+  int *flag = reinterpret_cast<int *>(empty + S);
+  int2 *tab = reinterpret_cast<int2 *>(smraw + ((16 * S + 16 + 15) / 16) * 16);
+  double *vec = reinterpret_cast<double *>(
+      reinterpret_cast<unsigned char *>(tab) + ((8 * (size_t)nch + 15) / 16) * 16);
+  unsigned char *ring =
+      reinterpret_cast<unsigned char *>(vec) + (((size_t)n * ESZ + 15) / 16) * 16;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NC / 32);
+    }
+    flag[0] = (a.done && *a.done) ? 1 : 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  for (int c = tid; c < nch; c += T) {
+    const RChunk m = p.chunks[c];
+    tab[c] = make_int2((int)(m.off >> 4), m.bytes);
+  }
+  // forward right-hand side (demoted input) preloaded into the vector
+  for (int i = tid; i < n; i += T) {
+    double r, m;
+    load_in<CX>(a, i, r, m);
+    if constexpr (CX) {
+      vec[2 * i] = r;
+      vec[2 * i + 1] = m;
+    } else {
+      vec[i] = r;
+    }
+  }
+  __syncthreads();
+  if (flag[0]) return;  // uniform: read once, after the barrier
+  if (tid >= NC) {
+    // producer warp: lane 0 keeps up to S chunks in flight
+    if (tid == NC) {
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % S, k = c / S;
+        if (k > 0) mbar_wait(&empty[s], (uint32_t)((k - 1) & 1));
+        const int2 m = tab[c];
+        mbar_arrive_tx(&full[s], (uint32_t)m.y);
+        bulk_g2s(ring + (size_t)s * p.slot, p.stream + ((size_t)m.x << 4),
+                 (uint32_t)m.y, &full[s]);
+      }
+    }
+    return;
+  }
+  const int lane = tid & 31;
+  for (int c = 0; c < nch; ++c) {
+    const int s = c % S;
+    mbar_wait(&full[s], (uint32_t)((c / S) & 1));
+    const unsigned char *base = ring + (size_t)s * p.slot;
+    const int4 h = *reinterpret_cast<const int4 *>(base);  // nrows nent end fwd
+    const RDesc *D = reinterpret_cast<const RDesc *>(base + 16);
+    const int *cols = reinterpret_cast<const int *>(base + 16 + 32 * (size_t)h.x);
+    const double *vals = reinterpret_cast<const double *>(
+        base + 16 + 32 * (size_t)h.x + (((size_t)h.y * 4 + 15) / 16) * 16);
+    for (int r = tid; r < h.x; r += NC) {
+      const RDesc d = D[r];
+      double ar, ai = 0.0;
+      if constexpr (CX) {
+        ar = vec[2 * d.row];
+        ai = vec[2 * d.row + 1];
+      } else {
+        ar = vec[d.row];
+      }
+      for (int e = 0; e < d.cnt; e += kRsBatch) {
+        double lr[kRsBatch], li[kRsBatch], vr[kRsBatch], vi[kRsBatch];
+#pragma unroll
+        for (int t = 0; t < kRsBatch; ++t) {
+          vr[t] = vi[t] = lr[t] = li[t] = 0.0;
+          if (e + t < d.cnt) {
+            const int q = d.e0 + e + t;
+            const int j = cols[q];
+            if constexpr (CX) {
+              lr[t] = vals[2 * q];
+              li[t] = vals[2 * q + 1];
+              vr[t] = vec[2 * j];
+              vi[t] = vec[2 * j + 1];
+            } else {
+              lr[t] = vals[q];
+              vr[t] = vec[j];
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < kRsBatch; ++t)
           if (e + t < d.cnt) mulsub<CX, ADJ>(ar, ai, lr[t], li[t], vr[t], vi[t]);
       }
       double qr = ar, qi = ai;
@@ -869,29 +1054,26 @@ __global__ void __launch_bounds__(1024, 1)
         else
           qr = ddiv(ar, d.dr);
       }
-      if constexpr (CX)
-        cl_st2(addr(d.out), qr, qi);
-      else
-        cl_st1(addr(d.out), qr);
+      if constexpr (CX) {
+        vec[2 * d.row] = qr;
+        vec[2 * d.row + 1] = qi;
+      } else {
+        vec[d.row] = qr;
+      }
     }
-    // no global stores inside the level loop: the release of the cluster
-    // barrier would have to wait for their acknowledgements
-    cl_arrive();
-    // buffer (g+2)%3 was last read at level g-1, which every CTA finished
-    if (tid == 0 && g + 2 < nl) issue(g + 2);
-    cl_wait();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (h.z) named_bar(1, NC);  // level complete: its values are readable
   }
-  // every slot now holds the backward result z of its row: write out the
-  // own slots (coalesced over slots) and check them (NumericBreakdownError)
+  // z = the vector after the backward phase; non-finite -> breakdown
   bool bad = false;
-  for (int s = s0 + tid; s < s1; s += T) {
-    const int i = p.slot_row[s];
+  for (int i = tid; i < n; i += NC) {
     if constexpr (CX) {
-      const double qr = vec[(s - s0) * 2], qi = vec[(s - s0) * 2 + 1];
+      const double qr = vec[2 * i], qi = vec[2 * i + 1];
       bad = bad || !isfin(qr) || !isfin(qi);
       reinterpret_cast<double2 *>(a.z)[i] = make_double2(qr, qi);
     } else {
-      const double qr = vec[s - s0];
+      const double qr = vec[i];
       bad = bad || !isfin(qr);
       a.z[i] = qr;
     }
@@ -899,30 +1081,30 @@ __global__ void __launch_bounds__(1024, 1)
   if (bad) atomicOr(a.err, 1);
 }
 
-__global__ void gather_csweep_kernel(const double *lu, CSweep p, int cx) {
+__global__ void gather_rsweep_kernel(const double *lu, RSweep p, int cx) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double *st = reinterpret_cast<double *>(p.stream);
   if (t < p.nent) {
     const int s = p.esrc[t];
+    const long long o = p.eoff[t];
     if (cx) {
-      CEntC &e = reinterpret_cast<CEntC *>(p.ent)[t];
       const double2 v = reinterpret_cast<const double2 *>(lu)[s];
-      e.vr = v.x;
-      e.vi = v.y;
+      st[o] = v.x;
+      st[o + 1] = v.y;
     } else {
-      reinterpret_cast<CEntR *>(p.ent)[t].v = lu[s];
+      st[o] = lu[s];
     }
   }
   if (t < p.ndesc) {
     const int s = p.dsrc[t];
-    CDesc &d = p.desc[t];
     if (s >= 0) {
+      const long long o = p.doff[t];
       if (cx) {
         const double2 v = reinterpret_cast<const double2 *>(lu)[s];
-        d.dr = v.x;
-        d.di = v.y;
+        st[o] = v.x;
+        st[o + 1] = v.y;
       } else {
-        d.dr = lu[s];
-        d.di = 0.0;
+        st[o] = lu[s];
       }
     }
   }
@@ -1052,10 +1234,41 @@ void launch_csweep(const SweepArgs &a, const CSweep &p, bool cx, bool adjoint,
 
 void gather_csweep(const double *lu, const CSweep &p, bool cx,
                    cudaStream_t st) {
-  const long long m = p.nent > p.ndesc ? p.nent : p.ndesc;
+  const long long m = p.nval;
   if (p.C == 0 || m <= 0) return;
   ++tl_launches;
   gather_csweep_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(lu, p,
+                                                                    cx ? 1 : 0);
+}
+
+template <bool CX, bool ADJ>
+static void launch_rsweep_t(const SweepArgs &a, const RSweep &p,
+                            cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rsweep_kernel<CX, ADJ>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemMax);
+    attr = true;
+  }
+  rsweep_kernel<CX, ADJ><<<1, p.T, p.smem, st>>>(a, p);
+}
+
+void launch_rsweep(const SweepArgs &a, const RSweep &p, bool cx, bool adjoint,
+                   cudaStream_t st) {
+  ++tl_launches;
+  if (!cx && !adjoint) launch_rsweep_t<false, false>(a, p, st);
+  if (!cx && adjoint) launch_rsweep_t<false, true>(a, p, st);
+  if (cx && !adjoint) launch_rsweep_t<true, false>(a, p, st);
+  if (cx && adjoint) launch_rsweep_t<true, true>(a, p, st);
+}
+
+void gather_rsweep(const double *lu, const RSweep &p, bool cx,
+                   cudaStream_t st) {
+  const long long m = p.nent > p.ndesc ? p.nent : p.ndesc;
+  if (p.nchunks == 0 || m <= 0) return;
+  ++tl_launches;
+  gather_rsweep_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(lu, p,
                                                                     cx ? 1 : 0);
 }
 

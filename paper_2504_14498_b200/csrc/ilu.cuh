@@ -61,52 +61,87 @@ struct SweepPhase {
 };
 
 // Cluster sweep plan: both phases of one apply split over the C CTAs of a
-// thread-block cluster (one SM each).  Row i's value lives in the shared
-// memory of the CTA that computes it in the forward phase ("owner", slot s);
-// every reference to it is a packed address pk = owner << 24 | s read with
-// ld.shared::cluster (DSMEM).  Per (level, CTA) the row descriptors and
-// entries are contiguous ("segments"), staged into shared memory by bulk
-// async copies two levels ahead; levels are separated by a cluster barrier.
-struct __align__(16) CDesc {
-  int init;   // pk of the initial value (forward: rhs in own slot; backward: y_i)
-  int out;    // pk the result is stored to (row's owner slot)
-  int e0;     // first entry, relative to the segment
-  int cnt;    // entries
-  int row;    // global row (z output, rhs)
-  int hasdiv; // divide by d at the end
-  int pad0, pad1;
-  double dr, di;  // divisor (gathered from the factors)
-};
-struct __align__(16) CEntR {
-  double v;
-  int pk;
-  int pad;
-};
-struct __align__(16) CEntC {
-  double vr, vi;
-  int pk;
-  int pad[3];
+// thread-block cluster (one SM each); levels are separated by a cluster
+// barrier.  Two layouts of the vector:
+//  * replicated (repl = 1, when it fits): every CTA holds the whole vector
+//    in its shared memory; values are read locally and every result is
+//    written to the own copy and pushed to each peer (st.shared::cluster);
+//  * distributed (repl = 0): row i lives in the shared memory of the CTA
+//    that computes it in the forward phase ("owner", slot s) and is read
+//    with ld.shared::cluster through the packed address pk = owner<<24 | s.
+// Per (level, CTA) the work is one "segment" of a byte stream, staged into
+// shared memory by one bulk async copy (TMA) nbuf-1 levels ahead:
+//   CSDesc[nd] | int32 ref[ne] (16-B padded) | value[ne] (f64 or double2)
+// with ne = sum(cnt + hasdiv): a row's divisor is the value after its
+// entries.  ref / CSDesc.row are row indices (repl) or pks (distributed).
+struct __align__(16) CSDesc {
+  int row;     // repl: row index; distributed: pk of the row's slot
+  int e0;      // first entry, relative to the segment
+  int cnt;     // entries (the divisor, if any, follows them)
+  int hasdiv;
 };
 struct CSweep {
   int C = 0, T = 0;   // cluster size, threads per CTA (0: no plan)
   int nl = 0, nf = 0; // levels (forward + backward), forward levels
-  int4 *seg = nullptr;        // [nl][C] {desc_off, ndesc, ent_off, nent}
-  CDesc *desc = nullptr;
-  int *dsrc = nullptr;        // per descriptor: lu index of divisor or -1
-  void *ent = nullptr;        // CEntR / CEntC
-  int *esrc = nullptr;        // per entry: lu index
-  int *slot_row = nullptr;    // [C][..] global row held in each slot
+  int repl = 0;       // replicated vector (see above)
+  int nbuf = 3;       // staging buffers (levels in flight + 1)
+  int4 *seg = nullptr;        // [nl][C] {byte offset / 16, bytes, nd, ne}
+  unsigned char *stream = nullptr;
+  long long *eoff = nullptr;  // per value slot: double index in the stream
+  int *esrc = nullptr;        // per value slot: lu index
+  long long nval = 0;
+  int *slot_row = nullptr;    // distributed: [C][..] global row of each slot
   int *slot_off = nullptr;    // C+1 offsets into slot_row
-  long long ndesc = 0, nent = 0;
-  int maxslots = 0, maxdesc = 0, maxent = 0;
+  int maxslots = 0;           // vector slots per CTA
+  int maxseg = 0;             // largest segment (bytes)
   size_t smem = 0;            // dynamic shared memory per CTA
+};
+
+// Ring sweep plan: one CTA holds the whole vector in shared memory; both
+// phases' rows (level order) and entries are laid out as a byte stream of
+// "chunks" (a chunk = consecutive rows of one level: RDesc[nrows] | col
+// int32[nent] | val f64-or-double2[nent], 16-byte aligned) that a producer
+// warp streams through a ring of shared-memory slots with bulk async copies
+// (TMA), while the consumer warps process the previous chunks.  Levels are
+// separated by a named barrier of the consumer warps only.
+struct __align__(16) RDesc {
+  int row;     // global row
+  int e0;      // first entry, relative to the chunk
+  int cnt;     // entries
+  int hasdiv;  // divide by d at the end
+  double dr, di;
+};
+struct RChunk {  // device + host metadata of one chunk
+  long long off; // byte offset in the stream
+  int bytes;     // multiple of 16
+  int nrows, nent;
+  int level_end; // last chunk of its level: barrier after it
+  int fwd;       // forward phase
+  int pad;
+};
+struct RSweep {
+  int nchunks = 0, S = 0, slot = 0;  // chunks, ring slots, slot bytes
+  int T = 0;                         // threads (consumers + 1 producer warp)
+  unsigned char *stream = nullptr;   // device byte stream
+  RChunk *chunks = nullptr;          // device chunk table
+  long long *eoff = nullptr;         // per entry: double index of its value
+  int *esrc = nullptr;               // per entry: lu index
+  long long nent = 0;
+  long long *doff = nullptr;         // per row desc: double index of dr
+  int *dsrc = nullptr;               // per row desc: lu index (-1: none)
+  long long ndesc = 0;
+  size_t smem = 0;
 };
 
 struct SweepMats {
   SweepPhase fwd, bwd;
   bool conj = false;  // adjoint: values are conjugated at use
   CSweep cs;          // cluster plan (cs.C > 0 when built)
+  RSweep rs;          // ring plan (rs.nchunks > 0 when built)
 };
+void launch_rsweep(const SweepArgs &a, const RSweep &p, bool cx, bool adjoint,
+                   cudaStream_t st);
+void gather_rsweep(const double *lu, const RSweep &p, bool cx, cudaStream_t st);
 // cluster sweep over a plan (values gathered); cfg: env MPK_CSWEEP_C
 void launch_csweep(const SweepArgs &a, const CSweep &p, bool cx, bool adjoint,
                    cudaStream_t st);

@@ -78,14 +78,18 @@ struct DMat {
   std::vector<int> h_rp, h_ci, h_dp;
 };
 
-// ILU(0)-mixed apply dispatch: cluster sweep when its plan exists, else the
-// prefetched single-CTA sweep over the level-ordered sweep matrices (small
-// n), else the sync-free multi-CTA kernel.
+// ILU(0)-mixed apply dispatch: the ring sweep (one SM, vector in shared
+// memory) or the cluster sweep when its plan exists, else the prefetched
+// single-CTA sweep over the level-ordered sweep matrices, else the sync-free
+// multi-CTA kernel.
 inline void do_sweep(const DMat &A, const SweepArgs &a, bool adjoint,
                      cudaStream_t st) {
   const bool mats = adjoint ? A.smat_adj_built : A.smat_built;
   const CSweep &cs = adjoint ? A.smat_adj.cs : A.smat.cs;
-  if (cs.C > 0)
+  const RSweep &rs = adjoint ? A.smat_adj.rs : A.smat.rs;
+  if (rs.nchunks > 0)
+    launch_rsweep(a, rs, A.cx, adjoint, st);
+  else if (cs.C > 0)
     launch_csweep(a, cs, A.cx, adjoint, st);
   else if (mats)
     launch_sweep_mats(a, adjoint ? A.smat_adj : A.smat, A.cx, adjoint, st);

@@ -1235,6 +1235,7 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
     }
     CK(cudaGraphInstantiate(&sv->ge, sv->g, 0));
   }
+  tl_phase[2] = host_ms();  // setup enqueued, graph ready
   if (use_cond) {
     CK(cudaGraphLaunch(sv->ge, st));
     tl_launches += 1;  // the init node; body nodes counted per run below
@@ -1258,6 +1259,7 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   CK(cudaMemcpyAsync(sv->hp, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   hs = *sv->hp;
+  tl_phase[3] = host_ms();  // loop done (synchronised)
   if (use_cond) tl_launches += sv->body_nodes * hs.body_runs;
   if (!hs.done) {
     // loop ran out without a device-side stop (max_iter reached)
@@ -1295,6 +1297,7 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   CK(cudaMemcpyAsync(sv->hp, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   hs = *sv->hp;
+  tl_phase[4] = host_ms();  // finish + true residual done
   if (chk_after) e_after = *sv->hpi;
   CK(cudaGetLastError());
   if (e_after) return sweep_fail();

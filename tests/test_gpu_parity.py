@@ -336,20 +336,24 @@ def test_device_edge_cases(pkg):
 
 
 SWEEP_PATHS = {
-    "global": {"MPK_CSWEEP": "0", "MPK_SWEEP_SMEM": "0"},
-    "single": {"MPK_CSWEEP": "0"},
-    "cluster1": {"MPK_CSWEEP_C": "1"},
-    "cluster2": {"MPK_CSWEEP_C": "2", "MPK_CSWEEP_ROWS": "1"},
-    "cluster8": {"MPK_CSWEEP_C": "8", "MPK_CSWEEP_ROWS": "1"},
-    "cluster16": {"MPK_CSWEEP_C": "16", "MPK_CSWEEP_ROWS": "1"},
+    "global": {"MPK_RSWEEP": "0", "MPK_CSWEEP": "0", "MPK_SWEEP_SMEM": "0"},
+    "single": {"MPK_RSWEEP": "0", "MPK_CSWEEP": "0"},
+    "ring": {"MPK_RSWEEP": "1", "MPK_SWEEP_PICK": "ring"},
+    "auto": {},
+    "cluster1": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "1"},
+    "cluster2": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "2", "MPK_CSWEEP_ROWS": "1"},
+    "cluster8": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "8", "MPK_CSWEEP_ROWS": "1"},
+    "cluster16": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "16", "MPK_CSWEEP_ROWS": "1"},
+    "cluster8d": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "8", "MPK_CSWEEP_REPL": "0",
+                  "MPK_CSWEEP_ROWS": "1"},
 }
 
 
 @pytest.mark.parametrize("path", list(SWEEP_PATHS))
 @pytest.mark.parametrize("mat", ["cfg1", "cfg2", "helm_c"])
 def test_device_sweep_paths_bitwise(pkg, monkeypatch, path, mat):
-    """Every sweep implementation (sync-free global, single-CTA, cluster of
-    1/2/8/16 CTAs) gives the oracle's binary64 ILU(0) apply bit for bit,
+    """Every sweep implementation (sync-free global, single-CTA, ring, cluster
+    of 1/2/8/16 CTAs) gives the oracle's binary64 ILU(0) apply bit for bit,
     plain and adjoint (ilu.py:410-470)."""
     import oracle.oracle as orc
     from paper_2504_14498_b200 import problems
