@@ -534,6 +534,13 @@ def main():
     achieved = bytes_apply / (apply_ms * 1e-3) / 1e9
     value = res["iters"] / (res["ms"] * 1e-3)
     e2e = res["e2e_iters"] / (res["e2e_ms"] * 1e-3)
+    # DRAM traffic of the same kernel from the committed ncu capture
+    traffic, tk = None, "ilu0_apply (forward + backward sweep kernel; plan autotuned)"
+    tf = ROOT / "profiles" / "r01_traffic.json"
+    if tf.exists():
+        t = json.loads(tf.read_text()).get(args.config)
+        if t:
+            traffic, tk = t["dram_bytes_per_launch"], t["kernel"]
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps,
@@ -544,9 +551,9 @@ def main():
                 "d2h_bytes_per_step": int(res["d2h"])},
         "gpu_launches": int(res["launches"]),
         "clocks": res["clocks"],
-        "roofline": {"bound": "hbm", "kernel": "ilu0_apply (sweep_kernel, fwd+bwd)",
+        "roofline": {"bound": "hbm", "kernel": tk,
                      "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None,
+                     "frac": achieved / hbm, "traffic": traffic,
                      "algorithmic_bytes": bytes_apply, "avg_ms": apply_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if PEAKS.exists()
                      else "fallback B200_PROFILING.md"},
