@@ -206,8 +206,9 @@ static int env_int(const char *name, int dflt) {
 // C from 2 up, or MPK_CSWEEP_C), else the distributed layout.  Returns false
 // if no layout fits in shared memory.
 static bool build_cplan_c(CSweep &p, int n, bool cx, const HPhase &f,
-                          const HPhase &b, int C, bool repl, bool commit,
-                          cudaStream_t st) {
+                          const HPhase &b, int C, bool repl, bool dflow,
+                          bool commit, cudaStream_t st) {
+  if (dflow && !repl) return false;
   const int nl = f.nlev + b.nlev;
   if (nl > 8192) return false;
   const size_t esz = cx ? 16 : 8;
@@ -227,13 +228,22 @@ static bool build_cplan_c(CSweep &p, int n, bool cx, const HPhase &f,
   std::vector<int> cf, cb;
   split(f, cf);
   split(b, cb);
-  std::vector<int> pk(n), nslot(C, 0);
-  std::vector<std::vector<int>> srow(C);
+  std::vector<int> pk(n), nslot(C, 0), kf(n), kb(n);
+  std::vector<std::vector<int>> srow(C), brow(C);
   for (int r = 0; r < n; ++r) {  // level order -> slots in compute order
     const int i = f.desc[r].x, c = cf[r];
+    kf[i] = (int)srow[c].size();
     pk[i] = repl ? i : ((c << 24) | nslot[c]++);
-    if (!repl) srow[c].push_back(i);
+    srow[c].push_back(i);
   }
+  for (int r = 0; r < n; ++r) {
+    const int i = b.desc[r].x, c = cb[r];
+    kb[i] = (int)brow[c].size();
+    brow[c].push_back(i);
+  }
+  int ninit = 0;
+  for (int c = 0; c < C; ++c)
+    ninit = std::max(ninit, (int)std::max(srow[c].size(), brow[c].size()));
   auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
   // sizes first (cheap), then the stream only when committing
   std::vector<int4> seg((size_t)nl * C);
@@ -262,6 +272,9 @@ static bool build_cplan_c(CSweep &p, int n, bool cx, const HPhase &f,
   if (repl) maxslots = n;
   if ((total >> 4) > (size_t)INT_MAX) return false;
   auto smem_for = [&](int nb) {
+    if (dflow)
+      return 144 + (size_t)nl * 16 + a16((size_t)n * esz) + a16((size_t)ninit * esz) +
+             nb * maxseg;
     return 80 + (size_t)nl * 16 + a16((size_t)maxslots * esz) + nb * maxseg;
   };
   int nb = std::min(8, std::max(3, env_int("MPK_CSWEEP_NBUF", 4)));
@@ -289,7 +302,8 @@ static bool build_cplan_c(CSweep &p, int n, bool cx, const HPhase &f,
       for (int r : rows_of[c]) {
         const int4 hd = h.desc[r];
         const bool dv = h.dsrc[r] >= 0;
-        CSDesc d{pk[hd.x], e, hd.z, dv ? 1 : 0};
+        const int kk = fw ? kf[hd.x] : kb[hd.x];
+        CSDesc d{pk[hd.x], e, hd.z, (kk << 1) | (dv ? 1 : 0)};
         std::memcpy(q + 16 * (size_t)k++, &d, sizeof d);
         const double one = 1.0;  // placeholder until the first gather
         for (int t = hd.y; t < hd.y + hd.z; ++t, ++e) {
@@ -310,19 +324,26 @@ static bool build_cplan_c(CSweep &p, int n, bool cx, const HPhase &f,
   }
   p.C = C;
   p.T = std::min(1024, std::max(64, (maxnd + 31) / 32 * 32));
+  if (dflow) p.T = std::min(1024, p.T + 32);  // + the producer warp
   p.nl = nl;
   p.nf = f.nlev;
   p.repl = repl ? 1 : 0;
+  p.dflow = dflow ? 1 : 0;
+  p.ninit = ninit;
   p.nbuf = nb;
   p.nval = (long long)esrc.size();
   p.maxslots = maxslots;
   p.maxseg = (int)maxseg;
   p.smem = smem_for(nb);
-  std::vector<int> slot_row, slot_off(C + 1, 0);
+  std::vector<int> slot_row, slot_off(C + 1, 0), brows, boff(C + 1, 0);
   for (int c = 0; c < C; ++c) {
     slot_off[c + 1] = slot_off[c] + (int)srow[c].size();
     slot_row.insert(slot_row.end(), srow[c].begin(), srow[c].end());
+    boff[c + 1] = boff[c] + (int)brow[c].size();
+    brows.insert(brows.end(), brow[c].begin(), brow[c].end());
   }
+  upload(&p.brow, brows, st);
+  upload(&p.boff, boff, st);
   upload(&p.seg, seg, st);
   upload(&p.stream, stream, st);
   upload(&p.eoff, eoff, st);
@@ -338,22 +359,25 @@ static bool build_cplan(CSweep &p, int n, bool cx, const HPhase &f,
   if (n == 0) return false;
   const int cenv = env_int("MPK_CSWEEP_C", 0);
   const int renv = env_int("MPK_CSWEEP_REPL", -1);
+  const int denv = env_int("MPK_CSWEEP_DFLOW", 1);
   const int cs[] = {2, 4, 8, 16};
   if (renv != 0) {  // replicated: smallest C that fits (or the forced one)
-    for (int C : cs) {
-      if (cenv && C != cenv) continue;
-      if (build_cplan_c(p, n, cx, f, b, C, true, false, st))
-        return build_cplan_c(p, n, cx, f, b, C, true, true, st);
+    for (int dflow = denv ? 1 : 0; dflow >= 0; --dflow) {
+      for (int C : cs) {
+        if (cenv && C != cenv) continue;
+        if (build_cplan_c(p, n, cx, f, b, C, true, dflow, false, st))
+          return build_cplan_c(p, n, cx, f, b, C, true, dflow, true, st);
+      }
     }
-    if (cenv == 1 && build_cplan_c(p, n, cx, f, b, 1, true, false, st))
-      return build_cplan_c(p, n, cx, f, b, 1, true, true, st);
+    if (cenv == 1 && build_cplan_c(p, n, cx, f, b, 1, true, false, false, st))
+      return build_cplan_c(p, n, cx, f, b, 1, true, false, true, st);
   }
   if (renv == 1) return false;
   const int maxw = std::max(f.maxw, b.maxw);
-  int C = cenv ? cenv : std::min(8, std::max(1, maxw / env_int("MPK_CSWEEP_ROWS", 24)));
+  int C = cenv ? cenv : std::min(16, std::max(1, maxw / env_int("MPK_CSWEEP_ROWS", 24)));
   if (C > 16) C = 16;
-  if (build_cplan_c(p, n, cx, f, b, C, false, false, st))
-    return build_cplan_c(p, n, cx, f, b, C, false, true, st);
+  if (build_cplan_c(p, n, cx, f, b, C, false, false, false, st))
+    return build_cplan_c(p, n, cx, f, b, C, false, false, true, st);
   return false;
 }
 
@@ -480,7 +504,7 @@ static void free_rplan(RSweep &p) {
 }
 
 static void free_cplan(CSweep &p) {
-  void *q[] = {p.seg, p.stream, p.eoff, p.esrc, p.slot_row, p.slot_off};
+  void *q[] = {p.seg, p.stream, p.eoff, p.esrc, p.slot_row, p.slot_off, p.brow, p.boff};
   for (void *v : q)
     if (v) cudaFree(v);
   p = CSweep{};
@@ -549,20 +573,45 @@ static bool build_sweeps(SweepMats &sm, int n, bool cx, const HPhase &f,
     single = true;
   }
   if (env_int("MPK_RSWEEP", 1)) build_rplan(sm.rs, n, cx, f, b, st);
-  if (env_int("MPK_CSWEEP", 1)) build_cplan(sm.cs, n, cx, f, b, st);
-  if (sm.rs.nchunks > 0 && sm.cs.C > 0) {
-    const char *pick = getenv("MPK_SWEEP_PICK");
-    int keep;
-    if (pick && !strcmp(pick, "ring"))
-      keep = 0;
-    else if (pick && !strcmp(pick, "cluster"))
-      keep = 1;
-    else
-      keep = time_plan(sm, n, cx, adjoint, 0, st) <= time_plan(sm, n, cx, adjoint, 1, st) ? 0 : 1;
-    if (keep == 0)
-      free_cplan(sm.cs);
-    else
-      free_rplan(sm.rs);
+  CSweep alt;  // the barrier-per-level variant when the dataflow plan exists
+  if (env_int("MPK_CSWEEP", 1)) {
+    build_cplan(sm.cs, n, cx, f, b, st);
+    if (sm.cs.dflow && env_int("MPK_CSWEEP_C", 0) == 0) {
+      const char *old = getenv("MPK_CSWEEP_DFLOW");
+      const std::string keep_old = old ? old : "";
+      setenv("MPK_CSWEEP_DFLOW", "0", 1);
+      build_cplan(alt, n, cx, f, b, st);
+      if (old)
+        setenv("MPK_CSWEEP_DFLOW", keep_old.c_str(), 1);
+      else
+        unsetenv("MPK_CSWEEP_DFLOW");
+    }
+  }
+  const char *pick = getenv("MPK_SWEEP_PICK");
+  // candidates: 0 ring, 1 cluster plan, 2 alternative cluster plan
+  float t[3] = {1e30f, 1e30f, 1e30f};
+  if (pick && !strcmp(pick, "ring")) {
+    t[0] = 0.f;
+  } else if (pick && !strcmp(pick, "cluster")) {
+    t[1] = 0.f;
+  } else {
+    if (sm.rs.nchunks > 0) t[0] = time_plan(sm, n, cx, adjoint, 0, st);
+    if (sm.cs.C > 0) t[1] = time_plan(sm, n, cx, adjoint, 1, st);
+    if (alt.C > 0) {
+      std::swap(sm.cs, alt);
+      t[2] = time_plan(sm, n, cx, adjoint, 1, st);
+      std::swap(sm.cs, alt);
+    }
+  }
+  int best = 0;
+  for (int i = 1; i < 3; ++i)
+    if (t[i] < t[best]) best = i;
+  if (best == 2) std::swap(sm.cs, alt);
+  free_cplan(alt);
+  if (best == 0 && sm.rs.nchunks > 0) {
+    free_cplan(sm.cs);
+  } else if (sm.cs.C > 0) {
+    free_rplan(sm.rs);
   }
   return single;
 }

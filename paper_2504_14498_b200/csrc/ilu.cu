@@ -702,6 +702,9 @@ __device__ __forceinline__ uint32_t cl_map(uint32_t a, uint32_t rank) {
 __device__ __forceinline__ void cl_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void cl_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -837,9 +840,19 @@ __global__ void __launch_bounds__(1024, 1)
       m = 0.0;
     }
   };
+#ifdef MPK_CSWEEP_PROF
+  // per-level phase times of CTA 0 (diagnostic build only)
+  long long *prof_sm = reinterpret_cast<long long *>(smraw + 72);
+  if (tid == 0) prof_sm[0] = 0;
+  long long pa[4] = {0, 0, 0, 0}, plast = clock64();
+  __syncthreads();
+#endif
   for (int g = 0; g < nl; ++g) {
     const int b = g % NB;
     mbar_wait(&bar[b], (uint32_t)((g / NB) & 1));
+#ifdef MPK_CSWEEP_PROF
+    const long long tq0 = clock64();
+#endif
     const int4 sg = seg[g];
     const unsigned char *base = stage + (size_t)b * p.maxseg;
     const CSDesc *D = reinterpret_cast<const CSDesc *>(base);
@@ -867,7 +880,7 @@ __global__ void __launch_bounds__(1024, 1)
           if (e + t < d.cnt) mulsub<CX, ADJ>(ar, ai, lr[t], li[t], vr[t], vi[t]);
       }
       double qr = ar, qi = ai;
-      if (d.hasdiv) {
+      if (d.hasdiv & 1) {
         const int x = d.e0 + d.cnt;
         if constexpr (CX)
           py_cdiv(ar, ai, vals[2 * x], ADJ ? -vals[2 * x + 1] : vals[2 * x + 1], qr, qi);
@@ -898,11 +911,35 @@ __global__ void __launch_bounds__(1024, 1)
     }
     // no global stores inside the level loop: the release of the cluster
     // barrier would have to wait for their acknowledgements
+#ifdef MPK_CSWEEP_PROF
+    const long long tq1 = clock64();
+    atomicMax(reinterpret_cast<unsigned long long *>(prof_sm),
+              (unsigned long long)(tq1 - tq0));
+#endif
     cl_arrive();
+#ifdef MPK_CSWEEP_PROF
+    const long long tq2 = clock64();
+#endif
     // buffer (g+NB-1)%NB was last read at level g-1, which every CTA finished
     if (tid == 0 && g + NB - 1 < nl) issue(g + NB - 1);
     cl_wait();
+#ifdef MPK_CSWEEP_PROF
+    if (tid == 0) {
+      const long long tq3 = clock64();
+      pa[0] += tq0 - plast;  // staging wait
+      pa[1] += prof_sm[0];   // slowest thread's rows
+      pa[2] += tq2 - tq1;    // arrive (release: drains the stores)
+      pa[3] += tq3 - tq2;    // wait for the cluster
+      plast = tq3;
+      prof_sm[0] = 0;
+    }
+#endif
   }
+#ifdef MPK_CSWEEP_PROF
+  if (tid == 0 && rank == 0)
+    printf("csweep prof C=%d repl=%d levels %d: staging %lld rows(max) %lld arrive %lld wait %lld cycles\n",
+           C, p.repl, nl, pa[0], pa[1], pa[2], pa[3]);
+#endif
   // every slot now holds the backward result z of its row: write out (the
   // replicated layout splits the rows over the CTAs) and check them
   bool bad = false;
@@ -926,6 +963,213 @@ __global__ void __launch_bounds__(1024, 1)
   cl_wait();
 }
 
+// ---------------------------------------------------------------------
+// dataflow cluster sweep (CSweep.dflow): replicated vector, no barrier per
+// level.  Every CTA's copy starts as signalling-NaN sentinels; a row polls
+// its dependencies in the LOCAL copy (volatile ld.shared, ~30 cycles) until
+// the producer's push (st.shared::cluster) has replaced the sentinel, so
+// the critical path is producer latency + DSMEM store latency per level.
+// Deadlock-free: all threads of the cluster are resident, every thread
+// processes its rows in level order, and a row only waits on lower levels.
+// Cluster barriers: start (copies initialised), forward -> backward (all
+// forward reads done; y_i of the own backward rows saved, copies reset) and
+// end.  A producer warp streams the level segments through nbuf staging
+// buffers (mbarriers full / empty) so warps of one CTA may be at different
+// levels.
+// ---------------------------------------------------------------------
+__device__ __forceinline__ double lds_volatile(const double *p) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
+  return v;
+}
+
+template <bool CX, bool ADJ>
+__global__ void __launch_bounds__(1024, 1)
+    dsweep_kernel(SweepArgs a, CSweep p) {
+  constexpr int ESZ = CX ? 16 : 8;
+  constexpr int BATCH = CX ? 4 : 8;
+  constexpr int W = CX ? 2 : 1;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int tid = threadIdx.x, T = blockDim.x, NC = T - 32;
+  const uint32_t rank = cl_rank();
+  const int C = p.C, nl = p.nl, nf = p.nf, NB = p.nbuf, n = a.n;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  uint64_t *empty = full + 8;
+  int *flag = reinterpret_cast<int *>(smraw + 128);
+  int4 *seg = reinterpret_cast<int4 *>(smraw + 144);
+  unsigned char *q = smraw + 144 + (size_t)nl * 16;
+  double *vec = reinterpret_cast<double *>(q);
+  q += ((size_t)n * ESZ + 15) / 16 * 16;
+  double *init = reinterpret_cast<double *>(q);
+  q += ((size_t)p.ninit * ESZ + 15) / 16 * 16;
+  unsigned char *stage = q;
+  const uint32_t vbase = smem_u32(vec);
+  const double SENT = sent_val();
+
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], NC / 32);
+    }
+    flag[0] = (a.done && *a.done) ? 1 : 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  for (int g = tid; g < nl; g += T) seg[g] = p.seg[(size_t)g * C + rank];
+  for (int s = tid; s < n * W; s += T) vec[s] = SENT;
+  const int f0 = p.slot_off[rank], f1 = p.slot_off[rank + 1];
+  for (int k = tid; k < f1 - f0; k += T) {
+    double r, m;
+    load_in<CX>(a, p.slot_row[f0 + k], r, m);
+    init[k * W] = r;
+    if constexpr (CX) init[k * 2 + 1] = m;
+  }
+  __syncthreads();
+  cl_arrive();  // #1: every copy is initialised before anyone pushes
+  cl_wait();
+  const bool skip = cl_ldi(cl_map(smem_u32(flag), 0)) != 0;
+  if (skip) {
+    cl_arrive();
+    cl_wait();
+    return;
+  }
+  auto issue = [&](int g) {
+    const int b = g % NB, k = g / NB;
+    if (k > 0) mbar_wait(&empty[b], (uint32_t)((k - 1) & 1));
+    const int4 sg = seg[g];
+    if (sg.y == 0) {
+      mbar_arrive(&full[b]);
+      return;
+    }
+    mbar_arrive_tx(&full[b], (uint32_t)sg.y);
+    bulk_g2s(stage + (size_t)b * p.maxseg, p.stream + ((size_t)sg.x << 4),
+             (uint32_t)sg.y, &full[b]);
+  };
+  if (tid >= NC) {
+    // producer warp: lane 0 streams the segments; the whole warp takes part
+    // in the cluster barriers
+    const int gb = nl < nf + NB - 1 ? nl : nf + NB - 1;
+    if (tid == NC)
+      for (int g = 0; g < gb; ++g) issue(g);
+    __syncwarp();
+    cl_arrive();  // #2 forward done
+    cl_wait();
+    cl_arrive();  // #3 copies reset
+    cl_wait();
+    if (tid == NC)
+      for (int g = gb; g < nl; ++g) issue(g);
+    __syncwarp();
+    cl_arrive();  // #4 end
+    cl_wait();
+    return;
+  }
+  const int lane = tid & 31;
+  for (int g = 0; g < nl; ++g) {
+    if (g == nf) {
+      // forward -> backward: everyone is done reading y; save y of the own
+      // backward rows, reset the copy, and only then let pushes start
+      cl_arrive();  // #2
+      cl_wait();
+      const int b0 = p.boff[rank], b1 = p.boff[rank + 1];
+      for (int k = tid; k < b1 - b0; k += NC) {
+        const int i = p.brow[b0 + k];
+        init[k * W] = vec[i * W];
+        if constexpr (CX) init[k * 2 + 1] = vec[i * 2 + 1];
+      }
+      named_bar(1, NC);
+      for (int s = tid; s < n * W; s += NC) vec[s] = SENT;
+      cl_arrive();  // #3
+      cl_wait();
+    }
+    const int b = g % NB;
+    mbar_wait(&full[b], (uint32_t)((g / NB) & 1));
+    const int4 sg = seg[g];
+    const unsigned char *base = stage + (size_t)b * p.maxseg;
+    const CSDesc *D = reinterpret_cast<const CSDesc *>(base);
+    const int *refs = reinterpret_cast<const int *>(base + 16 * (size_t)sg.z);
+    const double *vals = reinterpret_cast<const double *>(
+        base + 16 * (size_t)sg.z + (((size_t)sg.w * 4 + 15) / 16) * 16);
+    for (int r = tid; r < sg.z; r += NC) {
+      const CSDesc d = D[r];
+      const int k = d.hasdiv >> 1;
+      double ar = init[k * W], ai = CX ? init[k * 2 + 1] : 0.0;
+      for (int e = 0; e < d.cnt; e += BATCH) {
+        double lr[BATCH], li[BATCH], vr[BATCH], vi[BATCH];
+        int jj[BATCH];
+#pragma unroll
+        for (int t = 0; t < BATCH; ++t) {
+          vr[t] = vi[t] = lr[t] = li[t] = 0.0;
+          jj[t] = 0;
+          if (e + t < d.cnt) {
+            const int x = d.e0 + e + t;
+            lr[t] = vals[x * W];
+            if constexpr (CX) li[t] = vals[2 * x + 1];
+            jj[t] = refs[x];
+            vr[t] = lds_volatile(vec + jj[t] * W);
+            if constexpr (CX) vi[t] = lds_volatile(vec + jj[t] * 2 + 1);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < BATCH; ++t) {
+          if (e + t < d.cnt) {
+            while (is_sent(vr[t]) || (CX && is_sent(vi[t]))) {
+              vr[t] = lds_volatile(vec + jj[t] * W);
+              if constexpr (CX) vi[t] = lds_volatile(vec + jj[t] * 2 + 1);
+            }
+            mulsub<CX, ADJ>(ar, ai, lr[t], li[t], vr[t], vi[t]);
+          }
+        }
+      }
+      double qr = ar, qi = ai;
+      if (d.hasdiv & 1) {
+        const int x = d.e0 + d.cnt;
+        if constexpr (CX)
+          py_cdiv(ar, ai, vals[2 * x], ADJ ? -vals[2 * x + 1] : vals[2 * x + 1], qr, qi);
+        else
+          qr = ddiv(ar, vals[x]);
+      }
+      // push to every peer first, then the own copy
+      const uint32_t la = vbase + (uint32_t)d.row * ESZ;
+      for (int kk = 1; kk < C; ++kk) {
+        const uint32_t rr = (rank + (uint32_t)kk) % (uint32_t)C;
+        if constexpr (CX)
+          cl_st2(cl_map(la, rr), qr, qi);
+        else
+          cl_st1(cl_map(la, rr), qr);
+      }
+      if constexpr (CX) {
+        vec[2 * d.row] = qr;
+        vec[2 * d.row + 1] = qi;
+      } else {
+        vec[d.row] = qr;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+  }
+  if (nf == nl) {  // no backward phase (never for ILU): keep barriers paired
+    cl_arrive();
+    cl_wait();
+    cl_arrive();
+    cl_wait();
+  }
+  cl_arrive();  // #4: every z is pushed everywhere
+  cl_wait();
+  bool bad = false;
+  for (int s = (int)rank + tid * C; s < n; s += NC * C) {
+    if constexpr (CX) {
+      const double qr = vec[2 * s], qi = vec[2 * s + 1];
+      bad = bad || !isfin(qr) || !isfin(qi);
+      reinterpret_cast<double2 *>(a.z)[s] = make_double2(qr, qi);
+    } else {
+      const double qr = vec[s];
+      bad = bad || !isfin(qr);
+      a.z[s] = qr;
+    }
+  }
+  if (bad) atomicOr(a.err, 1);
+}
+
 __global__ void gather_csweep_kernel(const double *lu, CSweep p, int cx) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= p.nval) return;
@@ -946,9 +1190,6 @@ __global__ void gather_csweep_kernel(const double *lu, CSweep p, int cx) {
 // entries streamed by a producer warp through a ring of TMA-filled slots
 // ---------------------------------------------------------------------
 
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 template <bool CX, bool ADJ>
 __global__ void __launch_bounds__(1024, 1) rsweep_kernel(SweepArgs a, RSweep p) {
@@ -1196,17 +1437,13 @@ size_t csweep_smem_limit() { return kSmemMax; }
 template <bool CX, bool ADJ>
 static void launch_csweep_t(const SweepArgs &a, const CSweep &p,
                             cudaStream_t st) {
-  static size_t attr_smem = 0;
-  static bool nonport = false;
-  auto kfn = csweep_kernel<CX, ADJ>;
-  if (attr_smem < p.smem) {
+  static bool attr[2] = {false, false};
+  auto kfn = p.dflow ? dsweep_kernel<CX, ADJ> : csweep_kernel<CX, ADJ>;
+  if (!attr[p.dflow]) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kSmemMax);
-    attr_smem = kSmemMax;
-  }
-  if (p.C > 8 && !nonport) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    nonport = true;
+    attr[p.dflow] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.C);

@@ -78,7 +78,8 @@ struct __align__(16) CSDesc {
   int row;     // repl: row index; distributed: pk of the row's slot
   int e0;      // first entry, relative to the segment
   int cnt;     // entries (the divisor, if any, follows them)
-  int hasdiv;
+  int hasdiv;  // bit 0: divisor present; bits 1..: the row's position k in
+               // its CTA's compute order of the phase (dataflow mode)
 };
 struct CSweep {
   int C = 0, T = 0;   // cluster size, threads per CTA (0: no plan)
@@ -95,6 +96,16 @@ struct CSweep {
   int maxslots = 0;           // vector slots per CTA
   int maxseg = 0;             // largest segment (bytes)
   size_t smem = 0;            // dynamic shared memory per CTA
+  // dataflow mode (dflow = 1, replicated vector): no barrier per level --
+  // a value's arrival in the local copy (it replaces a signalling-NaN
+  // sentinel) is the readiness signal; three cluster barriers per apply
+  // (start, forward/backward switch, end).  Initial values of each CTA's
+  // rows live in a local array indexed by the row's compute position k:
+  // the forward right-hand side, then y_i for the backward phase.
+  int dflow = 0;
+  int ninit = 0;              // max rows per CTA and phase
+  int *brow = nullptr;        // [C][..] backward rows in compute order
+  int *boff = nullptr;        // C+1 offsets into brow
 };
 
 // Ring sweep plan: one CTA holds the whole vector in shared memory; both

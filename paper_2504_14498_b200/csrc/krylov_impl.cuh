@@ -176,20 +176,25 @@ struct Solver : PlanBase {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // side branch of the captured iteration (convergence tests overlapped
   // with the next sweep): its own stream, fork/join events, partials
-  cudaStream_t st2 = nullptr;
-  cudaEvent_t evf = nullptr, evj = nullptr;
+  cudaStream_t st2 = nullptr, st3 = nullptr;
+  cudaEvent_t evf = nullptr, evj = nullptr, evj3 = nullptr;
   double *part2 = nullptr;
   double *seqbuf = nullptr;  // twin-mode element terms [slot][i][2K]
   State *hp = nullptr;  // pinned host staging of the device State (x2)
   int *hpi = nullptr;
 
-  void fork() {
+  void fork(bool third = false) {
     cudaEventRecord(evf, st);
     cudaStreamWaitEvent(st2, evf, 0);
+    if (third) cudaStreamWaitEvent(st3, evf, 0);
   }
-  void join() {
+  void join(bool third = false) {
     cudaEventRecord(evj, st2);
     cudaStreamWaitEvent(st, evj, 0);
+    if (third) {
+      cudaEventRecord(evj3, st3);
+      cudaStreamWaitEvent(st, evj3, 0);
+    }
   }
 
   Solver(DMat &A_, const SolveParams &p_, cudaStream_t st_, char *eb)
@@ -217,8 +222,10 @@ struct Solver : PlanBase {
     cudaEventCreate(&ev0);
     cudaEventCreate(&ev1);
     cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&st3, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&evf, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&evj, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evj3, cudaEventDisableTiming);
     part2 = (double *)dalloc(sizeof(double) * 2 * kMaxGrid * 8);
     cudaMallocHost(&hp, sizeof(State) * 2);
     cudaMallocHost(&hpi, sizeof(int) * 4);
@@ -232,6 +239,8 @@ struct Solver : PlanBase {
     if (evf) cudaEventDestroy(evf);
     if (evj) cudaEventDestroy(evj);
     if (st2) cudaStreamDestroy(st2);
+    if (st3) cudaStreamDestroy(st3);
+    if (evj3) cudaEventDestroy(evj3);
     if (hp) cudaFreeHost(hp);
     if (hpi) cudaFreeHost(hpi);
     for (void *q : allocs) cudaFree(q);
@@ -963,17 +972,26 @@ struct Solver : PlanBase {
     const DA a = da;
     const long long L = ld;
     const double *pc = pp, *ptc = pt;
-    // q = A p ; qt = A^H pt ; sigma = hdot(pt, q)
-    rows<K, CX, 1, 0>(n, done, part, st,
-                      [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
-                        double qr[K], qi[K], wr[K], wi[K], pr[K], pi[K];
-                        spmv_row<K, CX, false, false>(a, (int)i, pc, L, qr, qi);
-                        spmv_row<K, CX, false, true>(a, (int)i, ptc, L, wr, wi);
-                        Q.store(i, qr, qi);
-                        QT.store(i, wr, wi);
-                        PT.load(i, pr, pi);
-                        acc_hdot<K, CX>(red.h[0], pr, pi, qr, qi);
-                      });
+    // q = A p ; sigma = hdot(pt, q) (role 0) || qt = A^H pt (role 1): the
+    // two SpMV chains run on separate threads
+    const long long nn = n;
+    rows<K, CX, 1, 0>(
+        n, done, part, st,
+        [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
+          if (i < nn) {
+            double qr[K], qi[K], pr[K], pi[K];
+            spmv_row<K, CX, false, false>(a, (int)i, pc, L, qr, qi);
+            Q.store(i, qr, qi);
+            PT.load(i, pr, pi);
+            acc_hdot<K, CX>(red.h[0], pr, pi, qr, qi);
+          } else {
+            const long long j = i - nn;
+            double wr[K], wi[K];
+            spmv_row<K, CX, false, true>(a, (int)j, ptc, L, wr, wi);
+            QT.store(j, wr, wi);
+          }
+        },
+        2);
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
           const Sc sg = finalize_slot<K, CX>(pt_, 0, G_, sm);
@@ -1017,8 +1035,8 @@ struct Solver : PlanBase {
     // hdot(zt, r), partials in part2) runs on the side branch, overlapped
     // with the norm test and the forward apply.  Work done after a stop is
     // dead (the next finalize exits on the done flag).
-    fork();
-    fin(S, err, part, G, st,
+    fork(true);
+    fin(S, err, part, G, st3,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
           const Sc ss = finalize_slot<K, false>(pt_, 0, G_, sm);
           if (threadIdx.x == 0) check_nrm<K>(S_, H, ss);
@@ -1032,7 +1050,7 @@ struct Solver : PlanBase {
                         Rr.load(i, rr, ri);
                         acc_hdot<K, CX>(red.h[0], wr, wi, rr, ri);
                       });
-    join();
+    join(true);
     fin(S, err, part2, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
           const Sc rn = finalize_slot<K, CX>(pt_, 0, G_, sm);

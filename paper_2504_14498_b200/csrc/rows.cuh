@@ -99,19 +99,24 @@ struct Red {
 #endif
 template <int K, bool CX, int NH, int NN, class F>
 __global__ void __launch_bounds__(kBlock, MPK_ROWS_MIN_BLOCKS)
-    rows_kernel(long long n, const int *done, double *part, double *seq, F f) {
+    rows_kernel(long long n_total, long long n, const int *done, double *part,
+                double *seq, F f) {
+  // n_total = roles * n: element i of role r is index r * n + i; only role 0
+  // (i < n) contributes to the reductions
   if (done && *done) return;
   __shared__ double smem[kWarpsPerBlock * 8];
   Red<K, CX, NH, NN> red;
   red.zero();
-  for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < n;
+  for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < n_total;
        i += (long long)gridDim.x * kBlock) {
     if (seq) {  // twin mode: element i's terms -> seq[slot][i]
+      const bool own = i < n;
 #pragma unroll
-      for (int s = 0; s < NH; ++s) red.h[s].seq = seq + ((size_t)s * n + i) * 2 * K;
+      for (int s = 0; s < NH; ++s)
+        red.h[s].seq = own ? seq + ((size_t)s * n + i) * 2 * K : nullptr;
 #pragma unroll
       for (int s = 0; s < NN; ++s)
-        red.nr[s].seq = seq + ((size_t)(NH + s) * n + i) * 2 * K;
+        red.nr[s].seq = own ? seq + ((size_t)(NH + s) * n + i) * 2 * K : nullptr;
     }
     f(i, red);
   }
@@ -185,13 +190,17 @@ inline void prefer_max_smem(KFn kfn) {
   }
 }
 
+// roles > 1: the kernel runs roles * n threads; f(i) with i >= n does the
+// independent part of element i % n assigned to role i / n (see callers)
 template <int K, bool CX, int NH, int NN, class F>
-void rows(long long n, const int *done, double *part, cudaStream_t st, F f) {
+void rows(long long n, const int *done, double *part, cudaStream_t st, F f,
+          int roles = 1) {
   ++tl_launches;
   prefer_max_smem(rows_kernel<K, CX, NH, NN, F>);
   double *seq = (NH + NN > 0) ? tl_seq : nullptr;
-  rows_kernel<K, CX, NH, NN, F><<<grid_for(n), kBlock, 0, st>>>(n, done, part,
-                                                                 seq, f);
+  const long long nt = n * roles;
+  rows_kernel<K, CX, NH, NN, F><<<grid_for(nt), kBlock, 0, st>>>(nt, n, done, part,
+                                                                  seq, f);
   if (seq) {
     ++tl_launches;
     constexpr int chains = NH * (CX ? 2 : 1) + NN;

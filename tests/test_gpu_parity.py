@@ -342,10 +342,15 @@ SWEEP_PATHS = {
     "auto": {},
     "cluster1": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "1"},
     "cluster2": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "2", "MPK_CSWEEP_ROWS": "1"},
-    "cluster8": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "8", "MPK_CSWEEP_ROWS": "1"},
-    "cluster16": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "16", "MPK_CSWEEP_ROWS": "1"},
+    "cluster8": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "8", "MPK_CSWEEP_DFLOW": "0",
+                 "MPK_CSWEEP_ROWS": "1"},
+    "cluster16": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "16", "MPK_CSWEEP_DFLOW": "0",
+                  "MPK_CSWEEP_ROWS": "1"},
     "cluster8d": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "8", "MPK_CSWEEP_REPL": "0",
                   "MPK_CSWEEP_ROWS": "1"},
+    "dflow4": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "4"},
+    "dflow8": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "8"},
+    "dflow16": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "16"},
 }
 
 
