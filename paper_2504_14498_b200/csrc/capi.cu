@@ -642,6 +642,65 @@ static void free_sweeps(SweepMats &sm) {
   free_phase(sm.bwd);
   free_cplan(sm.cs);
   free_rplan(sm.rs);
+  free_wsweep(sm.wf);
+}
+
+// Average device time of one plain ILU(0) apply (sentinel reset + sweep)
+// through the current plan dispatch (do_sweep); placeholder values.
+static float time_apply_plan(DMat &A, cudaStream_t st) {
+  const int n = A.n;
+  const size_t w = A.cx ? 2 : 1;
+  double *in = nullptr, *y = nullptr, *z = nullptr;
+  int *err = nullptr, *tick = nullptr;
+  cudaMalloc(&in, sizeof(double) * w * n + 16);
+  cudaMalloc(&y, sizeof(double) * w * n + 16);
+  cudaMalloc(&z, sizeof(double) * w * n + 16);
+  cudaMalloc(&err, sizeof(int) * 4);
+  cudaMalloc(&tick, sizeof(int) * 4);
+  cudaMemsetAsync(in, 0, sizeof(double) * w * n + 16, st);
+  cudaMemsetAsync(tick, 0, sizeof(int) * 4, st);
+  SweepArgs a{};
+  a.n = n;
+  a.rp = A.rp;
+  a.ci = A.ci;
+  a.dp = A.dp;
+  a.lu = A.lu ? A.lu : A.val;
+  a.ord_f = A.ord_f;
+  a.ord_b = A.ord_b;
+  a.lev_f = A.lev_f;
+  a.lev_b = A.lev_b;
+  a.nlev_f = A.levels_f;
+  a.nlev_b = A.levels_b;
+  a.in_re = in;
+  a.in_im = A.cx ? in + n : nullptr;
+  a.y = y;
+  a.z = z;
+  a.tick = tick;
+  a.err = err;
+  a.done = nullptr;
+  const long long l0 = tl_launches;
+  auto go = [&]() {
+    launch_sweep_reset(y, z, n, A.cx, nullptr, st);
+    do_sweep(A, a, false, st);
+  };
+  go();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  const int reps = 3;
+  for (int r = 0; r < reps; ++r) go();
+  cudaEventRecord(e1, st);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  tl_launches = l0;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  void *q[] = {in, y, z, err, tick};
+  for (void *v : q) cudaFree(v);
+  if (cudaGetLastError() != cudaSuccess) return 1e30f;
+  return ms / reps;
 }
 
 }  // namespace
@@ -897,6 +956,31 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
   CKR(cudaMalloc(&m->rowflag, sizeof(int) * (n + 1)));
   CKR(cudaMalloc(&m->fscratch, sizeof(int) * 4));
   CKR(cudaStreamSynchronize(st));
+  // lane-chunk wavefront plan (wf.cu) for banded sweep DAGs: kept when it
+  // beats the plan chosen above on this device (MPK_SWEEP_PICK=wf forces it)
+  {
+    WSweep wf;
+    if (build_wsweep(wf, (int)n, A.cx, A.h_rp.data(), A.h_ci.data(),
+                     A.h_dp.data(), A.levels_f, A.levels_b, st)) {
+      const char *pick = getenv("MPK_SWEEP_PICK");
+      const bool force = pick && !strcmp(pick, "wf");
+      const bool other = pick && !force;
+      float tb = 1e30f, tw = 0.f;
+      if (!force && !other) tb = time_apply_plan(A, st);
+      A.smat.wf = wf;
+      if (!force && !other) tw = time_apply_plan(A, st);
+      if (other || !(tw < tb)) free_wsweep(A.smat.wf);
+      if (getenv("MPK_VERBOSE"))
+        fprintf(stderr,
+                "[mpk] wavefront plan n=%lld: fwd Lc=%d lag=%d groups=%d S=%d, "
+                "bwd Lc=%d lag=%d groups=%d S=%d; apply %.4f ms vs %.4f ms "
+                "(other plan) -> %s\n",
+                (long long)n, wf.f.Lc, wf.f.lag, wf.f.ngroups, wf.f.S, wf.b.Lc,
+                wf.b.lag, wf.b.ngroups, wf.b.S, tw, tb,
+                A.smat.wf.on ? "wavefront" : "other");
+    }
+    CKR(cudaGetLastError());
+  }
   *out = m;
   return MPK_OK;
 }
@@ -997,6 +1081,7 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   }
   gather_csweep(A.lu, A.smat.cs, A.cx, m->ctx->stream);
   gather_rsweep(A.lu, A.smat.rs, A.cx, m->ctx->stream);
+  gather_wsweep(A.lu, A.smat.wf, A.cx, m->ctx->stream);
   return MPK_OK;
 }
 

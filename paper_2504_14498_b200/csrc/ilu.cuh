@@ -16,6 +16,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "wf.cuh"
 
 namespace mpk {
 
@@ -149,7 +150,14 @@ struct SweepMats {
   bool conj = false;  // adjoint: values are conjugated at use
   CSweep cs;          // cluster plan (cs.C > 0 when built)
   RSweep rs;          // ring plan (rs.nchunks > 0 when built)
+  WSweep wf;          // lane-chunk wavefront plan (wf.on when kept; wf.cu)
 };
+// wavefront plan (wf.cuh): analysis at upload, values gathered per factorization
+bool build_wsweep(WSweep &w, int n, bool cx, const int *rp, const int *ci,
+                  const int *dp, int nlev_f, int nlev_b, cudaStream_t st);
+void gather_wsweep(const double *lu, const WSweep &w, bool cx, cudaStream_t st);
+void launch_wsweep(const SweepArgs &a, const WSweep &w, bool cx, cudaStream_t st);
+void free_wsweep(WSweep &w);
 void launch_rsweep(const SweepArgs &a, const RSweep &p, bool cx, bool adjoint,
                    cudaStream_t st);
 void gather_rsweep(const double *lu, const RSweep &p, bool cx, cudaStream_t st);

@@ -87,7 +87,9 @@ inline void do_sweep(const DMat &A, const SweepArgs &a, bool adjoint,
   const bool mats = adjoint ? A.smat_adj_built : A.smat_built;
   const CSweep &cs = adjoint ? A.smat_adj.cs : A.smat.cs;
   const RSweep &rs = adjoint ? A.smat_adj.rs : A.smat.rs;
-  if (rs.nchunks > 0)
+  if (!adjoint && A.smat.wf.on)
+    launch_wsweep(a, A.smat.wf, A.cx, st);
+  else if (rs.nchunks > 0)
     launch_rsweep(a, rs, A.cx, adjoint, st);
   else if (cs.C > 0)
     launch_csweep(a, cs, A.cx, adjoint, st);

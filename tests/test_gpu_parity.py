@@ -351,6 +351,7 @@ SWEEP_PATHS = {
     "dflow4": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "4"},
     "dflow8": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "8"},
     "dflow16": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "16"},
+    "wavefront": {"MPK_SWEEP_PICK": "wf"},
 }
 
 
@@ -385,6 +386,65 @@ def test_device_sweep_paths_bitwise(pkg, monkeypatch, path, mat):
         assert bits_equal(z.re, zr), (path, mat, adj)
         if vim is not None:
             assert bits_equal(z.im, zi), (path, mat, adj)
+
+
+WF_MATS = {
+    "cd5_64": lambda pr: pr.convdiff5(64, 10.0)[:3] + (None,),
+    "cd9_200": lambda pr: pr.convdiff9(200, 5.0)[:3] + (None,),
+    "cd9_97": lambda pr: pr.convdiff9(97, 5.0)[:3] + (None,),
+    "helm_c12": lambda pr: pr.helmholtz7(12, 7)[:4],
+}
+
+
+@pytest.mark.parametrize("mat", list(WF_MATS))
+@pytest.mark.parametrize("pick", ["wf", "auto"])
+def test_device_wavefront_sweep_bitwise(pkg, monkeypatch, mat, pick):
+    """The lane-chunk wavefront plan (wf.cu; grid stencils in natural order,
+    5-/9-point 2D real, 7-point 3D complex, grids not a multiple of a warp)
+    gives the oracle's ILU(0)-mixed apply bit for bit (ilu.py:322-343,
+    448-458), both when forced and when picked by the upload-time timing."""
+    import oracle.oracle as orc
+    from paper_2504_14498_b200 import problems
+
+    if pick == "wf":
+        monkeypatch.setenv("MPK_SWEEP_PICK", "wf")
+    rp, ci, vre, vim = WF_MATS[mat](problems)
+    n = len(rp) - 1
+    A = _csr(pkg, rp, ci, vre, vim)
+    F = pkg.ilu0_factorize_demoted(A)
+    rc, lre, lim = orc.ilu0_factor(n, rp, ci, vre, vim)[:3]
+    assert rc == 0
+    rng = np.random.default_rng(5)
+    for rep in range(2):  # repeated applies: ticket reset, sentinels
+        r_re = rng.standard_normal((n, 2))
+        r_im = rng.standard_normal((n, 2)) if vim is not None else None
+        r = pkg.DenseVector(r_re.copy(), None if r_im is None else r_im.copy(),
+                            pkg.Precision.DD)
+        z = pkg.ilu0_apply_mixed(F, r)
+        _, zr, zi = orc.ilu0_apply_mixed(n, rp, ci, lre, lim, r_re, r_im, adjoint=False)
+        assert bits_equal(z.re, zr), (mat, pick, rep)
+        if vim is not None:
+            assert bits_equal(z.im, zi), (mat, pick, rep)
+
+
+def test_device_wavefront_solve_cfg1(pkg, monkeypatch):
+    """cfg1 DD BiCGSTAB with the wavefront plan inside the captured solver
+    graph: the reference's iteration count, and in twin mode a residual
+    history bit-identical to the golden fixture."""
+    monkeypatch.setenv("MPK_SWEEP_PICK", "wf")
+    from paper_2504_14498_b200 import problems
+
+    g = golden("solver_cfg1.npz")
+    p = problems.cfg1()
+    A, b = _problem_b(pkg, p, 2)
+    cfg = pkg.SolverConfig(method="bicgstab", precision=pkg.Precision.DD,
+                           precond=pkg.PrecondMode.ILU0_MIXED, spmv_mode="mixed",
+                           eps_rel=p.eps_rel, max_iter=p.max_iter)
+    pre = "cfg1_bicgstab_dd"
+    with pkg.reduction_mode("sequential"):
+        rep = pkg.solve(A, b, cfg)
+    assert rep.iterations == int(g[f"{pre}_iterations"]) and rep.converged
+    assert bits_equal(np.asarray(rep.history), g[f"{pre}_hist"])
 
 
 # ---------------------------------------------------------------------------
