@@ -72,9 +72,15 @@ __device__ __forceinline__ void cp_async_v(double *dst, const double *src) {
   else
     cp_async8(dst, src);
 }
+// sentinel test on the high word only: 0x7FF40000 is a signalling NaN no
+// binary64 operation produces and published values are never signalling
+// with that payload (wf_pub), so the low word need not be compared
+__device__ __forceinline__ bool wf_hi_sent(double v) {
+  return __double2hiint(v) == (int)(kSentBits >> 32);
+}
 template <bool CX>
 __device__ __forceinline__ bool wf_sent(double r, double m) {
-  return is_sent(r) || (CX && is_sent(m));
+  return wf_hi_sent(r) || (CX && wf_hi_sent(m));
 }
 template <bool CX>
 __device__ __forceinline__ void wf_poll(const double *buf, int j, double &r,
@@ -85,16 +91,19 @@ __device__ __forceinline__ void wf_poll(const double *buf, int j, double &r,
     wf_ld<CX>(buf, j, r, m);
   }
 }
+__device__ __forceinline__ double wf_unsent(double v) {
+  return wf_hi_sent(v) ? __longlong_as_double((long long)kQNaNBits) : v;
+}
 template <bool CX>
 __device__ __forceinline__ void wf_pub(double *buf, int j, double r, double m) {
   if constexpr (CX) {
-    const double2 v = make_double2(unsent(r), unsent(m));
+    const double2 v = make_double2(wf_unsent(r), wf_unsent(m));
     asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(
                      reinterpret_cast<double2 *>(buf) + j),
                  "d"(v.x), "d"(v.y));
   } else {
     asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(buf + j),
-                 "d"(unsent(r)));
+                 "d"(wf_unsent(r)));
   }
 }
 
@@ -113,106 +122,174 @@ __device__ __forceinline__ void wf_mulsub(double &ar, double &ai, double lr,
 }
 
 __device__ long long wf_dbg2[4096];  // clock64 per step of group 0 (dbg 2)
+__device__ int wf_dbg3[8192];        // slow-path steps per group (dbg)
 
-// Per-warp shared-memory layout (byte offsets from the warp's base; the
-// host analysis encodes value sources as such offsets):
-//   [0, 64) mbarriers | [64, 80) zero slot | [128, +kRing) ring [H][32] |
-//   stage [PG][EM+2][32] | NB record buffers
+// a / d on the critical path of a backward row: reciprocal (independent of
+// a, off the chain) + Markstein correction, then an exact residual test
+// that PROVES the result equals RN(a / d) (= __ddiv_rn): with e = a - q*d
+// exact (fma; q within an ulp of a/d), q == RN(a/d) iff |a/d - q| < ulp(q)/2
+// i.e. |e| < |d| * ulp(q)/2 (ties cannot occur in this range).  Outside
+// the safe exponent range, for q a power of two (asymmetric ulp) or when
+// the test fails, ok = false and the caller divides with __ddiv_rn.
+__device__ __forceinline__ double wf_fast_div(double a, double d, bool &ok) {
+  const double r = __drcp_rn(d);
+  const double q0 = __dmul_rn(a, r);
+  const double e0 = fma(-q0, d, a);
+  const double q1 = fma(e0, r, q0);
+  const double e1 = fma(-q1, d, a);
+  const double q2 = fma(e1, r, q1);
+  const double e2 = fma(-q2, d, a);
+  const unsigned long long qb = (unsigned long long)__double_as_longlong(q2);
+  const unsigned long long ab = (unsigned long long)__double_as_longlong(a);
+  const unsigned long long db = (unsigned long long)__double_as_longlong(d);
+  const int eq = (int)((qb >> 52) & 0x7ff), ea = (int)((ab >> 52) & 0x7ff),
+            ed = (int)((db >> 52) & 0x7ff);
+  const double half_ulp = __longlong_as_double((long long)(eq - 53) << 52);
+  ok = eq > 256 && eq < 1792 && ea > 256 && ea < 1792 && ed > 256 && ed < 1792 &&
+       (qb & 0xFFFFFFFFFFFFFull) != 0 && fabs(e2) < __dmul_rn(fabs(d), half_ulp);
+  return q2;
+}
+
+// Shared-memory layout of one CTA (= one group at a time, two warps:
+// warp 0 computes, warp 1 stages remote values), byte offsets; the host
+// analysis encodes value sources as such offsets:
+//   [0, 128) mbarriers | [128, 144) zero slot | ring [H][32] |
+//   stage [NS][T][EM+2][32] | NB record buffers
 // Record of one (group, step):
 //   int32 off[EM][32] (value source: ring / stage / zero slot) |
 //   int32 col[EM][32] (global row for stage-sourced values, else -1) |
 //   value[EM][32] | divisor[32] (backward)
+constexpr int kWfNS = 3;  // stage chunks (helper lead)
 template <bool CX>
 struct WfLayout {
   static constexpr int VB = CX ? 16 : 8;        // value bytes
-  static constexpr int PG = CX ? 4 : 8;         // global-value prefetch depth
-  static constexpr int kZero = 64;
-  static constexpr int kRingOff = 128;
+  static constexpr int kZero = 128;
+  static constexpr int kRingOff = 256;
   static constexpr int kRing = 32 * kWfH * VB;
   static constexpr int kStageOff = kRingOff + kRing;
-  static constexpr int kStage = PG * (kWfEM + 2) * 32 * VB;
-  static constexpr int kBufOff = kStageOff + kStage;
+  static constexpr int kStage = kWfNS * kWfT * (kWfEM + 2) * 32 * VB;
+  // rhs ring [4 chunks][2 planes][32 lanes][10 f64]: a lane's T values of
+  // a chunk are contiguous (16-byte copies), lane stride 80 B (2-way banks)
+  static constexpr int kRhsOff = kStageOff + kStage;
+  static constexpr int kRhs = 4 * 2 * 32 * 80;
+  static constexpr int kBufOff = kRhsOff + kRhs;
+  static __host__ __device__ constexpr int rhs_base(int c, int plane, int j) {
+    return kRhsOff + (((c & 3) * 2 + plane) * 32 + j) * 80;
+  }
   static constexpr int kOffB = kWfEM * 32 * 4;  // off block bytes
   static constexpr int kValOff = 2 * kOffB;     // values after off + col
   static constexpr int kVal = kWfEM * 32 * VB;
   static __host__ __device__ constexpr int ring_slot(int sq, int jq) {
     return kRingOff + ((sq & (kWfH - 1)) * 32 + jq) * VB;
   }
-  static __host__ __device__ constexpr int stage_slot(int u, int slot, int j) {
-    return kStageOff + ((u * (kWfEM + 2) + slot) * 32 + j) * VB;
+  // step s of a group (chunks restart at stage buffer 0 for every group)
+  static __host__ __device__ constexpr int stage_slot(int s, int slot, int j) {
+    return kStageOff +
+           ((((s / kWfT) % kWfNS) * kWfT + (s % kWfT)) * (kWfEM + 2) + slot) * 32 * VB +
+           j * VB;
   }
 };
 
-// One group (32 lanes) of one phase, run by the calling warp.  Per step the
-// lane's row is a branch-free chain: every entry reads its value through a
-// precomputed shared-memory offset (ring, prefetched stage, or the zero slot
-// for padding: acc - 0*0 == acc bit for bit), one rarely taken branch
-// re-polls stage values that were still sentinels when prefetched.
+// barriers: rec_full[NB] at 0
+__device__ __forceinline__ uint64_t *wf_bar(unsigned char *base, int i) {
+  return reinterpret_cast<uint64_t *>(base) + i;
+}
+
+// One group (32 lanes) of one phase, run by one warp.  Chunk c (T steps):
+// its step records arrive by TMA bulk copies NB chunks ahead; the remote
+// values of chunk c + 1 (right-hand sides, dependencies the ring does not
+// hold) are requested by cp.async at the top of chunk c.  Per step the lane's row is a
+// branch-free chain: every entry reads its value through a precomputed
+// shared-memory offset (ring, stage, or the zero slot for padding: acc -
+// 0*0 == acc bit for bit); a staged value still carrying the sentinel (not
+// yet published when requested) is re-polled with an L1-bypassing load.
+// L1-cached cp.async copies are safe: L1 starts every launch invalidated
+// and a published slot only changes sentinel -> final value, so a stale
+// copy can only be a sentinel.
 template <bool CX, bool FWD>
 __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
-                                         int gl, unsigned &cc, uint64_t *bar,
-                                         unsigned char *wbase, int bufsz,
-                                         bool dbgstep) {
+                                         int gl, unsigned char *wbase,
+                                         int bufsz, bool dbgstep, bool dbgcnt,
+                                         int dbgg) {
   using Lt = WfLayout<CX>;
-  constexpr int PG = Lt::PG;
   constexpr int VW = CX ? 2 : 1;
   const int j = threadIdx.x & 31;
   const int n = a.n, S = P.S, rs = P.recsz, Lc = P.Lc, lag = P.lag;
   const int nch = S / kWfT;
-  const unsigned char *src = P.rec + (size_t)gl * S * rs;
-  const long long p0 = ((long long)gl * 32 + j) * Lc - (long long)lag * j;
+  const unsigned char *src = P.rec + (size_t)gl * nch * P.chunkb;
+  const int p0 = (gl * 32 + j) * Lc - lag * j;  // n < 2^31 (C ABI check)
   const int pos0 = -lag * j;
   double *glob = FWD ? a.y : a.z;
   unsigned char *buf = wbase + Lt::kBufOff;
-  const uint32_t cb = (uint32_t)(kWfT * rs);
+  const uint32_t cb = (uint32_t)P.chunkb;
   if (j == 0) {
     const int first = nch < kWfNB ? nch : kWfNB;
     for (int c = 0; c < first; ++c) {
-      const int b = (int)((cc + c) % kWfNB);
-      wf_mbar_arrive_tx(&bar[b], cb);
-      wf_bulk(buf + (size_t)b * bufsz, src + (size_t)c * cb, cb, &bar[b]);
+      wf_mbar_arrive_tx(wf_bar(wbase, c), cb);
+      wf_bulk(buf + (size_t)c * bufsz, src + (size_t)c * cb, cb, wf_bar(wbase, c));
     }
   }
   auto recp = [&](int s) -> const unsigned char * {
-    const unsigned c = (unsigned)(s / kWfT);
-    return buf + (size_t)((cc + c) % kWfNB) * bufsz + (size_t)(s % kWfT) * rs;
+    return buf + (size_t)((s / kWfT) % kWfNB) * bufsz + (size_t)(s % kWfT) * rs;
   };
-  // lane active at step s: 0 <= s + pos0 < Lc and position < n
-  auto active = [&](int s, long long &pp) -> bool {
-    pp = p0 + s;
-    return (unsigned)(s + pos0) < (unsigned)Lc && pp < n;
+  auto rec_wait = [&](int c) {
+    if (c < nch) wf_mbar_wait(wf_bar(wbase, c % kWfNB), (c / kWfNB) & 1);
   };
-  // PG steps ahead: cp.async of the rhs and of stage-sourced values (L1
-  // may serve a stale copy only as a sentinel, see wf_poll below)
-  // cp.async of step s's rhs / stage-sourced values (col: the record's
-  // global rows, read ahead by the caller)
-  auto prefetch = [&](int s, int u, const int (&col)[kWfEM]) {
-    long long pp;
-    if (s < S && active(s, pp)) {
-      const int row = FWD ? (int)pp : (int)(n - 1 - pp);
-      double *rh = reinterpret_cast<double *>(wbase + Lt::stage_slot(u, kWfEM, j));
-      if constexpr (FWD) {
-        cp_async8(rh, a.in_re + row);
-        if constexpr (CX)
-          cp_async8(reinterpret_cast<double *>(wbase + Lt::stage_slot(u, kWfEM + 1, j)),
-                    a.in_im + row);
-      } else {
-        cp_async_v<CX>(rh, a.y + (size_t)row * VW);
+  // cp.async of chunk c's remote dependency values (one commit group per
+  // chunk, maybe empty): the chunk's fetch table spreads them over the 32
+  // lanes ({global row, shared offset} items, row -1 = none)
+  auto deps_issue = [&](int c) {
+    if (c < nch) {
+      const int2 *ft = reinterpret_cast<const int2 *>(
+          buf + (size_t)(c % kWfNB) * bufsz + (size_t)kWfT * rs);
+      for (int r = 0; r < P.kmax; ++r) {
+        const int2 it = ft[r * 32 + j];
+        if (it.x >= 0)
+          cp_async_v<CX>(reinterpret_cast<double *>(wbase + it.y), glob + (size_t)it.x * VW);
       }
-#pragma unroll
-      for (int e = 0; e < kWfEM; ++e)
-        if (col[e] >= 0)
-          cp_async_v<CX>(reinterpret_cast<double *>(wbase + Lt::stage_slot(u, e, j)),
-                         glob + (size_t)col[e] * VW);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  auto load_cols = [&](int s, int (&col)[kWfEM]) {
-    const int *colp = reinterpret_cast<const int *>(recp(s) + Lt::kOffB);
+  // chunk c's right-hand sides (static input / forward results, requested
+  // 3 chunks ahead): a lane's T rows are consecutive, 4 x 16-byte copies
+  // when aligned and all active, else one 8-byte copy per active step
+  auto rhs_issue = [&](int c) {
+    if (c < nch) {
+      const int s0 = c * kWfT;
+      const int pa = p0 + s0;
+      const bool full = (unsigned)(s0 + pos0) < (unsigned)Lc &&
+                        (unsigned)(s0 + pos0 + kWfT - 1) < (unsigned)Lc &&
+                        pa + kWfT - 1 < n;
+      double *d0 = reinterpret_cast<double *>(wbase + Lt::rhs_base(c, 0, j));
+      if (!CX && P.rhs16 && full) {
+        const double *g0 = FWD ? a.in_re + pa : a.y + (n - kWfT - pa);
 #pragma unroll
-    for (int e = 0; e < kWfEM; ++e) col[e] = s < S ? colp[e * 32 + j] : -1;
+        for (int q = 0; q < kWfT / 2; ++q)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(wf_smem_u32(d0 + 2 * q)),
+                       "l"(g0 + 2 * q)
+                       : "memory");
+      } else {
+        double *d1 = reinterpret_cast<double *>(wbase + Lt::rhs_base(c, 1, j));
+#pragma unroll
+        for (int t = 0; t < kWfT; ++t) {
+          const int s = s0 + t;
+          const int pp = p0 + s;
+          if ((unsigned)(s + pos0) < (unsigned)Lc && pp < n) {
+            const int row = FWD ? pp : n - 1 - pp;
+            const int ix = FWD ? t : kWfT - 1 - t;
+            if constexpr (FWD) {
+              cp_async8(d0 + ix, a.in_re + row);
+              if constexpr (CX) cp_async8(d1 + ix, a.in_im + row);
+            } else {
+              cp_async8(d0 + ix, a.y + (size_t)row * VW);
+              if constexpr (CX) cp_async8(d1 + ix, a.y + (size_t)row * VW + 1);
+            }
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  // record fields of a step, read one step ahead
   int off[kWfEM];
   double lr[kWfEM], li[kWfEM];
   auto load_rec = [&](int s) {
@@ -225,29 +302,31 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
       li[e] = CX ? val[(e * 32 + j) * VW + 1] : 0.0;
     }
   };
-  wf_mbar_wait(&bar[cc % kWfNB], (cc / kWfNB) & 1);
-  if (nch > 1) wf_mbar_wait(&bar[(cc + 1) % kWfNB], ((cc + 1) / kWfNB) & 1);
-#pragma unroll
-  for (int u = 0; u < PG; ++u) {
-    int col[kWfEM];
-    load_cols(u, col);
-    prefetch(u, u, col);
-  }
+  // commit order per chunk c: deps(c + 1), rhs(c + 3); at the top of chunk
+  // c the three most recent groups (rhs(c+3), deps(c+1), rhs(c+2)) may
+  // still be pending: deps(c) and rhs(c) are complete
+  rec_wait(0);
+  deps_issue(0);
+  rhs_issue(0);
+  rhs_issue(1);
+  rhs_issue(2);
   load_rec(0);
+  const bool dbc = dbgstep && j == 0;
   for (int c = 0; c < nch; ++c) {
-    if (c + 1 < nch) {
-      const unsigned q = cc + c + 1;
-      wf_mbar_wait(&bar[q % kWfNB], (q / kWfNB) & 1);
-    }
+    if (dbc && c < 256) wf_dbg2[3072 + 4 * c] = clock64();
+    rec_wait(c + 1);
+    if (dbc && c < 256) wf_dbg2[3072 + 4 * c + 1] = clock64();
+    deps_issue(c + 1);
+    if (dbc && c < 256) wf_dbg2[3072 + 4 * c + 2] = clock64();
+    rhs_issue(c + 3);
+    if (dbc && c < 256) wf_dbg2[3072 + 4 * c + 3] = clock64();
+    asm volatile("cp.async.wait_group 3;" ::: "memory");  // deps(c), rhs(c) landed
 #pragma unroll
     for (int t = 0; t < kWfT; ++t) {
       const int s = c * kWfT + t;
-      const int u = t % PG;
-      if (dbgstep && j == 0 && s < 1024) wf_dbg2[4 * s] = clock64();
-      asm volatile("cp.async.wait_group %0;" ::"n"(PG - 1) : "memory");
-      if (dbgstep && j == 0 && s < 1024) wf_dbg2[4 * s + 1] = clock64();
-      long long pp;
-      const bool act = active(s, pp);
+      if (dbgstep && j == 0 && s < 3072) wf_dbg2[s] = clock64();
+      const int pp = p0 + s;
+      const bool act = (unsigned)(s + pos0) < (unsigned)Lc && pp < n;
       double vr[kWfEM], vi[kWfEM], cl[kWfEM], cm[kWfEM];
       bool bad = false;
 #pragma unroll
@@ -259,23 +338,19 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
         cm[e] = li[e];
         bad |= wf_sent<CX>(vr[e], vi[e]);
       }
-      const double *rh = reinterpret_cast<const double *>(wbase + Lt::stage_slot(u, kWfEM, j));
+      const int rix = FWD ? t : kWfT - 1 - t;
+      const double *rh = reinterpret_cast<const double *>(wbase + Lt::rhs_base(c, 0, j)) + rix;
+      const double *rh1 = reinterpret_cast<const double *>(wbase + Lt::rhs_base(c, 1, j)) + rix;
       double ar, ai;
-      if constexpr (FWD) {
-        if constexpr (CX) {
-          const double re0 = rh[0];
-          const double im0 = *reinterpret_cast<const double *>(
-              wbase + Lt::stage_slot(u, kWfEM + 1, j));
-          ar = dadd(re0, dsub(dmul(0.0, im0), 0.0));  // numpy re + 1j*im
-          ai = dadd(0.0, im0);
-        } else {
-          ar = rh[0];
-          ai = 0.0;
-        }
+      if constexpr (FWD && CX) {
+        const double re0 = rh[0];
+        const double im0 = rh1[0];
+        ar = dadd(re0, dsub(dmul(0.0, im0), 0.0));  // numpy re + 1j*im
+        ai = dadd(0.0, im0);
       } else {
         ar = rh[0];
-        ai = CX ? rh[1] : 0.0;
-        bad |= wf_sent<CX>(ar, ai);
+        ai = CX ? rh1[0] : 0.0;
+        if (!FWD) bad |= wf_sent<CX>(ar, ai);
       }
       double dr = 0.0, di = 0.0;
       if constexpr (!FWD) {
@@ -284,52 +359,71 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
         dr = dv[j * VW];
         di = CX ? dv[j * VW + 1] : 0.0;
       }
-      // read ahead: the next step's record, the cols of step s + PG
-      if (s + 1 < S) load_rec(s + 1);
-      int coln[kWfEM];
-      load_cols(s + PG, coln);
-      if (dbgstep && j == 0 && s < 1024) wf_dbg2[4 * s + 2] = clock64();
-      if (act && bad) {  // a prefetched value was not yet published
-        const int row = FWD ? (int)pp : (int)(n - 1 - pp);
+      if (s + 1 < S) load_rec(s + 1);  // read ahead
+      // common path: the chain on the staged values (no branch before it)
+      double xr = ar, xi = ai;
+#pragma unroll
+      for (int e = 0; e < kWfEM; ++e) wf_mulsub<CX>(xr, xi, cl[e], cm[e], vr[e], vi[e]);
+      bool slow = act && bad;
+      if constexpr (!FWD) {
+        if constexpr (CX) {
+          double qr, qi;
+          py_cdiv(xr, xi, dr, di, qr, qi);
+          xr = qr;
+          xi = qi;
+        } else {
+          bool ok;
+          xr = wf_fast_div(xr, dr, ok);
+          slow |= act && !ok;
+        }
+      }
+      if (slow && dbgcnt) atomicAdd(&wf_dbg3[dbgg], bad ? 1 : 65536);
+      if (slow) {  // a staged value was requested before it was published,
+                   // or the fast quotient is not provably RN: redo the row
+        const int row = FWD ? pp : n - 1 - pp;
         const int *col = reinterpret_cast<const int *>(recp(s) + Lt::kOffB);
 #pragma unroll
         for (int e = 0; e < kWfEM; ++e)
           if (wf_sent<CX>(vr[e], vi[e])) wf_poll<CX>(glob, col[e * 32 + j], vr[e], vi[e]);
         if (!FWD && wf_sent<CX>(ar, ai)) wf_poll<CX>(a.y, row, ar, ai);
-      }
+        xr = ar;
+        xi = ai;
 #pragma unroll
-      for (int e = 0; e < kWfEM; ++e) wf_mulsub<CX>(ar, ai, cl[e], cm[e], vr[e], vi[e]);
-      if constexpr (!FWD) {
-        if constexpr (CX) {
-          double qr, qi;
-          py_cdiv(ar, ai, dr, di, qr, qi);
-          ar = qr;
-          ai = qi;
-        } else {
-          ar = ddiv(ar, dr);
+        for (int e = 0; e < kWfEM; ++e) wf_mulsub<CX>(xr, xi, cl[e], cm[e], vr[e], vi[e]);
+        if constexpr (!FWD) {
+          if constexpr (CX) {
+            double qr, qi;
+            py_cdiv(xr, xi, dr, di, qr, qi);
+            xr = qr;
+            xi = qi;
+          } else {
+            xr = ddiv(xr, dr);
+          }
         }
+      }
+      ar = xr;
+      ai = xi;
+      if constexpr (!FWD) {
         if (act && (!isfin(ar) || !isfin(ai))) atomicOr(a.err, 1);
       }
       if (act) {
         double *rg = reinterpret_cast<double *>(wbase + Lt::ring_slot(s, j));
         rg[0] = ar;
         if constexpr (CX) rg[1] = ai;
-        wf_pub<CX>(glob, FWD ? (int)pp : (int)(n - 1 - pp), ar, ai);
+        wf_pub<CX>(glob, FWD ? pp : n - 1 - pp, ar, ai);
       }
-      if (dbgstep && j == 0 && s < 1024) wf_dbg2[4 * s + 3] = clock64();
-      prefetch(s + PG, u, coln);
       __syncwarp();
     }
-    // chunk c consumed: refill its buffer with chunk c + NB
+    // record chunk c consumed: refill its buffer with chunk c + NB
     if (j == 0 && c + kWfNB < nch) {
-      const int b = (int)((cc + c) % kWfNB);
-      wf_mbar_arrive_tx(&bar[b], cb);
+      const int b = c % kWfNB;
+      wf_mbar_arrive_tx(wf_bar(wbase, b), cb);
       wf_bulk(buf + (size_t)b * bufsz, src + (size_t)(c + kWfNB) * cb, cb,
-              &bar[b]);
+              wf_bar(wbase, b));
     }
     __syncwarp();
   }
-  cc += (unsigned)nch;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // diagnostics (MPK_WF_DEBUG=1): globaltimer at start / end of every group
@@ -342,42 +436,39 @@ __device__ __forceinline__ long long wf_gtime() {
 }
 
 template <bool CX>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(32, 1)
     wsweep_kernel(SweepArgs a, WPhase F, WPhase B, int bufsz, int dbg) {
   if (a.done && *a.done) return;
   using Lt = WfLayout<CX>;
   extern __shared__ __align__(128) unsigned char wsm[];
-  const int warp = threadIdx.x >> 5, j = threadIdx.x & 31;
-  const size_t per_warp = Lt::kBufOff + (size_t)kWfNB * bufsz;
-  unsigned char *base = wsm + (size_t)warp * per_warp;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(base);
-  if (j == 0) {
-    for (int b = 0; b < kWfNB; ++b) wf_mbar_init(&bar[b], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
+  const int j = threadIdx.x & 31;
+  unsigned char *base = wsm;
   if (j < 4) reinterpret_cast<double *>(base + Lt::kZero)[j & 1] = 0.0;
-  __syncwarp();
-  unsigned cc = 0;
   const int gtot = F.ngroups + B.ngroups;
   for (;;) {
     int g = 0;
-    if (j == 0) g = atomicAdd(a.tick, 1);
+    if (j == 0) {
+      g = atomicAdd(a.tick, 1);
+      // fresh barriers per group (no copy is pending here)
+      for (int b = 0; b < kWfNB; ++b) wf_mbar_init(wf_bar(base, b), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
     g = __shfl_sync(kFullW, g, 0);
+    __syncwarp();
     if (g >= gtot) break;
     if (dbg && j == 0 && g < 8192) wf_dbg[2 * g] = wf_gtime();
     if (g < F.ngroups)
-      wf_group<CX, true>(a, F, g, cc, bar, base, bufsz, dbg == 2 && g == 0);
+      wf_group<CX, true>(a, F, g, base, bufsz, dbg == 2 && g == 0, dbg != 0, g & 8191);
     else
-      wf_group<CX, false>(a, B, g - F.ngroups, cc, bar, base, bufsz, false);
+      wf_group<CX, false>(a, B, g - F.ngroups, base, bufsz, false, dbg != 0, g & 8191);
     if (dbg && j == 0 && g < 8192) wf_dbg[2 * g + 1] = wf_gtime();
+    __syncwarp();
   }
-  // last warp out resets the ticket for the next launch / graph replay
-  __syncwarp();
+  // last CTA out resets the ticket for the next launch / graph replay
   if (j == 0) {
-    const int total = gridDim.x * (blockDim.x >> 5);
     __threadfence();
-    if (atomicAdd(&a.tick[1], 1) == total - 1) {
+    if (atomicAdd(&a.tick[1], 1) == (int)gridDim.x - 1) {
       atomicExch(&a.tick[0], 0);
       atomicExch(&a.tick[1], 0);
     }
@@ -396,11 +487,12 @@ __global__ void wf_gather_kernel(const double *lu, WPhase P, int cx) {
       const long long gs = i / (kWfEM * 32);
       const int rem = (int)(i % (kWfEM * 32));
       srcp = P.esrc[i];
-      dst = P.rec + gs * P.recsz + kCode + (size_t)rem * VB;
+      dst = P.rec + (gs / kWfT) * P.chunkb + (gs % kWfT) * P.recsz + kCode + (size_t)rem * VB;
     } else {
       const long long d = i - P.nslots;
       srcp = P.dsrc[d];
-      dst = P.rec + (d / 32) * P.recsz + kCode + kVal + (d % 32) * VB;
+      const long long gs = d / 32;
+      dst = P.rec + (gs / kWfT) * P.chunkb + (gs % kWfT) * P.recsz + kCode + kVal + (d % 32) * VB;
     }
     if (cx) {
       const double2 v = srcp >= 0 ? reinterpret_cast<const double2 *>(lu)[srcp]
@@ -488,9 +580,8 @@ static bool build_phase_wf(WPhase &ph, int n, bool cx, bool fwd,
               : WfLayout<false>::ring_slot((int)sq, (int)jq);
   };
   auto stage_slot = [&](long long s, int e, long long j) {
-    const int PG = cx ? WfLayout<true>::PG : WfLayout<false>::PG;
-    return cx ? WfLayout<true>::stage_slot((int)(s % PG), e, (int)j)
-              : WfLayout<false>::stage_slot((int)(s % PG), e, (int)j);
+    return cx ? WfLayout<true>::stage_slot((int)s, e, (int)j)
+              : WfLayout<false>::stage_slot((int)s, e, (int)j);
   };
   const int zero = WfLayout<false>::kZero;
   for (long long gs = 0; gs < nsteps; ++gs) {
@@ -541,6 +632,32 @@ static bool build_phase_wf(WPhase &ph, int n, bool cx, bool fwd,
     if (!fwd) dsrc[(size_t)(gs * 32 + j)] = div(p);
   }
   if (!ok) return false;
+  // fetch tables: the staged values of each chunk spread over the 32 lanes
+  const long long nchunks = nsteps / kWfT;
+  std::vector<std::vector<int2>> items((size_t)nchunks);
+  int kmax = 0;
+  for (long long ch = 0; ch < nchunks; ++ch) {
+    for (int t = 0; t < kWfT; ++t) {
+      const int *off = reinterpret_cast<const int *>(rec.data() + (ch * kWfT + t) * ph.recsz);
+      const int *colv = off + kWfEM * 32;
+      for (int q = 0; q < kWfEM * 32; ++q)
+        if (colv[q] >= 0) items[(size_t)ch].push_back(make_int2(colv[q], off[q]));
+    }
+    kmax = std::max(kmax, (int)((items[(size_t)ch].size() + 31) / 32));
+  }
+  ph.kmax = kmax;
+  ph.chunkb = kWfT * ph.recsz + kmax * 32 * 8;
+  ph.rhs16 = (!cx && ph.Lc % 2 == 0 && ph.lag % 2 == 0 && (fwd || n % 2 == 0)) ? 1 : 0;
+  std::vector<unsigned char> packed((size_t)nchunks * ph.chunkb, 0);
+  for (long long ch = 0; ch < nchunks; ++ch) {
+    unsigned char *dst = packed.data() + ch * ph.chunkb;
+    memcpy(dst, rec.data() + ch * kWfT * ph.recsz, (size_t)kWfT * ph.recsz);
+    int2 *ft = reinterpret_cast<int2 *>(dst + (size_t)kWfT * ph.recsz);
+    for (int q = 0; q < kmax * 32; ++q)
+      ft[q] = q < (int)items[(size_t)ch].size() ? items[(size_t)ch][(size_t)q]
+                                                 : make_int2(-1, 0);
+  }
+  rec.swap(packed);
   auto up = [&](void **d, const void *h, size_t bytes) {
     if (cudaMalloc(d, bytes < 16 ? 16 : bytes) != cudaSuccess) return false;
     return cudaMemcpyAsync(*d, h, bytes, cudaMemcpyHostToDevice, st) ==
@@ -562,10 +679,10 @@ static void free_phase_wf(WPhase &ph) {
 
 static size_t wf_per_warp(const WSweep &w, bool cx) {
   const int VB = cx ? 16 : 8;
-  const int maxrec = std::max(w.f.recsz, w.b.recsz);
+  const int maxchunk = std::max(w.f.chunkb, w.b.chunkb);
   (void)VB;
   const size_t bo = cx ? WfLayout<true>::kBufOff : WfLayout<false>::kBufOff;
-  return bo + (size_t)kWfNB * kWfT * maxrec;
+  return bo + (size_t)kWfNB * maxchunk;
 }
 
 }  // namespace
@@ -612,14 +729,12 @@ bool build_wsweep(WSweep &w, int n, bool cx, const int *rp, const int *ci,
     return false;
   }
   const size_t pw = wf_per_warp(t, cx);
-  const size_t lim_smem = 220 * 1024;
-  int wpb = (int)std::min<size_t>(4, lim_smem / pw);
-  if (wpb < 1) {
+  if (pw > 220 * 1024) {
     free_wsweep(t);
     return false;
   }
-  t.wpb = wpb;
-  t.smem = pw * wpb;
+  t.wpb = 1;  // one warp = one group per CTA
+  t.smem = pw;
   t.on = 1;
   w = t;
   return true;
@@ -642,15 +757,15 @@ void launch_wsweep(const SweepArgs &a, const WSweep &w, bool cx,
                    cudaStream_t st) {
   ++tl_launches;
   static const int dbg = getenv("MPK_WF_DEBUG") ? atoi(getenv("MPK_WF_DEBUG")) : 0;
-  const int bufsz = kWfT * std::max(w.f.recsz, w.b.recsz);
+  const int bufsz = std::max(w.f.chunkb, w.b.chunkb);
   const int gtot = w.f.ngroups + w.b.ngroups;
-  int grid = (gtot + w.wpb - 1) / w.wpb;
+  int grid = gtot;
   if (grid > 148) grid = 148;
   if (cx) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(wsweep_kernel<true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       attr = true;
     }
     wsweep_kernel<true><<<grid, 32 * w.wpb, w.smem, st>>>(a, w.f, w.b, bufsz, dbg);
@@ -658,7 +773,7 @@ void launch_wsweep(const SweepArgs &a, const WSweep &w, bool cx,
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(wsweep_kernel<false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       attr = true;
     }
     wsweep_kernel<false><<<grid, 32 * w.wpb, w.smem, st>>>(a, w.f, w.b, bufsz, dbg);
@@ -668,6 +783,13 @@ void launch_wsweep(const SweepArgs &a, const WSweep &w, bool cx,
 }  // namespace mpk
 
 // diagnostics for tools/: per-group globaltimer stamps of the last launch
+extern "C" int mpk_wf_debug3(int *out, int reset) {
+  if (reset) {
+    static int z[8192];
+    return cudaMemcpyToSymbol(mpk::wf_dbg3, z, sizeof(z)) == cudaSuccess ? 0 : 4;
+  }
+  return cudaMemcpyFromSymbol(out, mpk::wf_dbg3, sizeof(int) * 8192) == cudaSuccess ? 0 : 4;
+}
 extern "C" int mpk_wf_debug2(long long *out) {
   return cudaMemcpyFromSymbol(out, mpk::wf_dbg2, sizeof(long long) * 4096) == cudaSuccess ? 0 : 4;
 }

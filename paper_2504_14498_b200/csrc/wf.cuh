@@ -23,10 +23,11 @@
 // DAG level (cfg4: 6142 levels per phase).
 //
 // The per-(group, step) entries are pre-laid out as fixed-size records
-//   int32 code[EM][32] | value[EM][32] (f64 / double2) | divisor[32] (bwd)
-// and streamed into shared memory by bulk async copies (TMA) T steps per
-// copy, NB copies in flight.  code < 0: ring slot -(code+1); code >= 0:
-// global row index (polled); kSkip: padding.
+//   int32 off[EM][32] | int32 col[EM][32] | value[EM][32] | divisor[32]
+// (off: shared-memory source of the value -- ring, stage or zero slot;
+// col: global row of a staged value), T records + a fetch table (the
+// chunk's staged values spread over the 32 lanes) per chunk, streamed into
+// shared memory by one bulk async copy (TMA) per chunk, NB in flight.
 #pragma once
 
 #include "common.cuh"
@@ -45,7 +46,10 @@ struct WPhase {
   int nlanes = 0, ngroups = 0;
   int S = 0;            // steps per group, padded to a multiple of kWfT
   int recsz = 0;        // bytes per step record
-  unsigned char *rec = nullptr;  // [ngroups][S] records
+  int kmax = 0;         // fetch-table rounds per chunk (32 items each)
+  int chunkb = 0;       // bytes per chunk: T records + fetch table
+  int rhs16 = 0;        // lane rows 16-byte aligned per chunk (vector rhs copies)
+  unsigned char *rec = nullptr;  // [ngroups][S/T] chunks
   int *esrc = nullptr;  // per value slot ((g*S+s)*EM+e)*32+j: lu index or -1
   int *dsrc = nullptr;  // per divisor slot (g*S+s)*32+j: lu index or -1
   long long nslots = 0, ndslots = 0;

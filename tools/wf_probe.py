@@ -36,7 +36,12 @@ _lib.check(L.mpk_csr_upload(ctx, ctypes.c_int64(n), ctypes.c_int64(nnz), _lib.dp
 bad = ctypes.c_int64(); st = ctypes.c_int32()
 _lib.check(L.mpk_ilu0_factor(h, ctypes.byref(bad), ctypes.byref(st)))
 ms = ctypes.c_double()
-_lib.check(L.mpk_bench_apply(h, ctypes.c_int(2), ctypes.c_int(3), ctypes.byref(ms)))
+L.mpk_wf_debug3(None, ctypes.c_int(1))
+_lib.check(L.mpk_bench_apply(h, ctypes.c_int(2), ctypes.c_int(1), ctypes.byref(ms)))
+sl = np.zeros(8192, np.int32)
+L.mpk_wf_debug3(sl.ctypes.data_as(ctypes.c_void_p), ctypes.c_int(0))
+sb, sd = sl & 0xffff, sl >> 16
+print("slow-path steps per group: staged-not-ready (fwd, bwd totals)", sb[:64].sum(), sb[64:128].sum(), "; division test failed", sd[:128].sum())
 print(name, "apply ms", ms.value)
 buf = np.zeros(2 * 8192, np.int64)
 L.mpk_wf_debug(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int(len(buf)))
@@ -56,9 +61,14 @@ for lo, hi, tag in ((0, half, "fwd"), (half, ng, "bwd")):
 
 b2 = np.zeros(4096, np.int64)
 L.mpk_wf_debug2(b2.ctypes.data_as(ctypes.c_void_p))
-q = b2[:4096].reshape(1024, 4)
-q = q[:int(np.count_nonzero(q[:, 0]))]
-seg = np.diff(q, axis=1)
-nxt = q[1:, 0] - q[:-1, 3]
-print("per-step segments (median cycles): wait", np.median(seg[:, 0]), "loads+rhs", np.median(seg[:, 1]),
-      "chain+pub", np.median(seg[:, 2]), "prefetch+sync+loop", np.median(nxt))
+m = int(np.count_nonzero(b2[:3072]))
+cb = b2[3072:].reshape(256, 4).astype(np.int64)
+st = b2[:m]
+# chunk c boundary: last step stamp of chunk c-1 (t=7) -> cb[c,0..3] -> step stamp c*8
+rows = []
+for c in range(2, min(200, m // 8 - 1)):
+    rows.append([cb[c, 0] - st[c * 8 - 1], cb[c, 1] - cb[c, 0], cb[c, 2] - cb[c, 1], cb[c, 3] - cb[c, 2], st[c * 8] - cb[c, 3]])
+print("chunk boundary median cycles [t7 body+refill, rec_wait, deps_issue, rhs_issue, wait_group]:", np.median(np.array(rows), axis=0))
+d = np.diff(b2[:m])
+print("group0 step cycles: n", m, "median", np.median(d), "mean", round(d.mean(), 1))
+print("  by t%8:", [int(np.median(d[t::8])) for t in range(8)])
