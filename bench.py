@@ -396,6 +396,101 @@ def run_ours(args, rank, world, local_rank):
     }
 
 
+def run_sharded(args, rank, world, local_rank):
+    """cfg4 over N GPUs: ONE system, row-block sharded BiCGSTAB (csrc/shard.cuh;
+    SpMV / vector rows split, ILU(0) sweeps in full on every rank, NCCL
+    all-gathers of partials and sweep inputs).  value = that system's
+    iterations / device time (max over ranks) -> strong scaling."""
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    import paper_2504_14498_b200 as mpk
+    from paper_2504_14498_b200 import _lib, problems
+    from paper_2504_14498_b200.sharded import Communicator, ShardedSolver
+
+    L = _lib.lib()
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        comm = Communicator.nccl(local_rank)
+    else:
+        comm = Communicator.local(1)[0]
+    p = problems.CONFIGS[args.config]()
+    P = mpk.Precision.DD
+    A = mpk.CsrMatrix.from_binary64(p.n, p.row_ptr, p.col_idx, p.val_re, None, P)
+    sv = ShardedSolver(A, P, comm, local_rank)
+    k = 2
+    # b = A*1 in working precision (problems: b64 None -> x_true = ones)
+    xt = mpk.DenseVector.from_float64(np.real(p.x_true) if p.x_true is not None
+                                      else np.ones(p.n), P)
+    b = mpk.spmv_mixed(A.demoted(), xt) if p.b64 is None else \
+        mpk.DenseVector.from_float64(np.real(p.b64), P)
+    b_pin = torch.empty((p.n, k), dtype=torch.float64, pin_memory=True).numpy()
+    b_pin[:] = b.re
+    x_pin = torch.empty((p.n, k), dtype=torch.float64, pin_memory=True).numpy()
+    sv.load_b(b)
+    max_iter = p.max_iter if p.max_iter is not None else 3 * p.n
+    stream = torch.cuda.ExternalStream(L.mpk_ctx_stream(sv.ctx), device=local_rank)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            tdist.barrier()
+
+    iters = launches = 0
+    with Clocks(local_rank) as clk:
+        for _ in range(args.warmup):
+            sv.solve_dev(p.eps_rel, p.eps_abs, max_iter)
+        barrier()
+        clk.samples.clear()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            rep = sv.solve_dev(p.eps_rel, p.eps_abs, max_iter)
+            iters += int(rep.iterations)
+            launches += int(rep.launches)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    # e2e: pinned host b in, x out, every step
+    barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    e2e_iters = 0
+    for _ in range(args.steps):
+        _lib.check(L.mpk_to_planar(sv.ctx, ctypes.c_int64(p.n), ctypes.c_int(k),
+                                   _lib.dptr(b_pin), None,
+                                   ctypes.c_void_p(sv.d_b.data_ptr())), "to_planar")
+        rep = sv.solve_dev(p.eps_rel, p.eps_abs, max_iter)
+        _lib.check(L.mpk_from_planar(sv.ctx, ctypes.c_int64(p.n), ctypes.c_int(k),
+                                     ctypes.c_void_p(sv.d_x.data_ptr()), _lib.dptr(x_pin),
+                                     None, ctypes.c_int(0)), "from_planar")
+        e2e_iters += int(rep.iterations)
+    e3.record(stream)
+    barrier()
+    e2e_ms = e2.elapsed_time(e3)
+    avg = ctypes.c_double(0)
+    _lib.check(L.mpk_bench_apply(sv.m, ctypes.c_int(k), ctypes.c_int(5), ctypes.byref(avg)),
+               "bench_apply")
+
+    class _C:  # probe record shaped like bench Cell
+        pass
+
+    cell = _C()
+    cell.p = p
+    vals = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        tdist.all_reduce(vals, op=tdist.ReduceOp.MAX)
+    ms, e2e_ms = float(vals[0]), float(vals[1])
+    comm.close()
+    return {"ms": ms, "e2e_ms": e2e_ms, "iters": float(iters), "e2e_iters": float(e2e_iters),
+            "launches": launches, "h2d": 8 * k * p.n * world, "d2h": 8 * k * p.n * world,
+            "clocks": clk.summary(), "probe": [(cell, avg.value)], "cells": [],
+            "sharded": True}
+
+
 def cpu_baseline_sample(config: str):
     """The reference restated in C (oracle/, kind "port") on a bounded
     sample of the same workload: BiCGSTAB TD and QD full solves of cfg2."""
@@ -500,6 +595,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="cfg4: the row-block sharded path also at N=1")
     ap.add_argument("--serial", dest="concurrent", action="store_false",
                     help="run the cells of a step one after another")
     args = ap.parse_args()
@@ -519,7 +616,10 @@ def main():
 
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    res = run_ours(args, rank, world, local_rank)
+    if args.config == "cfg4" and (world > 1 or args.shard):
+        res = run_sharded(args, rank, world, local_rank)
+    else:
+        res = run_ours(args, rank, world, local_rank)
     if rank != 0:
         if world > 1:
             import torch.distributed as tdist
@@ -544,7 +644,8 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if res.get("sharded") else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE.json generators, DESIGN.md)",
         "config": config_dict(args),
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(res["h2d"]),
@@ -557,8 +658,11 @@ def main():
                      "algorithmic_bytes": bytes_apply, "avg_ms": apply_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if PEAKS.exists()
                      else "fallback B200_PROFILING.md"},
-        "iterations_per_step": res["iters"] / args.steps / world,
+        "iterations_per_step": res["iters"] / args.steps / (1 if res.get("sharded") else world),
     }
+    if res.get("sharded"):
+        out["config"]["parallelism"] = (f"one system, rows sharded over {world} GPU(s); "
+                                        "ILU(0) sweeps replicated; NCCL all-gathers")
     if world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline_sample(args.config)

@@ -204,6 +204,36 @@ int mpk_solve_batch(int nsys, mpk_matrix **ms, int method, int k,
                     const double *const *b_re, double *const *x_re,
                     mpk_report *reps);
 
+/* Row-block sharded solve (BASELINE cfg4 at 1/2/4/8 GPUs).
+ * The reference has no multi-process path (solvers.py is single-threaded);
+ * this is the B200 extension of solve() (solvers.py:418-453) for one system
+ * over W GPUs.  Every rank uploads and factors the whole matrix and runs the
+ * ILU(0) sweeps in full (the triangular solve does not shard); SpMV rows,
+ * vector updates and reduction partials run on the rank's block of
+ * ceil(n/W) rows (W*ceil(n/W) <= mpk_plane_ld(n)).  Exchanges: in-place
+ * all-gathers of the reduction block partials and of the sweep inputs'
+ * head planes; the finalize folds all partials in one fixed order, so
+ * every rank takes the same decisions.  b_dev/x_dev/hist_dev as in
+ * mpk_solve_dev (x complete on every rank on return).  BiCGSTAB, tree
+ * reductions. */
+typedef struct mpk_comm mpk_comm;
+/* ncclUniqueId (128 bytes) for rank 0 to broadcast (torch.distributed) */
+int mpk_comm_unique_id(void *id128);
+/* NCCL communicator over W processes (one GPU each) */
+int mpk_comm_create(int device, int rank, int world, const void *id128,
+                    mpk_comm **out);
+/* W virtual ranks in ONE process on one device (tests): out[0..W-1]; each
+ * rank's solve must run on its own host thread (device copies + events,
+ * host barrier between the ranks' enqueues; no cross-rank kernel waits) */
+int mpk_comm_create_local(int world, mpk_comm **out);
+void mpk_comm_destroy(mpk_comm *c);
+int mpk_comm_rank(const mpk_comm *c);
+int mpk_comm_world(const mpk_comm *c);
+int mpk_solve_dev_sharded(mpk_matrix *m, mpk_comm *comm, int method, int k,
+                          double eps_rel, double eps_abs, int64_t max_iter,
+                          const double *b_dev, double *x_dev, double *hist_dev,
+                          int64_t hist_cap, mpk_report *rep);
+
 #ifdef __cplusplus
 }
 #endif

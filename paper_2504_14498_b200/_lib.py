@@ -48,6 +48,8 @@ EXPORTS = (
     "mpk_mc_host", "mpk_solve", "mpk_plane_ld", "mpk_solve_dev", "mpk_to_planar",
     "mpk_from_planar", "mpk_solve_batch", "mpk_ctx_stream", "mpk_bench_apply",
     "mpk_csr_set_values", "mpk_run_jobs", "mpk_ctx_set_option",
+    "mpk_comm_unique_id", "mpk_comm_create", "mpk_comm_create_local", "mpk_comm_destroy",
+    "mpk_comm_rank", "mpk_comm_world", "mpk_solve_dev_sharded",
 )
 
 MPK_OPT_REDUCTION = 1

@@ -1471,7 +1471,7 @@ int mpk_bench_apply(mpk_matrix *m, int k, int reps, double *ms_avg) {
 static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
                       double eps_abs, int64_t max_iter, const double *d_b,
                       double *d_x, double *d_hist, int64_t hist_cap,
-                      mpk_report *rep) {
+                      mpk_report *rep, Exchange *ex = nullptr) {
   std::memset(rep, 0, sizeof(*rep));
   rep->final_recursive_relres = NAN;
   rep->true_relres = NAN;
@@ -1508,6 +1508,7 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   p.precond_ilu = 1;
   p.hist_cap = hist_cap;
   p.reduce_seq = m->ctx->reduce_seq;
+  p.ex = ex;
   SolveOut o{};
   char eb[256] = {0};
   rc = run_solve(m->A, p, d_b, d_x, d_hist, &o, m->ctx->stream, eb);
@@ -1537,6 +1538,66 @@ int mpk_solve_dev(mpk_matrix *m, int method, int k, double eps_rel,
             tl_phase[1] - tl_phase[0], tl_phase[2] - tl_phase[1],
             tl_phase[3] - tl_phase[2], tl_phase[4] - tl_phase[3],
             host_ms() - tl_phase[4]);
+  return rc;
+}
+
+// ---- row-block sharded solve (shard.cuh) ----
+struct mpk_comm {
+  Exchange *ex = nullptr;
+};
+
+int mpk_comm_unique_id(void *id128) {
+  char eb[256] = {0};
+  if (nccl_unique_id(id128, eb)) return fail(MPK_CUDA_ERROR, eb);
+  return MPK_OK;
+}
+
+int mpk_comm_create(int device, int rank, int world, const void *id128,
+                    mpk_comm **out) {
+  if (world < 1 || rank < 0 || rank >= world || !out)
+    return fail(MPK_INVALID, "bad rank / world");
+  char eb[256] = {0};
+  Exchange *ex = make_nccl_exchange(device, rank, world, id128, eb);
+  if (!ex) return fail(MPK_CUDA_ERROR, eb);
+  *out = new mpk_comm{ex};
+  return MPK_OK;
+}
+
+int mpk_comm_create_local(int world, mpk_comm **out) {
+  if (world < 1 || !out) return fail(MPK_INVALID, "bad world");
+  std::vector<Exchange *> ex(world);
+  if (make_local_exchanges(world, ex.data())) return fail(MPK_CUDA_ERROR, "events");
+  for (int r = 0; r < world; ++r) out[r] = new mpk_comm{ex[r]};
+  return MPK_OK;
+}
+
+void mpk_comm_destroy(mpk_comm *c) {
+  if (!c) return;
+  delete c->ex;
+  delete c;
+}
+
+int mpk_comm_rank(const mpk_comm *c) { return c ? c->ex->rank : -1; }
+int mpk_comm_world(const mpk_comm *c) { return c ? c->ex->world : -1; }
+
+int mpk_solve_dev_sharded(mpk_matrix *m, mpk_comm *comm, int method, int k,
+                          double eps_rel, double eps_abs, int64_t max_iter,
+                          const double *b_dev, double *x_dev, double *hist_dev,
+                          int64_t hist_cap, mpk_report *rep) {
+  if (!comm) return fail(MPK_INVALID, "null communicator");
+  if (method != MPK_BICGSTAB)
+    return fail(MPK_INVALID, "sharded solve: BiCGSTAB only");
+  if (m->ctx->reduce_seq)
+    return fail(MPK_INVALID, "sharded solve: tree reductions only");
+  const auto t0 = std::chrono::steady_clock::now();
+  const long long l0 = tl_launches;
+  CKR(cudaSetDevice(m->ctx->device));
+  int rc = solve_core(m, method, k, eps_rel, eps_abs, max_iter, b_dev, x_dev,
+                      hist_dev, hist_cap, rep, comm->ex);
+  rep->total_ms = std::chrono::duration<double, std::milli>(
+                      std::chrono::steady_clock::now() - t0)
+                      .count();
+  rep->launches = tl_launches - l0;
   return rc;
 }
 

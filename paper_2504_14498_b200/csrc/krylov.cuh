@@ -7,6 +7,7 @@
 
 #include "common.cuh"
 #include "ilu.cuh"
+#include "shard.cuh"
 
 namespace mpk {
 
@@ -106,6 +107,7 @@ struct SolveParams {
   int precond_ilu;  // 1: ILU(0)-mixed, 0: identity
   long long hist_cap;
   int reduce_seq;   // 1: sequential-order (bit-identical twin) reductions
+  Exchange *ex = nullptr;  // row-block sharded solve (shard.cuh), else null
 };
 
 struct SolveOut {

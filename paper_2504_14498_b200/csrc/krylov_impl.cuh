@@ -160,6 +160,9 @@ struct Solver : PlanBase {
   int n;
   long long ld;
   int G;
+  // row-block sharding (p.ex): rows [r0, r1) of blocks of nb, Gl blocks
+  long long r0 = 0, r1 = 0, nb = 0;
+  int gl = 0;
   State *S = nullptr;
   double *part = nullptr;
   double *hist = nullptr;
@@ -203,6 +206,21 @@ struct Solver : PlanBase {
     ld = plane_ld(n);
     // twin mode: element terms + ascending chains; finalize over 1 partial
     G = p.reduce_seq ? 1 : grid_for(n);
+    if (p.ex) {  // row-block sharded (shard.cuh): W ranks x Gl blocks
+      const int W = p.ex->world;
+      gl = kMaxGrid / W;
+      G = W * gl;
+      nb = (n + W - 1) / W;
+      r0 = (long long)p.ex->rank * nb;
+      r1 = r0 + nb < n ? r0 + nb : n;
+      if (r0 > n) r0 = n;
+      if ((long long)W * nb > ld || p.reduce_seq || p.method != kBiCGSTAB) {
+        ok = false;
+        snprintf(errbuf, 256,
+                 "sharded solve: BiCGSTAB with tree reductions and W*ceil(n/W) <= "
+                 "plane_ld(n) only");
+      }
+    }
     if (p.reduce_seq)
       seqbuf = (double *)dalloc(sizeof(double) * 8 * 2 * K * (size_t)(n > 0 ? n : 1));
     da = DA{A.n, A.rp, A.ci, A.val, A.at_rp, A.at_ci, A.at_val};
@@ -267,7 +285,20 @@ struct Solver : PlanBase {
   // ILU(0)-mixed apply: z = promote(U^-1 L^-1 demote(in)).
   void sweep(const double *in_re, const double *in_im, double *y, double *z,
              bool adjoint, int which, bool after_loop = false) {
+    if (p.ex) {
+      // every rank sweeps the whole vector: gather the demoted input's rows
+      // and reset all sentinels (the row kernels only touched own rows)
+      p.ex->allgather_inplace(const_cast<double *>(in_re), (size_t)nb, st);
+      if (in_im) p.ex->allgather_inplace(const_cast<double *>(in_im), (size_t)nb, st);
+      launch_sweep_reset(y, z, n, CX, after_loop ? nullptr : done, st);
+    }
     sweep_on(st, in_re, in_im, y, z, adjoint, which, after_loop);
+  }
+  // all planes of an MC vector complete on every rank (sharded solve)
+  void gather_mc(double *v) {
+    if (!p.ex) return;
+    for (int c = 0; c < K * (CX ? 2 : 1); ++c)
+      p.ex->allgather_inplace(v + (size_t)c * ld, (size_t)nb, st);
   }
   void sweep_on(cudaStream_t s_, const double *in_re, const double *in_im,
                 double *y, double *z, bool adjoint, int which,
@@ -1110,6 +1141,7 @@ struct Solver : PlanBase {
       promote(x, d_x);
       return;
     }
+    gather_mc(x);
     cudaMemcpyAsync(d_x, x, sizeof(double) * planes * ld,
                     cudaMemcpyDeviceToDevice, st);
   }
@@ -1167,7 +1199,8 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   const char *nocond = getenv("MPK_NO_COND_GRAPH");
   const bool use_cond = !nocond || nocond[0] == '0';
   // plan cache: one workspace + graph per (method, K, field) on this matrix
-  const int key = p.reduce_seq * 1000 + p.method * 100 + K * 10 + (CX ? 1 : 0);
+  const int key = (p.ex ? 100000 * p.ex->world : 0) + p.reduce_seq * 1000 +
+                  p.method * 100 + K * 10 + (CX ? 1 : 0);
   Solver<K, CX> *sv = nullptr;
   auto it = A.plans.find(key);
   if (it != A.plans.end()) {
@@ -1195,6 +1228,19 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
     explicit SeqScope(double *s) { tl_seq = s; }
     ~SeqScope() { tl_seq = nullptr; }
   } seq_scope(sv->seqbuf);
+  struct ShardScope {  // row kernels of a sharded solve cover the own rows
+    explicit ShardScope(const Solver<K, CX> *v) {
+      if (v->p.ex) {
+        tl_shard.ex = v->p.ex;
+        tl_shard.r0 = v->r0;
+        tl_shard.r1 = v->r1;
+        tl_shard.gl = v->gl;
+        tl_shard.boff = v->p.ex->rank * v->gl;
+      }
+    }
+    ~ShardScope() { tl_shard = ShardCtx{}; }
+  } shard_scope(sv);
+  const bool sharded = p.ex != nullptr;
   const long long launches0 = tl_launches;
   State hs{};
   hs.max_iter = p.max_iter;
@@ -1211,7 +1257,7 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   sv->setup();
   CK(cudaGetLastError());
 
-  if (!sv->ge) {
+  if (!sv->ge && !sharded) {
     if (use_cond) {
       // one iteration -> body of a device-side WHILE conditional node
       CK(cudaGraphCreate(&sv->g, 0));
@@ -1254,7 +1300,24 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
     CK(cudaGraphInstantiate(&sv->ge, sv->g, 0));
   }
   tl_phase[2] = host_ms();  // setup enqueued, graph ready
-  if (use_cond) {
+  if (sharded) {
+    // eager iterations (the exchanges are host-enqueued collectives); the
+    // ranks compute identical stop decisions, so they leave together
+    // (the device decides the stop, incl. max_iter, one body after the last
+    // iteration: BiCGSTAB's norm test is deferred into the next body)
+    long long launched = 0;
+    const long long cap = p.max_iter + 8;
+    int chunk = 4;
+    State probe{};
+    while (launched < cap) {
+      for (int c = 0; c < chunk && launched < cap; ++c, ++launched) sv->iter();
+      CK(cudaMemcpyAsync(sv->hp + 1, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      probe = sv->hp[1];
+      if (probe.done) break;
+      if (chunk < 16) chunk *= 2;
+    }
+  } else if (use_cond) {
     CK(cudaGraphLaunch(sv->ge, st));
     tl_launches += 1;  // the init node; body nodes counted per run below
   } else {
@@ -1278,7 +1341,7 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   CK(cudaStreamSynchronize(st));
   hs = *sv->hp;
   tl_phase[3] = host_ms();  // loop done (synchronised)
-  if (use_cond) tl_launches += sv->body_nodes * hs.body_runs;
+  if (use_cond && !sharded) tl_launches += sv->body_nodes * hs.body_runs;
   if (!hs.done) {
     // loop ran out without a device-side stop (max_iter reached)
     hs.iterations = p.max_iter;

@@ -100,7 +100,7 @@ struct Red {
 template <int K, bool CX, int NH, int NN, class F>
 __global__ void __launch_bounds__(kBlock, MPK_ROWS_MIN_BLOCKS)
     rows_kernel(long long n_total, long long n, const int *done, double *part,
-                double *seq, F f) {
+                double *seq, F f, long long i0) {
   // n_total = roles * n: element i of role r is index r * n + i; only role 0
   // (i < n) contributes to the reductions
   if (done && *done) return;
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kBlock, MPK_ROWS_MIN_BLOCKS)
       for (int s = 0; s < NN; ++s)
         red.nr[s].seq = own ? seq + ((size_t)(NH + s) * n + i) * 2 * K : nullptr;
     }
-    f(i, red);
+    f(i0 + i, red);
   }
   if constexpr (NH + NN > 0)
     if (!seq) red.store(part, smem);
@@ -192,15 +192,29 @@ inline void prefer_max_smem(KFn kfn) {
 
 // roles > 1: the kernel runs roles * n threads; f(i) with i >= n does the
 // independent part of element i % n assigned to role i / n (see callers)
+//
+// Row-block sharded solve (shard.cuh, tl_shard set): the kernel covers the
+// rank's rows [r0, r1) with Gl blocks whose partials land at blocks
+// [boff, boff+Gl) of every slot, then each reduction slot is all-gathered
+// in place so that every rank folds the same W*Gl partials.
 template <int K, bool CX, int NH, int NN, class F>
 void rows(long long n, const int *done, double *part, cudaStream_t st, F f,
           int roles = 1) {
   ++tl_launches;
   prefer_max_smem(rows_kernel<K, CX, NH, NN, F>);
   double *seq = (NH + NN > 0) ? tl_seq : nullptr;
+  const ShardCtx &sh = tl_shard;
+  if (sh.ex && roles == 1 && !seq) {
+    const long long nl = sh.r1 - sh.r0;
+    rows_kernel<K, CX, NH, NN, F><<<sh.gl, kBlock, 0, st>>>(
+        nl, nl, done, part + (size_t)sh.boff * 8, nullptr, f, sh.r0);
+    for (int s = 0; s < NH + NN; ++s)
+      sh.ex->allgather_inplace(part + (size_t)s * kMaxGrid * 8, (size_t)sh.gl * 8, st);
+    return;
+  }
   const long long nt = n * roles;
   rows_kernel<K, CX, NH, NN, F><<<grid_for(nt), kBlock, 0, st>>>(nt, n, done, part,
-                                                                  seq, f);
+                                                                  seq, f, 0);
   if (seq) {
     ++tl_launches;
     constexpr int chains = NH * (CX ? 2 : 1) + NN;

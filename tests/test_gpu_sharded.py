@@ -1,0 +1,100 @@
+"""Row-block sharded BiCGSTAB (csrc/shard.cuh, BASELINE cfg4's multi-GPU
+mode) on ONE GPU: W virtual ranks in this process (each on its own thread
+and stream; the all-gathers are device copies ordered by events, no kernel
+waits on another rank's kernel).  Every rank must take the same decisions
+(iteration count, residual history bit for bit across ranks) and agree
+with the single-GPU solve within the north-star DD bound (the partial
+blocks differ: W*Gl instead of one grid, so the tree differs in rounding)."""
+
+from __future__ import annotations
+
+import ctypes
+import fractions
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _system(m=64):
+    import paper_2504_14498_b200 as mpk
+    from paper_2504_14498_b200 import problems
+
+    rp, ci, v = problems.convdiff9(m, 5.0)[:3]
+    n = m * m
+    P = mpk.Precision.DD
+    A = mpk.CsrMatrix.from_binary64(n, rp, ci, v, None, P)
+    b = mpk.spmv_mixed(A.demoted(), mpk.DenseVector.from_float64(np.ones(n), P))
+    cfg = mpk.SolverConfig(method="bicgstab", precision=P, precond=mpk.PrecondMode.ILU0_MIXED,
+                           spmv_mode="mixed", eps_rel=1e-20, max_iter=400)
+    return A, b, cfg
+
+
+def _dev(h, h0):
+    F = fractions.Fraction
+    r0 = F(h0[0][0]) + F(h0[0][1])
+    return max(float(abs(F(a[0]) + F(a[1]) - F(o[0]) - F(o[1])) / r0)
+               for a, o in zip(h[:41], h0[:41]))
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_sharded_virtual_ranks_match_single(world):
+    import paper_2504_14498_b200 as mpk
+    from paper_2504_14498_b200.sharded import Communicator, solve_sharded
+
+    A, b, cfg = _system()
+    single = mpk.solve(A, b, cfg)
+    comms = Communicator.local(world)
+    out = [None] * world
+    err = []
+
+    def run(r):
+        try:
+            out[r] = solve_sharded(A, b, cfg, comms[r])
+        except Exception as e:  # surfaced below
+            err.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for c in comms:
+        c.close()
+    assert not err, err
+    for rep in out:
+        assert rep.converged and rep.iterations == single.iterations
+        assert rep.true_relres <= 1e-20
+        # ranks agree bit for bit (same partials, same fold order)
+        assert np.array_equal(np.asarray(rep.history), np.asarray(out[0].history))
+        assert np.array_equal(rep.x.re, out[0].x.re)
+    assert _dev(out[0].history, single.history) <= 1e-25
+
+
+def test_sharded_nccl_world1_and_bad_shapes():
+    """The NCCL communicator path at world 1 (libnccl resolved at run time),
+    and the shape / method checks of the sharded entry point."""
+    import paper_2504_14498_b200 as mpk
+    from paper_2504_14498_b200 import _lib
+    from paper_2504_14498_b200.sharded import Communicator, check_shardable, solve_sharded
+
+    L = _lib.lib()
+    idb = (ctypes.c_char * 128)()
+    _lib.check(L.mpk_comm_unique_id(idb))
+    h = ctypes.c_void_p()
+    _lib.check(L.mpk_comm_create(ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(1), idb,
+                                 ctypes.byref(h)))
+    comm = Communicator(h)
+    assert comm.rank == 0 and comm.world == 1
+    A, b, cfg = _system(32)
+    rep = solve_sharded(A, b, cfg, comm)
+    single = mpk.solve(A, b, cfg)
+    assert rep.iterations == single.iterations and rep.converged
+    with pytest.raises(NotImplementedError):
+        solve_sharded(A, b, mpk.SolverConfig(method="cgs", precision=cfg.precision,
+                                             precond=cfg.precond, spmv_mode="mixed"), comm)
+    comm.close()
+    with pytest.raises(ValueError):
+        check_shardable(32, 3)  # 3 * 11 = 33 rows > plane stride 32

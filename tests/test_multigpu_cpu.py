@@ -84,3 +84,89 @@ def test_gloo_two_ranks_shard_and_gather(orc):
         assert p.exitcode == 0
     serial = [_solve(s) for s in _systems()]
     assert merged == serial
+
+
+# ---------------------------------------------------------------------------
+# row-block sharded solve (csrc/shard.cuh, paper_2504_14498_b200/sharded.py):
+# the partition and the two in-place all-gather layouts it relies on, run
+# with gloo over 2 ranks.  Each rank fills ITS row block / partial blocks
+# exactly like the device kernels (rows [r*nb, (r+1)*nb), partial blocks
+# [r*Gl, (r+1)*Gl) of every slot) and all-gathers in place; afterwards every
+# rank must hold the single-process arrays.
+# ---------------------------------------------------------------------------
+def test_row_blocks_and_partial_blocks():
+    from paper_2504_14498_b200.sharded import KMAXGRID, blocks_per_rank, row_blocks
+
+    for n in (1, 7, 4096, 4194304):
+        for w in (1, 2, 4, 8):
+            nb, blk = row_blocks(n, w)
+            rows = [i for r0, r1 in blk for i in range(r0, r1)]
+            assert rows == list(range(n)) and w * nb >= n
+            assert w * blocks_per_rank(w) <= KMAXGRID
+
+
+def _sharded_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_14498_b200.sharded import KMAXGRID, blocks_per_rank, row_blocks
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 1000
+    nb, blk = row_blocks(n, world)
+    r0, r1 = blk[rank]
+    rng = np.random.default_rng(0)
+    full = rng.standard_normal(world * nb)  # the head plane every rank needs
+    plane = np.full(world * nb, np.nan)
+    plane[r0:r1] = full[r0:r1]
+    # in-place all-gather of rank ranges (NCCL: recvbuf = plane, send = own range)
+    chunks = [torch.empty(nb, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(chunks, torch.from_numpy(plane[rank * nb:(rank + 1) * nb].copy()))
+    gathered = torch.cat(chunks).numpy()
+    # reduction partials: slot-major [slot][KMAXGRID][8]; rank owns blocks
+    gl = blocks_per_rank(world)
+    part = np.zeros((2, KMAXGRID, 8))
+    for s in range(2):
+        for g in range(gl):
+            part[s, rank * gl + g, :] = 100 * s + rank * gl + g
+    for s in range(2):
+        flat = part[s].reshape(-1)
+        cnk = [torch.empty(gl * 8, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(cnk, torch.from_numpy(flat[rank * gl * 8:(rank + 1) * gl * 8].copy()))
+        flat[: world * gl * 8] = torch.cat(cnk).numpy()
+    if rank == 0:
+        q.put((gathered[:n].tolist(), part.tolist()))
+    else:
+        q.put(None)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_sharded_exchange_layout():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    got = [r for r in res if r is not None][0]
+    from paper_2504_14498_b200.sharded import KMAXGRID, blocks_per_rank, row_blocks
+
+    nb, _ = row_blocks(1000, 2)
+    full = np.random.default_rng(0).standard_normal(2 * nb)
+    assert np.array_equal(np.asarray(got[0]), full[:1000])
+    part = np.asarray(got[1])
+    gl = blocks_per_rank(2)
+    for s in range(2):
+        assert np.array_equal(part[s, : 2 * gl, 0], 100 * s + np.arange(2 * gl))
