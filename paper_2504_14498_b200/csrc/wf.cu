@@ -123,6 +123,12 @@ __device__ __forceinline__ void wf_mulsub(double &ar, double &ai, double lr,
 
 __device__ long long wf_dbg2[4096];  // clock64 per step of group 0 (dbg 2)
 __device__ int wf_dbg3[8192];        // slow-path steps per group (dbg)
+__device__ long long wf_dbg4[4096];  // clock per step of group 1 (dbg 2)
+__device__ __forceinline__ long long wf_gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // a / d on the critical path of a backward row: reciprocal (independent of
 // a, off the chain) + Markstein correction, then an exact residual test
@@ -131,8 +137,8 @@ __device__ int wf_dbg3[8192];        // slow-path steps per group (dbg)
 // i.e. |e| < |d| * ulp(q)/2 (ties cannot occur in this range).  Outside
 // the safe exponent range, for q a power of two (asymmetric ulp) or when
 // the test fails, ok = false and the caller divides with __ddiv_rn.
-__device__ __forceinline__ double wf_fast_div(double a, double d, bool &ok) {
-  const double r = __drcp_rn(d);
+__device__ __forceinline__ double wf_fast_div(double a, double d, double r, bool &ok) {
+  // r = __drcp_rn(d), precomputed per factorization (wf_gather_kernel)
   const double q0 = __dmul_rn(a, r);
   const double e0 = fma(-q0, d, a);
   const double q1 = fma(e0, r, q0);
@@ -238,8 +244,40 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
   // cp.async of chunk c's remote dependency values (one commit group per
   // chunk, maybe empty): the chunk's fetch table spreads them over the 32
   // lanes ({global row, shared offset} items, row -1 = none)
+  // Register path (kmax <= kWfRegItems): the items of chunk c are LOADED at
+  // the top of chunk c-1 with L1-bypassing relaxed loads (an L1-cached copy
+  // of the line, fetched while neighbouring values were still sentinels,
+  // would keep re-serving the sentinel) and stored to their stage slots at
+  // the top of chunk c.  The cp.async group of the chunk is then empty.
+  constexpr int kWfRegItems = 4;
+  const bool regpath = P.kmax <= kWfRegItems;
+  double dvr[kWfRegItems], dvi[kWfRegItems];
+  int dvo[kWfRegItems];
+  auto deps_load = [&](int c) {
+#pragma unroll
+    for (int r = 0; r < kWfRegItems; ++r) {
+      dvo[r] = -1;
+      if (c < nch && r < P.kmax) {
+        const int2 it = reinterpret_cast<const int2 *>(
+            buf + (size_t)(c % kWfNB) * bufsz + (size_t)kWfT * rs)[r * 32 + j];
+        if (it.x >= 0) {
+          dvo[r] = it.y;
+          wf_ld<CX>(glob, it.x, dvr[r], dvi[r]);
+        }
+      }
+    }
+  };
+  auto deps_store = [&]() {
+#pragma unroll
+    for (int r = 0; r < kWfRegItems; ++r)
+      if (dvo[r] >= 0) {
+        double *d = reinterpret_cast<double *>(wbase + dvo[r]);
+        d[0] = dvr[r];
+        if constexpr (CX) d[1] = dvi[r];
+      }
+  };
   auto deps_issue = [&](int c) {
-    if (c < nch) {
+    if (c < nch && !regpath) {
       const int2 *ft = reinterpret_cast<const int2 *>(
           buf + (size_t)(c % kWfNB) * bufsz + (size_t)kWfT * rs);
       for (int r = 0; r < P.kmax; ++r) {
@@ -311,10 +349,15 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
   rhs_issue(1);
   rhs_issue(2);
   load_rec(0);
+  if (regpath) deps_load(0);
   const bool dbc = dbgstep && j == 0;
   for (int c = 0; c < nch; ++c) {
     if (dbc && c < 256) wf_dbg2[3072 + 4 * c] = clock64();
     rec_wait(c + 1);
+    if (regpath) {
+      deps_store();     // chunk c's remote values (loaded one chunk ago)
+      deps_load(c + 1);
+    }
     if (dbc && c < 256) wf_dbg2[3072 + 4 * c + 1] = clock64();
     deps_issue(c + 1);
     if (dbc && c < 256) wf_dbg2[3072 + 4 * c + 2] = clock64();
@@ -324,7 +367,8 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
 #pragma unroll
     for (int t = 0; t < kWfT; ++t) {
       const int s = c * kWfT + t;
-      if (dbgstep && j == 0 && s < 3072) wf_dbg2[s] = clock64();
+      if (dbgstep && j == 0 && s < 3072) wf_dbg2[s] = wf_gtime();
+      if (dbgcnt && dbgg == 1 && j == 0 && s < 3072) wf_dbg4[s] = wf_gtime();
       const int pp = p0 + s;
       const bool act = (unsigned)(s + pos0) < (unsigned)Lc && pp < n;
       double vr[kWfEM], vi[kWfEM], cl[kWfEM], cm[kWfEM];
@@ -352,12 +396,13 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
         ai = CX ? rh1[0] : 0.0;
         if (!FWD) bad |= wf_sent<CX>(ar, ai);
       }
-      double dr = 0.0, di = 0.0;
+      double dr = 0.0, di = 0.0, drc = 0.0;
       if constexpr (!FWD) {
         const double *dv =
             reinterpret_cast<const double *>(recp(s) + Lt::kValOff + Lt::kVal);
         dr = dv[j * VW];
         di = CX ? dv[j * VW + 1] : 0.0;
+        if constexpr (!CX) drc = dv[32 + j];  // reciprocal block follows
       }
       if (s + 1 < S) load_rec(s + 1);  // read ahead
       // common path: the chain on the staged values (no branch before it)
@@ -373,7 +418,7 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
           xi = qi;
         } else {
           bool ok;
-          xr = wf_fast_div(xr, dr, ok);
+          xr = wf_fast_div(xr, dr, drc, ok);
           slow |= act && !ok;
         }
       }
@@ -429,11 +474,6 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
 // diagnostics (MPK_WF_DEBUG=1): globaltimer at start / end of every group
 __device__ long long wf_dbg[2 * 8192];
 
-__device__ __forceinline__ long long wf_gtime() {
-  long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 template <bool CX>
 __global__ void __launch_bounds__(32, 1)
@@ -499,7 +539,10 @@ __global__ void wf_gather_kernel(const double *lu, WPhase P, int cx) {
                                   : make_double2(0.0, 0.0);
       *reinterpret_cast<double2 *>(dst) = v;
     } else {
-      *reinterpret_cast<double *>(dst) = srcp >= 0 ? lu[srcp] : 0.0;
+      const double v = srcp >= 0 ? lu[srcp] : 0.0;
+      *reinterpret_cast<double *>(dst) = v;
+      if (i >= P.nslots)  // backward divisor: its RN reciprocal follows the block
+        *reinterpret_cast<double *>(dst + 32 * 8) = __drcp_rn(v);
     }
   }
 }
@@ -568,7 +611,8 @@ static bool build_phase_wf(WPhase &ph, int n, bool cx, bool fwd,
   ph.ngroups = hp.ngroups;
   ph.S = hp.S;
   ph.cost = hp.cost;
-  ph.recsz = 2 * kWfEM * 32 * 4 + kWfEM * 32 * VB + (fwd ? 0 : 32 * VB);
+  // backward: divisors [32] (+ their reciprocals [32], real field)
+  ph.recsz = 2 * kWfEM * 32 * 4 + kWfEM * 32 * VB + (fwd ? 0 : 32 * VB + (cx ? 0 : 32 * 8));
   const long long nsteps = (long long)ph.ngroups * ph.S;
   ph.nslots = nsteps * kWfEM * 32;
   ph.ndslots = fwd ? 0 : nsteps * 32;
@@ -789,6 +833,9 @@ extern "C" int mpk_wf_debug3(int *out, int reset) {
     return cudaMemcpyToSymbol(mpk::wf_dbg3, z, sizeof(z)) == cudaSuccess ? 0 : 4;
   }
   return cudaMemcpyFromSymbol(out, mpk::wf_dbg3, sizeof(int) * 8192) == cudaSuccess ? 0 : 4;
+}
+extern "C" int mpk_wf_debug4(long long *out) {
+  return cudaMemcpyFromSymbol(out, mpk::wf_dbg4, sizeof(long long) * 4096) == cudaSuccess ? 0 : 4;
 }
 extern "C" int mpk_wf_debug2(long long *out) {
   return cudaMemcpyFromSymbol(out, mpk::wf_dbg2, sizeof(long long) * 4096) == cudaSuccess ? 0 : 4;

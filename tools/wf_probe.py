@@ -72,3 +72,13 @@ print("chunk boundary median cycles [t7 body+refill, rec_wait, deps_issue, rhs_i
 d = np.diff(b2[:m])
 print("group0 step cycles: n", m, "median", np.median(d), "mean", round(d.mean(), 1))
 print("  by t%8:", [int(np.median(d[t::8])) for t in range(8)])
+
+b4 = np.zeros(4096, np.int64)
+L.mpk_wf_debug4(b4.ctypes.data_as(ctypes.c_void_p))
+g0 = b2[:2112].astype(np.float64); g1 = b4[:2112].astype(np.float64)
+if g1[100] > 0 and g0[200] > 0:
+    # consumer step x needs producer step x+63; measure time(consumer x) - time(producer x+63)
+    xs = np.arange(0, 2112 - 64, 100)
+    print("group1 step x minus group0 step x+63 (us):", [round((g1[x] - g0[x + 63]) / 1e3, 2) for x in xs])
+    tau0 = np.median(np.diff(g0[:2000])); tau1 = np.median(np.diff(g1[:2000]))
+    print("median step ns g0/g1:", tau0, tau1, " lag in steps at x=1000:", round((g1[1000] - g0[1000]) / tau0, 1))
