@@ -349,6 +349,23 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
   rhs_issue(1);
   rhs_issue(2);
   load_rec(0);
+  if (regpath && P.kmax > 0 && nch > 1) {
+    // Start at the steady-state lag: wait until every remote value of
+    // chunk 1 is published, so that from here on each chunk's values
+    // (requested one chunk ahead) are ready when requested.  Starting
+    // earlier only ends in per-step polls that overshoot the lag.
+    rec_wait(1);
+    const int2 *ft = reinterpret_cast<const int2 *>(
+        buf + (size_t)(1 % kWfNB) * bufsz + (size_t)kWfT * rs);
+    for (int r = 0; r < P.kmax; ++r) {
+      const int2 it = ft[r * 32 + j];
+      if (it.x >= 0) {
+        double vr0, vi0;
+        wf_poll<CX>(glob, it.x, vr0, vi0);
+      }
+    }
+    __syncwarp();
+  }
   if (regpath) deps_load(0);
   const bool dbc = dbgstep && j == 0;
   for (int c = 0; c < nch; ++c) {
