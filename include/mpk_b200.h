@@ -86,6 +86,14 @@ void *mpk_ctx_stream(mpk_ctx *ctx);
 #define MPK_OPT_REDUCTION 1
 #define MPK_REDUCE_TREE 0
 #define MPK_REDUCE_SEQUENTIAL 1
+/* MPK_OPT_PRECOND: the preconditioner of the solvers (SolverConfig.precond,
+ * solvers.py:64-85, _Ctx.apply solvers.py:128-136): MPK_PRECOND_ILU0_MIXED
+ * (default; binary64 ILU(0) applied to the demoted vector) or
+ * MPK_PRECOND_NONE (M = I: no factorization, the methods run on the MC
+ * vectors themselves, SpMV on MC inputs) */
+#define MPK_OPT_PRECOND 2
+#define MPK_PRECOND_NONE 0
+#define MPK_PRECOND_ILU0_MIXED 1
 int mpk_ctx_set_option(mpk_ctx *ctx, int option, int64_t value);
 
 /* CsrMatrix.demoted() upload (sparse.py:192-249): binary64 values, val_im

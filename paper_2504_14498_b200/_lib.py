@@ -54,6 +54,32 @@ EXPORTS = (
 
 MPK_OPT_REDUCTION = 1
 REDUCTION_MODE = {"tree": 0, "sequential": 1}
+MPK_OPT_PRECOND = 2  # 0: none (M = I), 1: ILU(0)-mixed (default)
+_precond_lock = threading.Lock()
+
+
+class precond_scope:
+    """Selects the solvers' preconditioner on a context for one call
+    (MPK_OPT_PRECOND) and restores ILU(0)-mixed afterwards; calls on the same
+    context are serialised while a non-default preconditioner is set."""
+
+    def __init__(self, ctx, ilu: bool):
+        self.ctx, self.ilu = ctx, ilu
+
+    def __enter__(self):
+        if not self.ilu:
+            _precond_lock.acquire()
+            check(lib().mpk_ctx_set_option(self.ctx, ctypes.c_int(MPK_OPT_PRECOND),
+                                           ctypes.c_int64(0)), "mpk_ctx_set_option")
+        return self
+
+    def __exit__(self, *exc):
+        if not self.ilu:
+            try:
+                lib().mpk_ctx_set_option(self.ctx, ctypes.c_int(MPK_OPT_PRECOND),
+                                         ctypes.c_int64(1))
+            finally:
+                _precond_lock.release()
 
 
 class MpkReport(ctypes.Structure):

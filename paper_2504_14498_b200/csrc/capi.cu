@@ -30,6 +30,7 @@ struct mpk_ctx {
   int device;
   cudaStream_t stream;
   int reduce_seq = 0;  // MPK_OPT_REDUCTION
+  int precond = 1;     // MPK_OPT_PRECOND: 1 ILU(0)-mixed, 0 none (M = I)
 };
 
 // Per-k device I/O buffers of mpk_solve, kept across calls (no
@@ -849,6 +850,11 @@ int mpk_ctx_set_option(mpk_ctx *ctx, int option, int64_t value) {
         return fail(MPK_INVALID, "reduction mode must be 0 (tree) or 1 (sequential)");
       ctx->reduce_seq = (int)value;
       return MPK_OK;
+    case MPK_OPT_PRECOND:
+      if (value != MPK_PRECOND_NONE && value != MPK_PRECOND_ILU0_MIXED)
+        return fail(MPK_INVALID, "precond must be 0 (none) or 1 (ilu0-mixed)");
+      ctx->precond = (int)value;
+      return MPK_OK;
     default:
       return fail(MPK_INVALID, "unknown option");
   }
@@ -1485,7 +1491,10 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   int64_t bad = -1;
   int32_t structural = 0;
   tl_phase[0] = host_ms();
-  int rc = mpk_ilu0_factor(m, &bad, &structural);
+  const bool ilu = m->ctx->precond != MPK_PRECOND_NONE;
+  if (!ilu && ex) return fail(MPK_INVALID, "sharded solve: ILU(0)-mixed only");
+  int rc = ilu ? mpk_ilu0_factor(m, &bad, &structural) : MPK_OK;  // M = I: no factors
+  if (!ilu) m->factor_ms = 0.f;
   tl_phase[1] = host_ms();
   if (rc == MPK_SINGULAR_PIVOT || rc == MPK_NUMERIC_BREAKDOWN) {
     rep->iterations = 0;
@@ -1505,7 +1514,7 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   p.eps_rel = eps_rel;
   p.eps_abs = eps_abs;
   p.max_iter = max_iter < 0 ? 3LL * m->A.n : max_iter;
-  p.precond_ilu = 1;
+  p.precond_ilu = ilu ? 1 : 0;
   p.hist_cap = hist_cap;
   p.reduce_seq = m->ctx->reduce_seq;
   p.ex = ex;

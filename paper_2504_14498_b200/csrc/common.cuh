@@ -144,9 +144,14 @@ struct MV {
   }
 };
 
+// F vector view: the output of an ILU(0)-mixed apply, stored as its
+// binary64 head only.  mc != 0 (preconditioner 'none', M = I): the "applied"
+// vector is a full planar MC copy (ld stride), read back unchanged.
 template <bool CX>
 struct FV {
   double *p;
+  long long ld = 0;
+  int mc = 0;
   __device__ __forceinline__ void load(int64_t i, double &re,
                                        double &im) const {
     if constexpr (CX) {
@@ -162,6 +167,14 @@ struct FV {
   template <int K>
   __device__ __forceinline__ void load_mc(int64_t i, double (&re)[K],
                                           double (&im)[K]) const {
+    if (mc) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        re[c] = p[c * ld + i];
+        im[c] = CX ? p[(K + c) * ld + i] : 0.0;
+      }
+      return;
+    }
     double r, m;
     load(i, r, m);
 #pragma unroll

@@ -163,6 +163,8 @@ struct Solver : PlanBase {
   // row-block sharding (p.ex): rows [r0, r1) of blocks of nb, Gl blocks
   long long r0 = 0, r1 = 0, nb = 0;
   int gl = 0;
+  // preconditioner 'none' (M = I): "applied" vectors are MC copies
+  int nopre = 0;
   State *S = nullptr;
   double *part = nullptr;
   double *hist = nullptr;
@@ -202,6 +204,7 @@ struct Solver : PlanBase {
 
   Solver(DMat &A_, const SolveParams &p_, cudaStream_t st_, char *eb)
       : A(A_), p(p_), st(st_), errbuf(eb) {
+    nopre = p.precond_ilu ? 0 : 1;  // before any fv() allocation
     n = A.n;
     ld = plane_ld(n);
     // twin mode: element terms + ascending chains; finalize over 1 partial
@@ -214,7 +217,8 @@ struct Solver : PlanBase {
       r0 = (long long)p.ex->rank * nb;
       r1 = r0 + nb < n ? r0 + nb : n;
       if (r0 > n) r0 = n;
-      if ((long long)W * nb > ld || p.reduce_seq || p.method != kBiCGSTAB) {
+      if ((long long)W * nb > ld || p.reduce_seq || p.method != kBiCGSTAB ||
+          !p.precond_ilu) {
         ok = false;
         snprintf(errbuf, 256,
                  "sharded solve: BiCGSTAB with tree reductions and W*ceil(n/W) <= "
@@ -278,13 +282,22 @@ struct Solver : PlanBase {
     return q;
   }
   double *mc() { return (double *)dalloc(sizeof(double) * K * (CX ? 2 : 1) * ld); }
-  double *fv() { return (double *)dalloc(sizeof(double) * (CX ? 2 : 1) * ld); }
+  // F vector (head of an ILU(0)-mixed apply); none mode: a full MC vector
+  double *fv() {
+    return (double *)dalloc(sizeof(double) * (CX ? 2 : 1) * (nopre ? K : 1) * ld);
+  }
   MVt mv(double *q) const { return MVt{q, ld}; }
-  FVt fvv(double *q) const { return FVt{q}; }
+  FVt fvv(double *q) const { return FVt{q, ld, nopre}; }
 
   // ILU(0)-mixed apply: z = promote(U^-1 L^-1 demote(in)).
   void sweep(const double *in_re, const double *in_im, double *y, double *z,
              bool adjoint, int which, bool after_loop = false) {
+    if (nopre) {  // M = I (and M^H = I): the MC vector itself
+      (void)in_im;
+      cudaMemcpyAsync(z, in_re, sizeof(double) * K * (CX ? 2 : 1) * ld,
+                      cudaMemcpyDeviceToDevice, st);
+      return;
+    }
     if (p.ex) {
       // every rank sweeps the whole vector: gather the demoted input's rows
       // and reset all sentinels (the row kernels only touched own rows)
@@ -303,6 +316,11 @@ struct Solver : PlanBase {
   void sweep_on(cudaStream_t s_, const double *in_re, const double *in_im,
                 double *y, double *z, bool adjoint, int which,
                 bool after_loop = false) {
+    if (nopre) {
+      cudaMemcpyAsync(z, in_re, sizeof(double) * K * (CX ? 2 : 1) * ld,
+                      cudaMemcpyDeviceToDevice, s_);
+      return;
+    }
     SweepArgs a{};
     a.n = n;
     a.rp = A.rp;
@@ -348,11 +366,12 @@ struct Solver : PlanBase {
     const DA a = da;
     const double *fz = fzero;
     const long long L = ld;
+    const int np_ = nopre;
     const bool two = r2_ != nullptr;
     rows<K, CX, 1, 1>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 1> &red) {
                         double axr[K], axi[K], br[K], bi[K], rr[K], ri[K];
-                        spmv_row<K, CX, true, false>(a, (int)i, fz, L, axr, axi);
+                        spmv_fv<K, CX>(a, (int)i, fz, L, np_, axr, axi);
                         B.load(i, br, bi);
                         e_sub<K, CX>(br, bi, axr, axi, rr, ri);
                         Rv.store(i, rr, ri);
@@ -390,6 +409,7 @@ struct Solver : PlanBase {
     double *H = hist;
     const DA a = da;
     const long long L = ld;
+    const int np_ = nopre;
     // F5+F1: [end of the previous iteration, deferred: rho_old = rho,
     // ||r|| record + tests, iteration count] then [this iteration: rho,
     // rho/omega zero tests, beta = (rho/rho_old)*(alpha/omega)].  The norm
@@ -462,7 +482,7 @@ struct Solver : PlanBase {
     rows<K, CX, 1, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
                         double vr[K], vi[K], rr[K], ri[K];
-                        spmv_row<K, CX, true, false>(a, (int)i, phc, L, vr, vi);
+                        spmv_fv<K, CX>(a, (int)i, phc, L, np_, vr, vi);
                         V.store(i, vr, vi);
                         RT.load(i, rr, ri);
                         acc_hdot<K, CX>(red.h[0], rr, ri, vr, vi);
@@ -510,7 +530,7 @@ struct Solver : PlanBase {
     rows<K, CX, 2, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 2, 0> &red) {
                         double tr[K], ti[K], sr[K], si[K];
-                        spmv_row<K, CX, true, false>(a, (int)i, shc, L, tr, ti);
+                        spmv_fv<K, CX>(a, (int)i, shc, L, np_, tr, ti);
                         T.store(i, tr, ti);
                         Sv.load(i, sr, si);
                         acc_hdot<K, CX>(red.h[0], tr, ti, tr, ti);
@@ -577,7 +597,7 @@ struct Solver : PlanBase {
   void cgs_alloc() {
     x = mc(); r = mc(); rt0 = mc(); u = mc(); pp = mc(); q = mc(); v = mc();
     phat = fv(); uhat = fv();
-    whead = (double *)dalloc(sizeof(double) * 2 * ld);
+    whead = (double *)dalloc(sizeof(double) * (nopre ? K * 2 : 2) * ld);
   }
   void cgs_setup() {
     zero_mc(x);
@@ -592,6 +612,7 @@ struct Solver : PlanBase {
     double *H = hist;
     const DA a = da;
     const long long L = ld;
+    const int np_ = nopre;
     double *WH = whead;
     fin(S, err, part, G, st,
         [=] __device__(State * S_, const double *pt_, int G_, double *sm) {
@@ -633,7 +654,7 @@ struct Solver : PlanBase {
     rows<K, CX, 1, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
                         double vr[K], vi[K], rr[K], ri[K];
-                        spmv_row<K, CX, true, false>(a, (int)i, phc, L, vr, vi);
+                        spmv_fv<K, CX>(a, (int)i, phc, L, np_, vr, vi);
                         V.store(i, vr, vi);
                         RT.load(i, rr, ri);
                         acc_hdot<K, CX>(red.h[0], rr, ri, vr, vi);
@@ -660,8 +681,16 @@ struct Solver : PlanBase {
                         e_axpy<K, CX>(ma, vr, vi, ur, ui, qr, qi);
                         Q.store(i, qr, qi);
                         e_add<K, CX>(ur, ui, qr, qi, wr, wi);
-                        WH[i] = wr[0];
-                        if (CX) WH[L + i] = wi[0];
+                        if (np_) {  // M = I: the whole u + q
+#pragma unroll
+                          for (int c = 0; c < K; ++c) {
+                            WH[c * L + i] = wr[c];
+                            if (CX) WH[(K + c) * L + i] = wi[c];
+                          }
+                        } else {
+                          WH[i] = wr[0];
+                          if (CX) WH[L + i] = wi[0];
+                        }
                         Y.set_sent(i);
                         UH.set_sent(i);
                       });
@@ -672,7 +701,7 @@ struct Solver : PlanBase {
                       [=] __device__(long long i, Red<K, CX, 1, 1> &red) {
                         double qr[K], qi[K], xr[K], xi[K], fr[K], fi[K],
                             tr[K], ti[K], rr[K], ri[K];
-                        spmv_row<K, CX, true, false>(a, (int)i, uhc, L, qr, qi);
+                        spmv_fv<K, CX>(a, (int)i, uhc, L, np_, qr, qi);
                         X.load(i, xr, xi);
                         UH.template load_mc<K>(i, fr, fi);
                         e_axpy<K, CX>(Sd->alpha, fr, fi, xr, xi, tr, ti);
@@ -721,6 +750,7 @@ struct Solver : PlanBase {
     double *H = hist;
     const DA a = da;
     const long long L = ld;
+    const int np_ = nopre;
     // K2: w = Bt + beta Bp (end of previous iteration), p = r + beta (p - u)
     rows<K, CX, 0, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 0, 0> &) {
@@ -751,7 +781,7 @@ struct Solver : PlanBase {
     rows<K, CX, 1, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
                         double vr[K], vi[K], rr[K], ri[K];
-                        spmv_row<K, CX, true, false>(a, (int)i, mpc, L, vr, vi);
+                        spmv_fv<K, CX>(a, (int)i, mpc, L, np_, vr, vi);
                         BP.store(i, vr, vi);
                         RT.load(i, rr, ri);
                         acc_hdot<K, CX>(red.h[0], rr, ri, vr, vi);
@@ -798,7 +828,7 @@ struct Solver : PlanBase {
     rows<K, CX, 6, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 6, 0> &red) {
                         double br[K], bi[K], tr[K], ti[K];
-                        spmv_row<K, CX, true, false>(a, (int)i, mtc, L, br, bi);
+                        spmv_fv<K, CX>(a, (int)i, mtc, L, np_, br, bi);
                         BT.store(i, br, bi);
                         T.load(i, tr, ti);
                         acc_hdot<K, CX>(red.h[0], br, bi, br, bi);
@@ -1002,6 +1032,7 @@ struct Solver : PlanBase {
     double *H = hist;
     const DA a = da;
     const long long L = ld;
+    const int np_ = nopre;
     const double *pc = pp, *ptc = pt;
     // q = A p ; sigma = hdot(pt, q) (role 0) || qt = A^H pt (role 1): the
     // two SpMV chains run on separate threads
@@ -1162,6 +1193,7 @@ struct Solver : PlanBase {
     const MVt B = mv(b);
     const DA a = da;
     const long long L = ld;
+    const int np_ = nopre;
     rows<K, CX, 0, 2>(n, nullptr, part, st,
                       [=] __device__(long long i, Red<K, CX, 0, 2> &red) {
                         double axr[K], axi[K], br[K], bi[K], rr[K], ri[K];
@@ -1191,15 +1223,12 @@ struct Solver : PlanBase {
 template <int K, bool CX>
 int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
               double *d_hist, SolveOut *out, cudaStream_t st, char *errbuf) {
-  if (!p.precond_ilu) {
-    snprintf(errbuf, 256, "precond 'none' is not implemented on the device path");
-    return 3;
-  }
   if (p.method == kBiCG) ensure_adjoint(A, st);
   const char *nocond = getenv("MPK_NO_COND_GRAPH");
   const bool use_cond = !nocond || nocond[0] == '0';
   // plan cache: one workspace + graph per (method, K, field) on this matrix
-  const int key = (p.ex ? 100000 * p.ex->world : 0) + p.reduce_seq * 1000 +
+  const int key = (p.precond_ilu ? 0 : 10000000) + (p.ex ? 100000 * p.ex->world : 0) +
+                  p.reduce_seq * 1000 +
                   p.method * 100 + K * 10 + (CX ? 1 : 0);
   Solver<K, CX> *sv = nullptr;
   auto it = A.plans.find(key);

@@ -64,6 +64,19 @@ __device__ __forceinline__ void spmv_row(const DA &A, int i, const double *x,
   }
 }
 
+// SpMV row on an "applied" vector: the binary64 head of an ILU(0)-mixed
+// output (promoted per product), or, preconditioner 'none' (mc != 0), the
+// full MC vector (solvers.py:128-136: M = I returns the vector itself)
+template <int K, bool CX>
+__device__ __forceinline__ void spmv_fv(const DA &A, int i, const double *x,
+                                        long long ld, int mc, double (&yr)[K],
+                                        double (&yi)[K]) {
+  if (mc)
+    spmv_row<K, CX, false, false>(A, i, x, ld, yr, yi);
+  else
+    spmv_row<K, CX, true, false>(A, i, x, ld, yr, yi);
+}
+
 // ---------------------------------------------------------------------
 // row-kernel framework: NH complex-or-real hdot slots + NN norm slots
 // ---------------------------------------------------------------------

@@ -116,11 +116,19 @@ def _device_solve(A, b: DenseVector, cfg: SolverConfig, hist_cap: int | None = N
         raise ValueError(f"field mismatch: matrix {A.field}, vector {b.field}")
     if b.precision != cfg.precision:
         raise ValueError("vector precision must match cfg.precision")
-    if cfg.spmv_mode != "mixed" or cfg.precond != PrecondMode.ILU0_MIXED:
+    if cfg.precond not in (PrecondMode.ILU0_MIXED, PrecondMode.NONE):
         raise NotImplementedError(
-            "the B200 path implements precond=ILU0_MIXED with spmv_mode='mixed' "
-            "(SURVEY.md section 8); other variants are listed in section 8f")
-    if not _binary64_exact(A):
+            "the B200 path implements precond ILU0_MIXED and NONE; the working-"
+            "precision ILU(0) ('ilu0') is listed in SURVEY.md section 8f")
+    if cfg.spmv_mode == "full":
+        # full SpMV on a matrix whose values are exactly binary64 IS the mixed
+        # computation bit for bit (reference tests/test_sparse.py:130-147);
+        # matrices with non-zero tails need MC x MC products (section 8f)
+        if not _binary64_exact(A):
+            raise NotImplementedError(
+                "spmv_mode='full' on the B200 path needs binary64-representable "
+                "matrix values (MC-valued matrices: SURVEY.md section 8f)")
+    elif not _binary64_exact(A):
         raise ValueError("mixed SpMV requires binary64-representable matrix values")
     k = cfg.precision.k
     n = A.n
@@ -131,12 +139,13 @@ def _device_solve(A, b: DenseVector, cfg: SolverConfig, hist_cap: int | None = N
     x = DenseVector.zeros(n, cfg.precision, A.field)
     hist = np.zeros((max(hist_cap, 1), k))
     rep = _lib.MpkReport()
-    rc = _lib.lib().mpk_solve(
-        d.h, ctypes.c_int(_lib.METHOD_CODE[cfg.method]), ctypes.c_int(k),
-        ctypes.c_double(cfg.eps_rel), ctypes.c_double(cfg.eps_abs),
-        ctypes.c_int64(max_iter), _lib.dptr(_lib.f64(b.re)),
-        _lib.dptr(None if b.im is None else _lib.f64(b.im)), _lib.dptr(x.re),
-        _lib.dptr(x.im), _lib.dptr(hist), ctypes.c_int64(hist_cap), ctypes.byref(rep))
+    with _lib.precond_scope(d.ctx, cfg.precond == PrecondMode.ILU0_MIXED):
+        rc = _lib.lib().mpk_solve(
+            d.h, ctypes.c_int(_lib.METHOD_CODE[cfg.method]), ctypes.c_int(k),
+            ctypes.c_double(cfg.eps_rel), ctypes.c_double(cfg.eps_abs),
+            ctypes.c_int64(max_iter), _lib.dptr(_lib.f64(b.re)),
+            _lib.dptr(None if b.im is None else _lib.f64(b.im)), _lib.dptr(x.re),
+            _lib.dptr(x.im), _lib.dptr(hist), ctypes.c_int64(hist_cap), ctypes.byref(rep))
     _lib.check(rc, "mpk_solve")
     h = [tuple(r) for r in hist[: min(rep.hist_len, hist_cap)]]
     return rep, (x if rep.has_x else None), h
@@ -196,12 +205,16 @@ def _unit(x: DenseVector, v: float):
 
 
 def _method(name: str, A, b, cfg: SolverConfig, M=None) -> SolveReport:
-    if M is None or not isinstance(M, Ilu0Preconditioner) or not M.mixed:
+    if M is None:  # the reference's unpreconditioned call (M = I)
+        pre = PrecondMode.NONE
+    elif isinstance(M, Ilu0Preconditioner) and M.mixed:
+        pre = PrecondMode.ILU0_MIXED
+    else:
         raise NotImplementedError(
-            f"{name}(M=...) on the B200 path needs an ILU(0)-mixed preconditioner "
-            "(build_preconditioner(A, PrecondMode.ILU0_MIXED))")
-    c = SolverConfig(method=name, precision=cfg.precision, precond=PrecondMode.ILU0_MIXED,
-                     spmv_mode="mixed", eps_rel=cfg.eps_rel, eps_abs=cfg.eps_abs,
+            f"{name}(M=...) on the B200 path takes M=None or an ILU(0)-mixed "
+            "preconditioner (build_preconditioner(A, PrecondMode.ILU0_MIXED))")
+    c = SolverConfig(method=name, precision=cfg.precision, precond=pre,
+                     spmv_mode=cfg.spmv_mode, eps_rel=cfg.eps_rel, eps_abs=cfg.eps_abs,
                      max_iter=cfg.max_iter)
     rep, x, hist = _device_solve(A, b, c)
     if rep.breakdown == 9:

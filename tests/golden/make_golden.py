@@ -282,7 +282,8 @@ class HistoryHook:
         solvers._DISPATCH.update(self._disp)
 
 
-def run_ref(A64_re, A64_im, rp, ci, n, b, method, k, eps_rel, eps_abs, max_iter):
+def run_ref(A64_re, A64_im, rp, ci, n, b, method, k, eps_rel, eps_abs, max_iter,
+            precond="ilu0-mixed", spmv_mode="mixed"):
     prec = PREC[k]
     vre = np.zeros((len(ci), k))
     vre[:, 0] = A64_re
@@ -292,7 +293,7 @@ def run_ref(A64_re, A64_im, rp, ci, n, b, method, k, eps_rel, eps_abs, max_iter)
         vim[:, 0] = A64_im
     A = sparse.CsrMatrix(n, rp, ci, vre, vim, prec)
     cfg = solvers.SolverConfig(method=method, precision=prec,
-                               precond=ilu.PrecondMode.ILU0_MIXED, spmv_mode="mixed",
+                               precond=ilu.PrecondMode(precond), spmv_mode=spmv_mode,
                                eps_rel=eps_rel, eps_abs=eps_abs, max_iter=max_iter)
     with HistoryHook() as hk:
         t0 = time.perf_counter()
@@ -350,6 +351,35 @@ def gen_solver_small():
                 for key, v in o.items():
                     data[f"{tag}{k}_{m}_{key}"] = v
     np.savez_compressed(HERE / "solver_small.npz", **data)
+
+
+def gen_solver_none():
+    """the unpreconditioned path (precond='none',
+    M = I, solvers.py:128-136) in mixed SpMV mode, and spmv_mode='full' with
+    ILU(0)-mixed on a binary64 matrix at working precision, on the
+    solver_small systems."""
+    data = {}
+    for cx in (False, True):
+        tag = "c" if cx else "r"
+        rng = np.random.default_rng(31 if not cx else 32)
+        A64 = random_dd(rng, 60, 0.12, cx)
+        n = A64.n
+        xt = rng.uniform(-1, 1, n) + (1j * rng.uniform(-1, 1, n) if cx else 0.0)
+        vim = A64.val_im[:, 0] if cx else None
+        for k in (2, 3):
+            b = rhs(A64.val_re[:, 0], vim, A64.row_ptr, A64.col_idx, n, k, x_true=xt)
+            tol = {2: 1e-25, 3: 1e-40}[k]
+            for m in ("bicg", "cgs", "bicgstab", "gpbicg"):
+                o = run_ref(A64.val_re[:, 0], vim, A64.row_ptr, A64.col_idx, n, b, m, k,
+                            tol, 1e-100, None, precond="none")
+                for key, v in o.items():
+                    data[f"{tag}{k}_none_{m}_{key}"] = v
+            for m in ("bicgstab", "gpbicg"):
+                o = run_ref(A64.val_re[:, 0], vim, A64.row_ptr, A64.col_idx, n, b, m, k,
+                            tol, 1e-100, None, spmv_mode="full")
+                for key, v in o.items():
+                    data[f"{tag}{k}_full_{m}_{key}"] = v
+    np.savez_compressed(HERE / "solver_none.npz", **data)
 
 
 def gen_solver_cfg(which):
@@ -420,6 +450,9 @@ if __name__ == "__main__":
     if "small" in what:
         gen_solver_small()
         print("solver_small done", time.time() - t0, flush=True)
+    if "none" in what:
+        gen_solver_none()
+        print("solver_none done", time.time() - t0, flush=True)
     for c in ("cfg1", "cfg2", "cfg3", "cfg5"):
         if "cfg" in what or c in what:
             gen_solver_cfg([c])

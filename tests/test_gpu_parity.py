@@ -502,3 +502,56 @@ def test_device_twin_mode_reductions_bitwise(pkg, field, k):
         assert bits_equal(np.array(h.im.components), g[f"{t}_hdot_im"])
     else:
         assert bits_equal(np.array(h.components), g[f"{t}_hdot_re"])
+
+
+# ---------------------------------------------------------------------------
+# precond='none' (M = I; the methods run on the MC vectors,
+# SpMV on MC inputs, no factorization) and spmv_mode='full' on a binary64
+# matrix at working precision, against the reference's own runs
+# (tests/golden/solver_none.npz): twin mode bit-identical histories and x,
+# tree mode within the north-star bound with the same iteration count.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("field", ["r", "c"])
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("method", ["bicg", "cgs", "bicgstab", "gpbicg"])
+@pytest.mark.parametrize("variant", ["none", "full"])
+def test_device_precond_none_and_spmv_full(pkg, field, k, method, variant):
+    g = golden("solver_small.npz")
+    gn = golden("solver_none.npz")
+    pre = f"{field}{k}_{variant}_{method}"
+    if f"{pre}_iterations" not in gn.files:
+        pytest.skip("spmv_mode='full' fixtures cover bicgstab and gpbicg")
+    cx = field == "c"
+    A = _csr(pkg, g[f"{field}_rp"], g[f"{field}_ci"], g[f"{field}_vre"],
+             g[f"{field}_vim"] if cx else None)
+    P = getattr(pkg.Precision, PREC_OF[k])
+    Ak = A.promoted(P)
+    b = pkg.DenseVector(g[f"{field}{k}_b_re"].copy(),
+                        g[f"{field}{k}_b_im"].copy() if cx else None, P)
+    cfg = pkg.SolverConfig(
+        method=method, precision=P,
+        precond=pkg.PrecondMode.NONE if variant == "none" else pkg.PrecondMode.ILU0_MIXED,
+        spmv_mode="mixed" if variant == "none" else "full", eps_rel=TOL[k], eps_abs=1e-100)
+    with pkg.reduction_mode("sequential"):
+        twin = pkg.solve(Ak, b, cfg)
+    assert twin.iterations == int(gn[f"{pre}_iterations"])
+    assert twin.converged == bool(gn[f"{pre}_converged"])
+    assert bits_equal(np.asarray(twin.history), gn[f"{pre}_hist"])
+    assert bits_equal(twin.x.re, gn[f"{pre}_x_re"])
+    if cx:
+        assert bits_equal(twin.x.im, gn[f"{pre}_x_im"])
+    rep = pkg.solve(Ak, b, cfg)  # tree reductions
+    assert rep.iterations == int(gn[f"{pre}_iterations"])
+    _hist_check(rep.history, gn[f"{pre}_hist"], k)
+
+
+def test_device_precond_none_per_method_entry(pkg):
+    """bicgstab(A, b, cfg, M=None) is the reference's unpreconditioned call."""
+    g = golden("solver_small.npz")
+    gn = golden("solver_none.npz")
+    A = _csr(pkg, g["r_rp"], g["r_ci"], g["r_vre"], None)
+    P = pkg.Precision.DD
+    b = pkg.DenseVector(g["r2_b_re"].copy(), None, P)
+    cfg = pkg.SolverConfig(method="bicgstab", precision=P, eps_rel=1e-25, eps_abs=1e-100)
+    rep = pkg.bicgstab(A.promoted(P), b, cfg, M=None)
+    assert rep.iterations == int(gn["r2_none_bicgstab_iterations"])

@@ -161,6 +161,48 @@ def test_solver_small_bitwise(orc, field, k, method):
     _check_run(orc, rep, hist, xr, xi, g, f"{field}{k}_{method}", cx)
 
 
+# precond='none' (M = I) and spmv_mode='full' on a
+# binary64 matrix held at working precision (tests/golden/solver_none.npz,
+# generated by the reference: make_golden.py none)
+@pytest.mark.parametrize("field", ["r", "c"])
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("method", ["bicg", "cgs", "bicgstab", "gpbicg"])
+def test_solver_precond_none_bitwise(orc, field, k, method):
+    g = golden("solver_small.npz")
+    gn = golden("solver_none.npz")
+    cx = field == "c"
+    rp, ci = g[f"{field}_rp"], g[f"{field}_ci"]
+    n = len(rp) - 1
+    tol = {2: 1e-25, 3: 1e-40}[k]
+    rep, xr, xi, hist = orc.solve(n, rp, ci, g[f"{field}_vre"],
+                                  g[f"{field}_vim"] if cx else None, method, k,
+                                  g[f"{field}{k}_b_re"],
+                                  g[f"{field}{k}_b_im"] if cx else None,
+                                  eps_rel=tol, eps_abs=1e-100, precond_ilu=False)
+    _check_run(orc, rep, hist, xr, xi, gn, f"{field}{k}_none_{method}", cx)
+
+
+@pytest.mark.parametrize("field", ["r", "c"])
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("method", ["bicgstab", "gpbicg"])
+def test_solver_spmv_full_equals_mixed(orc, field, k, method):
+    """spmv_mode='full' on a binary64 matrix at working precision is the
+    mixed computation bit for bit (reference tests/test_sparse.py:130-147):
+    the oracle's mixed run reproduces the reference's 'full' run."""
+    g = golden("solver_small.npz")
+    gn = golden("solver_none.npz")
+    cx = field == "c"
+    rp, ci = g[f"{field}_rp"], g[f"{field}_ci"]
+    n = len(rp) - 1
+    tol = {2: 1e-25, 3: 1e-40}[k]
+    rep, xr, xi, hist = orc.solve(n, rp, ci, g[f"{field}_vre"],
+                                  g[f"{field}_vim"] if cx else None, method, k,
+                                  g[f"{field}{k}_b_re"],
+                                  g[f"{field}{k}_b_im"] if cx else None,
+                                  eps_rel=tol, eps_abs=1e-100)
+    _check_run(orc, rep, hist, xr, xi, gn, f"{field}{k}_full_{method}", cx)
+
+
 def _cfg_fixture(name):
     return golden(name)
 
