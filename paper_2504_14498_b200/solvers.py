@@ -28,6 +28,7 @@ import numpy as np
 
 from . import _lib
 from .ilu import (
+    IdentityPreconditioner,
     Ilu0Preconditioner,
     NumericBreakdownError,
     PrecondMode,
@@ -205,7 +206,7 @@ def _unit(x: DenseVector, v: float):
 
 
 def _method(name: str, A, b, cfg: SolverConfig, M=None) -> SolveReport:
-    if M is None:  # the reference's unpreconditioned call (M = I)
+    if M is None or isinstance(M, IdentityPreconditioner):  # M = I (reference default)
         pre = PrecondMode.NONE
     elif isinstance(M, Ilu0Preconditioner) and M.mixed:
         pre = PrecondMode.ILU0_MIXED

@@ -382,6 +382,65 @@ def gen_solver_none():
     np.savez_compressed(HERE / "solver_none.npz", **data)
 
 
+def mm_texts():
+    """Synthetic Matrix Market files for the f3 fixtures: every field /
+    symmetry, duplicated entries (exact MC sums), comments, blank lines."""
+    rng = np.random.default_rng(77)
+    out = {}
+    for field in ("real", "integer", "complex", "pattern"):
+        for sym in ("general", "symmetric", "hermitian", "skew-symmetric"):
+            if sym == "hermitian" and field != "complex":
+                continue
+            n = 7
+            ents = []
+            for _ in range(18):
+                i, j = sorted(rng.integers(1, n + 1, 2), reverse=True)
+                if sym == "skew-symmetric" and i == j:
+                    continue
+                if sym == "general" and rng.random() < 0.5:
+                    i, j = j, i
+                if field == "pattern":
+                    ents.append(f"{i} {j}")
+                elif field == "integer":
+                    ents.append(f"{i} {j} {int(rng.integers(-9, 10))}")
+                elif field == "complex":
+                    ents.append(f"{i} {j} {rng.standard_normal():.17g} {rng.standard_normal():.17g}")
+                else:
+                    # duplicates with widely different magnitudes: MC sums matter
+                    v = rng.standard_normal() * 10.0 ** int(rng.integers(-20, 20))
+                    ents.append(f"{i} {j} {v:.17g}")
+            for d in range(1, n + 1):
+                if sym != "skew-symmetric":
+                    if field == "pattern":
+                        ents.append(f"{d} {d}")
+                    elif field == "complex":
+                        ents.append(f"{d} {d} {float(n + d)} 0.0")
+                    else:
+                        ents.append(f"{d} {d} {n + d}")
+            text = (f"%%MatrixMarket matrix coordinate {field} {sym}\n% generated\n\n"
+                    f"{n} {n} {len(ents)}\n" + "\n".join(ents) + "\n")
+            out[f"{field}_{sym}"] = text
+    return out
+
+
+def gen_mm():
+    from mpkrylov import coo_to_csr, parse_matrix_market
+
+    data = {}
+    for tag, text in mm_texts().items():
+        data[f"{tag}_text"] = np.array(text)
+        coo = parse_matrix_market(text)
+        data[f"{tag}_coo_row"], data[f"{tag}_coo_col"] = coo.row, coo.col
+        data[f"{tag}_coo_re"] = coo.val_re
+        for k in (1, 2, 3, 4):
+            A = coo_to_csr(coo, PREC[k] if k > 1 else Precision.F64)
+            data[f"{tag}_{k}_rp"], data[f"{tag}_{k}_ci"] = A.row_ptr, A.col_idx
+            data[f"{tag}_{k}_re"] = A.val_re
+            if A.val_im is not None:
+                data[f"{tag}_{k}_im"] = A.val_im
+    np.savez_compressed(HERE / "mm_small.npz", **data)
+
+
 def gen_solver_cfg(which):
     data = {}
     if "cfg1" in which:
@@ -450,6 +509,9 @@ if __name__ == "__main__":
     if "small" in what:
         gen_solver_small()
         print("solver_small done", time.time() - t0, flush=True)
+    if "mm" in what:
+        gen_mm()
+        print("mm done", time.time() - t0, flush=True)
     if "none" in what:
         gen_solver_none()
         print("solver_none done", time.time() - t0, flush=True)
