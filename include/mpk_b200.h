@@ -94,6 +94,11 @@ void *mpk_ctx_stream(mpk_ctx *ctx);
 #define MPK_OPT_PRECOND 2
 #define MPK_PRECOND_NONE 0
 #define MPK_PRECOND_ILU0_MIXED 1
+/* MPK_PRECOND_ILU0_FULL: ILU(0) at the working precision (ilu.py:279-281;
+ * factors and sweeps in k-component arithmetic with the _mcfast fused
+ * a - b*c, _mcfast.py:80-183, 390-402); real field, CGS / BiCGSTAB /
+ * GPBiCG */
+#define MPK_PRECOND_ILU0_FULL 2
 int mpk_ctx_set_option(mpk_ctx *ctx, int option, int64_t value);
 
 /* CsrMatrix.demoted() upload (sparse.py:192-249): binary64 values, val_im
@@ -112,6 +117,12 @@ int mpk_csr_set_values(mpk_matrix *m, const double *val_re,
  * Returns MPK_SINGULAR_PIVOT with *bad_row / *structural, or
  * MPK_NUMERIC_BREAKDOWN for non-finite factors. */
 int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural);
+/* ilu0_factorize (ilu.py:279-281) of the uploaded binary64 matrix promoted
+ * to k = 2..4 components (real); factors downloadable as (nnz,k) and
+ * applicable to (n,k) vectors (ilu0_apply, ilu.py:410-420) */
+int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *structural);
+int mpk_ilu0_download_full(mpk_matrix *m, int k, double *lu);
+int mpk_ilu0_apply_full(mpk_matrix *m, int k, const double *r, double *z);
 /* IluFactors.val_re / val_im as (nnz,) arrays (bitwise parity tests) */
 int mpk_ilu0_download(mpk_matrix *m, double *lu_re, double *lu_im);
 /* ilu0_apply on binary64 vectors (ilu.py:410-433): z = U^-1 L^-1 r, or the
@@ -144,7 +155,9 @@ int mpk_axpy(mpk_ctx *ctx, int64_t n, int k, const double *alpha_re,
 /* Element-wise MC scalar arithmetic on the device (twin tests of
  * _mccore.py): op 0 add, 1 sub, 2 mul, 3 div, 4 sqrt(a), 5 complex mul,
  * 6 complex div, 7 renorm of 7 terms (a is (n,7)), 8 mul((a0,0..), b),
- * 9 mul(a, (b0,0..)), 10 mul((a0,0..),(b0,0..)).  Arrays (n,k). */
+ * 9 mul(a, (b0,0..)), 10 mul((a0,0..),(b0,0..)), 11 fused a - b*c of the
+ * working-precision ILU(0) sweeps (_mcfast.rmulsubK, c passed in a_im),
+ * 12 fused product (_mcfast.rmulK).  Arrays (n,k). */
 int mpk_mc_elementwise(mpk_ctx *ctx, int op, int k, int64_t n,
                        const double *a_re, const double *a_im,
                        const double *b_re, const double *b_im, double *o_re,

@@ -50,6 +50,7 @@ EXPORTS = (
     "mpk_csr_set_values", "mpk_run_jobs", "mpk_ctx_set_option",
     "mpk_comm_unique_id", "mpk_comm_create", "mpk_comm_create_local", "mpk_comm_destroy",
     "mpk_comm_rank", "mpk_comm_world", "mpk_solve_dev_sharded",
+    "mpk_ilu0_factor_full", "mpk_ilu0_download_full", "mpk_ilu0_apply_full",
 )
 
 MPK_OPT_REDUCTION = 1
@@ -60,17 +61,21 @@ _precond_lock = threading.Lock()
 
 class precond_scope:
     """Selects the solvers' preconditioner on a context for one call
-    (MPK_OPT_PRECOND) and restores ILU(0)-mixed afterwards; calls on the same
-    context are serialised while a non-default preconditioner is set."""
+    (MPK_OPT_PRECOND: 0 none, 1 ILU(0)-mixed, 2 working-precision ILU(0))
+    and restores ILU(0)-mixed afterwards; calls on the same context are
+    serialised while a non-default preconditioner is set."""
 
-    def __init__(self, ctx, ilu: bool):
-        self.ctx, self.ilu = ctx, ilu
+    def __init__(self, ctx, ilu):
+        # ilu: True -> 1 (default), False -> 0, or the option value itself
+        self.ctx = ctx
+        self.value = int(ilu) if isinstance(ilu, bool) else int(ilu)
+        self.ilu = self.value == 1
 
     def __enter__(self):
         if not self.ilu:
             _precond_lock.acquire()
             check(lib().mpk_ctx_set_option(self.ctx, ctypes.c_int(MPK_OPT_PRECOND),
-                                           ctypes.c_int64(0)), "mpk_ctx_set_option")
+                                           ctypes.c_int64(self.value)), "mpk_ctx_set_option")
         return self
 
     def __exit__(self, *exc):

@@ -851,8 +851,9 @@ int mpk_ctx_set_option(mpk_ctx *ctx, int option, int64_t value) {
       ctx->reduce_seq = (int)value;
       return MPK_OK;
     case MPK_OPT_PRECOND:
-      if (value != MPK_PRECOND_NONE && value != MPK_PRECOND_ILU0_MIXED)
-        return fail(MPK_INVALID, "precond must be 0 (none) or 1 (ilu0-mixed)");
+      if (value != MPK_PRECOND_NONE && value != MPK_PRECOND_ILU0_MIXED &&
+          value != MPK_PRECOND_ILU0_FULL)
+        return fail(MPK_INVALID, "precond must be 0 (none), 1 (ilu0-mixed) or 2 (ilu0)");
       ctx->precond = (int)value;
       return MPK_OK;
     default:
@@ -1011,6 +1012,9 @@ void mpk_csr_free(mpk_matrix *m) {
   }
   free_sweeps(A.smat);
   free_sweeps(A.smat_adj);
+  if (A.lu_mc) cudaFree(A.lu_mc);
+  if (A.rcp_mc) cudaFree(A.rcp_mc);
+  if (A.sw_mc) cudaFree(A.sw_mc);
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete m;
@@ -1088,6 +1092,135 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   gather_csweep(A.lu, A.smat.cs, A.cx, m->ctx->stream);
   gather_rsweep(A.lu, A.smat.rs, A.cx, m->ctx->stream);
   gather_wsweep(A.lu, A.smat.wf, A.cx, m->ctx->stream);
+  return MPK_OK;
+}
+
+__global__ void promote_vals_kernel(long long nnz, int k, const double *v, double *o) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < nnz;
+       p += (long long)gridDim.x * blockDim.x)
+    for (int c = 0; c < k; ++c) o[p * k + c] = c == 0 ? v[p] : 0.0;
+}
+
+// ilu0_factorize (ilu.py:279-281 -> _factorize_tuples at precision k > 1) of
+// the uploaded binary64 matrix promoted to k components; real field.
+int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *structural) {
+  DMat &A = m->A;
+  cudaStream_t st = m->ctx->stream;
+  if (k < 2 || k > 4) return fail(MPK_INVALID, "working-precision ILU(0): k = 2..4");
+  if (A.cx) return fail(MPK_INVALID, "working-precision ILU(0): real field only");
+  CKR(cudaSetDevice(m->ctx->device));
+  for (int i = 0; i < A.n; ++i) {  // _structural_check ilu.py:172-175
+    if (A.h_dp[i] < 0) {
+      if (bad_row) *bad_row = i;
+      if (structural) *structural = 1;
+      return fail(MPK_SINGULAR_PIVOT, "ILU(0): structurally missing pivot U[" +
+                                          std::to_string(i) + "," + std::to_string(i) + "]");
+    }
+  }
+  const long long L = plane_ld(A.n);
+  if (A.lu_mc_k != k) {
+    if (A.lu_mc) cudaFree(A.lu_mc);
+    if (A.rcp_mc) cudaFree(A.rcp_mc);
+    if (A.sw_mc) cudaFree(A.sw_mc);
+    A.lu_mc = A.rcp_mc = A.sw_mc = nullptr;
+    CKR(cudaMalloc(&A.lu_mc, sizeof(double) * k * (A.nnz ? A.nnz : 1)));
+    CKR(cudaMalloc(&A.rcp_mc, sizeof(double) * k * (A.n ? A.n : 1)));
+    CKR(cudaMalloc(&A.sw_mc, sizeof(double) * k * L + 16));
+    A.lu_mc_k = k;
+  }
+  A.mc_factored = false;
+  if (A.nnz > 0) {
+    ++tl_launches;
+    promote_vals_kernel<<<148 * 4, 256, 0, st>>>(A.nnz, k, A.val, A.lu_mc);
+  }
+  CKR(cudaMemsetAsync(m->rowflag, 0, sizeof(int) * (A.n + 1), st));
+  if (!m->hres) CKR(cudaMallocHost(&m->hres, sizeof(int) * 8));
+  int *init = m->hres;
+  init[0] = 0;
+  init[1] = 0;
+  init[2] = INT_MAX;
+  init[3] = 0;
+  CKR(cudaMemcpyAsync(m->fscratch, init, sizeof(int) * 4, cudaMemcpyHostToDevice, st));
+  FactorMcArgs fa{};
+  fa.n = A.n;
+  fa.rp = A.rp;
+  fa.ci = A.ci;
+  fa.dp = A.dp;
+  fa.lu = A.lu_mc;
+  fa.rowflag = m->rowflag;
+  fa.tick = m->fscratch;
+  fa.bad_row = m->fscratch + 2;
+  fa.nonfinite = m->fscratch + 3;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  if (A.n > 0) launch_factor_mc(fa, k, st);
+  cudaEventRecord(e1, st);
+  int *res = m->hres + 4;
+  CKR(cudaMemcpyAsync(res, m->fscratch, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  cudaEventElapsedTime(&m->factor_ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (res[2] != INT_MAX) {
+    if (bad_row) *bad_row = res[2];
+    if (structural) *structural = 0;
+    return fail(MPK_SINGULAR_PIVOT, "ILU(0): zero pivot U[" + std::to_string(res[2]) + "," +
+                                        std::to_string(res[2]) + "]");
+  }
+  if (res[3]) return fail(MPK_NUMERIC_BREAKDOWN, "non-finite value in ILU(0) factors");
+  launch_recip_mc(A.n, A.dp, A.lu_mc, A.rcp_mc, k, st);
+  A.mc_factored = true;
+  return MPK_OK;
+}
+
+int mpk_ilu0_download_full(mpk_matrix *m, int k, double *lu) {
+  DMat &A = m->A;
+  if (!A.mc_factored || A.lu_mc_k != k) return fail(MPK_INVALID, "no working-precision factors");
+  CKR(cudaSetDevice(m->ctx->device));
+  CKR(cudaMemcpy(lu, A.lu_mc, sizeof(double) * k * A.nnz, cudaMemcpyDeviceToHost));
+  return MPK_OK;
+}
+
+// ilu0_apply (ilu.py:410-420) at working precision, (n,k) host arrays
+int mpk_ilu0_apply_full(mpk_matrix *m, int k, const double *r, double *z) {
+  DMat &A = m->A;
+  if (!A.mc_factored || A.lu_mc_k != k) return fail(MPK_INVALID, "no working-precision factors");
+  CKR(cudaSetDevice(m->ctx->device));
+  cudaStream_t st = m->ctx->stream;
+  const long long n = A.n, L = plane_ld(A.n);
+  double *din = nullptr, *dz = nullptr, *stage = nullptr;
+  CKR(cudaMalloc(&din, sizeof(double) * k * L + 16));
+  CKR(cudaMalloc(&dz, sizeof(double) * k * L + 16));
+  CKR(cudaMalloc(&stage, sizeof(double) * k * (n ? n : 1)));
+  CKR(cudaMemcpyAsync(stage, r, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
+  launch_to_planar(n, k, stage, nullptr, din, st);
+  CKR(cudaMemsetAsync(A.err, 0, sizeof(int), st));
+  SweepMcArgs a{};
+  a.n = A.n;
+  a.ld = L;
+  a.rp = A.rp;
+  a.ci = A.ci;
+  a.dp = A.dp;
+  a.lu = A.lu_mc;
+  a.rcp = A.rcp_mc;
+  a.in = din;
+  a.y = A.sw_mc;
+  a.z = dz;
+  a.tick = A.tick;
+  a.err = A.err;
+  a.done = nullptr;
+  launch_sweep_mc(a, k, st);
+  launch_from_planar(n, k, dz, stage, nullptr, st);
+  CKR(cudaMemcpyAsync(z, stage, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
+  int e = 0;
+  CKR(cudaMemcpyAsync(&e, A.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  cudaFree(din);
+  cudaFree(dz);
+  cudaFree(stage);
+  if (e) return fail(MPK_NUMERIC_BREAKDOWN, "non-finite value in triangular sweep");
   return MPK_OK;
 }
 
@@ -1491,10 +1624,19 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   int64_t bad = -1;
   int32_t structural = 0;
   tl_phase[0] = host_ms();
-  const bool ilu = m->ctx->precond != MPK_PRECOND_NONE;
-  if (!ilu && ex) return fail(MPK_INVALID, "sharded solve: ILU(0)-mixed only");
-  int rc = ilu ? mpk_ilu0_factor(m, &bad, &structural) : MPK_OK;  // M = I: no factors
-  if (!ilu) m->factor_ms = 0.f;
+  const int pre = m->ctx->precond;
+  const bool ilu = pre != MPK_PRECOND_NONE;
+  if (pre != MPK_PRECOND_ILU0_MIXED && ex)
+    return fail(MPK_INVALID, "sharded solve: ILU(0)-mixed only");
+  if (pre == MPK_PRECOND_ILU0_FULL && (m->A.cx || method == MPK_BICG))
+    return fail(MPK_INVALID,
+                "working-precision ILU(0) on the B200 path: real field, CGS / BiCGSTAB / GPBiCG");
+  int rc = MPK_OK;
+  if (pre == MPK_PRECOND_ILU0_MIXED)
+    rc = mpk_ilu0_factor(m, &bad, &structural);
+  else if (pre == MPK_PRECOND_ILU0_FULL)
+    rc = mpk_ilu0_factor_full(m, k, &bad, &structural);
+  if (!ilu) m->factor_ms = 0.f;  // M = I: no factors
   tl_phase[1] = host_ms();
   if (rc == MPK_SINGULAR_PIVOT || rc == MPK_NUMERIC_BREAKDOWN) {
     rep->iterations = 0;
@@ -1514,7 +1656,7 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   p.eps_rel = eps_rel;
   p.eps_abs = eps_abs;
   p.max_iter = max_iter < 0 ? 3LL * m->A.n : max_iter;
-  p.precond_ilu = ilu ? 1 : 0;
+  p.precond_ilu = pre == MPK_PRECOND_ILU0_FULL ? 2 : (ilu ? 1 : 0);
   p.hist_cap = hist_cap;
   p.reduce_seq = m->ctx->reduce_seq;
   p.ex = ex;

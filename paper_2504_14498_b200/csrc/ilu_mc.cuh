@@ -1,0 +1,34 @@
+// ilu_mc.cuh -- working-precision ILU(0) (precond 'ilu0'), see ilu_mc.cu.
+#pragma once
+
+#include "common.cuh"
+
+namespace mpk {
+
+struct FactorMcArgs {
+  int n;
+  const int *rp, *ci, *dp;
+  double *lu;      // [nnz][K]: in A promoted, out the factors (in place)
+  int *rowflag;    // per-row completion flags (zeroed)
+  int *tick;       // [0] ticket, [1] exit counter
+  int *bad_row;    // atomicMin of zero-pivot rows (init INT_MAX)
+  int *nonfinite;  // set if any factor is non-finite
+};
+struct SweepMcArgs {
+  int n;
+  long long ld;          // plane stride of in / y / z
+  const int *rp, *ci, *dp;
+  const double *lu;      // [nnz][K] factors
+  const double *rcp;     // [n][K] mc_div(1, U_ii)
+  const double *in;      // planar K-component input
+  double *y, *z;         // planar scratch / output (plane 0 sentinel-reset here)
+  int *tick;
+  int *err;
+  const int *done;
+};
+void launch_factor_mc(const FactorMcArgs &a, int k, cudaStream_t st);
+void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k,
+                     cudaStream_t st);
+void launch_sweep_mc(const SweepMcArgs &a, int k, cudaStream_t st);
+
+}  // namespace mpk

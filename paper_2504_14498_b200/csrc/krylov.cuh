@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "ilu.cuh"
 #include "shard.cuh"
+#include "ilu_mc.cuh"
 
 namespace mpk {
 
@@ -73,6 +74,11 @@ struct DMat {
   // level-ordered sweep matrices (single-CTA path, small n)
   SweepMats smat, smat_adj;
   bool smat_built = false, smat_adj_built = false;
+  // working-precision ILU(0) (precond 'ilu0', ilu_mc.cu): [nnz][K] factors,
+  // [n][K] reciprocal diagonals, planar K-component sweep scratch
+  double *lu_mc = nullptr, *rcp_mc = nullptr, *sw_mc = nullptr;
+  int lu_mc_k = 0;
+  bool mc_factored = false;
   int *tick = nullptr;  // 4 ints: [0..1] sweep A, [2..3] sweep B
   int *err = nullptr;
   // host copies of the pattern (for building transposes)
@@ -104,7 +110,7 @@ struct SolveParams {
   int method, k;
   double eps_rel, eps_abs;
   long long max_iter;
-  int precond_ilu;  // 1: ILU(0)-mixed, 0: identity
+  int precond_ilu;  // 1: ILU(0)-mixed, 0: identity, 2: working-precision ILU(0)
   long long hist_cap;
   int reduce_seq;   // 1: sequential-order (bit-identical twin) reductions
   Exchange *ex = nullptr;  // row-block sharded solve (shard.cuh), else null

@@ -204,7 +204,7 @@ struct Solver : PlanBase {
 
   Solver(DMat &A_, const SolveParams &p_, cudaStream_t st_, char *eb)
       : A(A_), p(p_), st(st_), errbuf(eb) {
-    nopre = p.precond_ilu ? 0 : 1;  // before any fv() allocation
+    nopre = p.precond_ilu == 1 ? 0 : 1;  // before any fv() allocation
     n = A.n;
     ld = plane_ld(n);
     // twin mode: element terms + ascending chains; finalize over 1 partial
@@ -292,8 +292,13 @@ struct Solver : PlanBase {
   // ILU(0)-mixed apply: z = promote(U^-1 L^-1 demote(in)).
   void sweep(const double *in_re, const double *in_im, double *y, double *z,
              bool adjoint, int which, bool after_loop = false) {
-    if (nopre) {  // M = I (and M^H = I): the MC vector itself
+    if (nopre) {
       (void)in_im;
+      if (p.precond_ilu == 2) {  // working-precision ILU(0) (ilu_mc.cu)
+        mc_sweep(in_re, z, which, after_loop, st);
+        return;
+      }
+      // M = I (and M^H = I): the MC vector itself
       cudaMemcpyAsync(z, in_re, sizeof(double) * K * (CX ? 2 : 1) * ld,
                       cudaMemcpyDeviceToDevice, st);
       return;
@@ -307,6 +312,25 @@ struct Solver : PlanBase {
     }
     sweep_on(st, in_re, in_im, y, z, adjoint, which, after_loop);
   }
+  // z = U^-1 L^-1 in at working precision (real; planar K-component)
+  void mc_sweep(const double *in, double *z, int which, bool after_loop,
+                cudaStream_t s_) {
+    SweepMcArgs a{};
+    a.n = n;
+    a.ld = ld;
+    a.rp = A.rp;
+    a.ci = A.ci;
+    a.dp = A.dp;
+    a.lu = A.lu_mc;
+    a.rcp = A.rcp_mc;
+    a.in = in;
+    a.y = A.sw_mc;
+    a.z = z;
+    a.tick = A.tick + 2 * which;
+    a.err = A.err;
+    a.done = after_loop ? nullptr : done;
+    launch_sweep_mc(a, K, s_);
+  }
   // all planes of an MC vector complete on every rank (sharded solve)
   void gather_mc(double *v) {
     if (!p.ex) return;
@@ -317,6 +341,10 @@ struct Solver : PlanBase {
                 double *y, double *z, bool adjoint, int which,
                 bool after_loop = false) {
     if (nopre) {
+      if (p.precond_ilu == 2) {
+        mc_sweep(in_re, z, which, after_loop, s_);
+        return;
+      }
       cudaMemcpyAsync(z, in_re, sizeof(double) * K * (CX ? 2 : 1) * ld,
                       cudaMemcpyDeviceToDevice, s_);
       return;
@@ -1227,7 +1255,8 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   const char *nocond = getenv("MPK_NO_COND_GRAPH");
   const bool use_cond = !nocond || nocond[0] == '0';
   // plan cache: one workspace + graph per (method, K, field) on this matrix
-  const int key = (p.precond_ilu ? 0 : 10000000) + (p.ex ? 100000 * p.ex->world : 0) +
+  const int key = (p.precond_ilu == 1 ? 0 : (p.precond_ilu + 1) * 10000000) +
+                  (p.ex ? 100000 * p.ex->world : 0) +
                   p.reduce_seq * 1000 +
                   p.method * 100 + K * 10 + (CX ? 1 : 0);
   Solver<K, CX> *sv = nullptr;

@@ -914,4 +914,78 @@ MPK_HD void py_cdiv(double ar, double ai, double br, double bi, double &qr,
   }
 }
 
+// ---------------------------------------------------------------------
+// Fused sweep primitives of the working-precision ILU(0) (_mcfast.py:80-183):
+// r = a - b*c and p = a*b build the full partial-product term list (Dekker
+// errors of the leading products, plain binary64 sums of the highest kept
+// level) and renormalise ONCE.  The reference's _fr is one distillation
+// pass with the fixpoint renorm_terms as fallback when the pass is not
+// strict, i.e. renorm_terms itself for finite terms (same VecSum, same
+// zero-eliminating extraction, same strictness test, same -0 -> +0
+// normalisation); renorm<M,K> is the device twin of renorm_terms.
+// ---------------------------------------------------------------------
+template <int K>
+MPK_HD void fmulsub(const double (&a)[K], const double (&b)[K],
+                    const double (&c)[K], double (&out)[K]) {
+  static_assert(K >= 2 && K <= 4, "fused ops: k = 2..4");
+  if constexpr (K == 2) {
+    double p, e;
+    two_prod(b[0], c[0], p, e);
+    double t[5] = {a[0], -p, a[1], -dadd(dmul(b[0], c[1]), dmul(b[1], c[0])), -e};
+    renorm<5, 2>(t, out);
+  } else if constexpr (K == 3) {
+    double p00, e00, p01, e01, p10, e10;
+    two_prod(b[0], c[0], p00, e00);
+    two_prod(b[0], c[1], p01, e01);
+    two_prod(b[1], c[0], p10, e10);
+    const double top = dadd(dadd(dmul(b[0], c[2]), dmul(b[1], c[1])), dmul(b[2], c[0]));
+    double t[10] = {a[0], -p00, a[1], -p01, -p10, -e00, a[2], -top, -e01, -e10};
+    renorm<10, 3>(t, out);
+  } else {
+    double p00, e00, p01, e01, p10, e10, p02, e02, p11, e11, p20, e20;
+    two_prod(b[0], c[0], p00, e00);
+    two_prod(b[0], c[1], p01, e01);
+    two_prod(b[1], c[0], p10, e10);
+    two_prod(b[0], c[2], p02, e02);
+    two_prod(b[1], c[1], p11, e11);
+    two_prod(b[2], c[0], p20, e20);
+    const double top = dadd(dadd(dadd(dmul(b[0], c[3]), dmul(b[1], c[2])), dmul(b[2], c[1])),
+                            dmul(b[3], c[0]));
+    double t[17] = {a[0], -p00, a[1], -p01, -p10, -e00, a[2], -p02, -p11,
+                    -p20, -e01, -e10, a[3], -top, -e02, -e11, -e20};
+    renorm<17, 4>(t, out);
+  }
+}
+
+template <int K>
+MPK_HD void fmul(const double (&a)[K], const double (&b)[K], double (&out)[K]) {
+  static_assert(K >= 2 && K <= 4, "fused ops: k = 2..4");
+  if constexpr (K == 2) {
+    double p, e;
+    two_prod(a[0], b[0], p, e);
+    double t[3] = {p, dadd(dmul(a[0], b[1]), dmul(a[1], b[0])), e};
+    renorm<3, 2>(t, out);
+  } else if constexpr (K == 3) {
+    double p00, e00, p01, e01, p10, e10;
+    two_prod(a[0], b[0], p00, e00);
+    two_prod(a[0], b[1], p01, e01);
+    two_prod(a[1], b[0], p10, e10);
+    const double top = dadd(dadd(dmul(a[0], b[2]), dmul(a[1], b[1])), dmul(a[2], b[0]));
+    double t[7] = {p00, p01, p10, e00, top, e01, e10};
+    renorm<7, 3>(t, out);
+  } else {
+    double p00, e00, p01, e01, p10, e10, p02, e02, p11, e11, p20, e20;
+    two_prod(a[0], b[0], p00, e00);
+    two_prod(a[0], b[1], p01, e01);
+    two_prod(a[1], b[0], p10, e10);
+    two_prod(a[0], b[2], p02, e02);
+    two_prod(a[1], b[1], p11, e11);
+    two_prod(a[2], b[0], p20, e20);
+    const double top = dadd(dadd(dadd(dmul(a[0], b[3]), dmul(a[1], b[2])), dmul(a[2], b[1])),
+                            dmul(a[3], b[0]));
+    double t[13] = {p00, p01, p10, e00, p02, p11, p20, e01, e10, top, e02, e11, e20};
+    renorm<13, 4>(t, out);
+  }
+}
+
 }  // namespace mpk

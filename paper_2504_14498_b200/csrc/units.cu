@@ -208,6 +208,8 @@ __host__ __device__ void mc_op_one(int op, const double *ar, const double *ai,
       o[1] = l;
       break;
     }
+    case 11: fmulsub<K>(a, b, c, o); break;  // a - b*c, c passed as a_im
+    case 12: fmul<K>(a, b, o); break;
     default: break;
   }
   for (int q = 0; q < K; ++q) {

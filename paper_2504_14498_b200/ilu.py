@@ -125,12 +125,47 @@ def ilu0_factorize_demoted(A) -> IluFactors:
     return _factor(A.demoted() if A.precision.k > 1 else A)
 
 
+class IluFactorsMC(IluFactors):
+    """Working-precision factors (k = 2..4, real) resident on the device
+    (csrc/ilu_mc.cu); ``val_re`` downloads them as (nnz, k).  The device
+    matrix keeps one such set (the latest k factorised)."""
+
+    def __init__(self, A, dev, precision):
+        super().__init__(A, dev)
+        self.precision = precision
+
+    def _download(self):
+        if self._host is None:
+            k = self.precision.k
+            lu = np.zeros((self.nnz, k))
+            _lib.check(_lib.lib().mpk_ilu0_download_full(self._dev.h, ctypes.c_int(k),
+                                                         _lib.dptr(lu)), "download_full")
+            self._host = (lu, None)
+        return self._host
+
+    @property
+    def val_re(self) -> np.ndarray:
+        return self._download()[0]
+
+
 def ilu0_factorize(A) -> IluFactors:
+    """Zero-fill ILU at the matrix's working precision (ilu.py:279-281): k = 1
+    binary64, k = 2..4 in K-component arithmetic with the reference's fused
+    a - b*c (real field, binary64-valued matrices on the device path)."""
     if A.precision.k == 1:
         return _factor(A)
-    raise NotImplementedError(
-        "full-precision ILU(0) (PrecondMode.ILU0_FULL) is not on the device path; "
-        "use ilu0_factorize_demoted / PrecondMode.ILU0_MIXED")
+    if A.val_im is not None or np.any(np.asarray(A.val_re)[:, 1:]):
+        raise NotImplementedError(
+            "working-precision ILU(0) on the B200 path: real, binary64-valued matrices")
+    d = device_matrix(A)
+    bad = ctypes.c_int64(-1)
+    st = ctypes.c_int32(0)
+    rc = _lib.lib().mpk_ilu0_factor_full(d.h, ctypes.c_int(A.precision.k), ctypes.byref(bad),
+                                         ctypes.byref(st))
+    if rc == _lib.MPK_SINGULAR_PIVOT:
+        raise SingularPivotError(int(bad.value), structural=bool(st.value))
+    _lib.check(rc, "mpk_ilu0_factor_full")
+    return IluFactorsMC(A, d, A.precision)
 
 
 def _check_apply(F: IluFactors, r: DenseVector):
@@ -157,7 +192,19 @@ def _apply_f64(F: IluFactors, r: DenseVector, adjoint: bool) -> DenseVector:
 
 
 def ilu0_apply(F: IluFactors, r: DenseVector) -> DenseVector:
-    """z = U^-1 (L^-1 r) on binary64 vectors (ilu.py:410-420)."""
+    """z = U^-1 (L^-1 r) at the factors' precision (ilu.py:410-420)."""
+    if isinstance(F, IluFactorsMC):
+        _check_apply(F, r)
+        if F.precision != r.precision:
+            raise ValueError("factor precision must match the vector precision")
+        k = F.precision.k
+        z = np.zeros((F.n, k))
+        rc = _lib.lib().mpk_ilu0_apply_full(F._dev.h, ctypes.c_int(k),
+                                            _lib.dptr(_lib.f64(r.re)), _lib.dptr(z))
+        if rc == _lib.MPK_NUMERIC_BREAKDOWN:
+            raise NumericBreakdownError("non-finite value in triangular sweep")
+        _lib.check(rc, "mpk_ilu0_apply_full")
+        return DenseVector(z, None, F.precision)
     return _apply_f64(F, r, False)
 
 

@@ -117,10 +117,10 @@ def _device_solve(A, b: DenseVector, cfg: SolverConfig, hist_cap: int | None = N
         raise ValueError(f"field mismatch: matrix {A.field}, vector {b.field}")
     if b.precision != cfg.precision:
         raise ValueError("vector precision must match cfg.precision")
-    if cfg.precond not in (PrecondMode.ILU0_MIXED, PrecondMode.NONE):
+    if cfg.precond == PrecondMode.ILU0_FULL and (A.field == "complex" or cfg.method == "bicg"):
         raise NotImplementedError(
-            "the B200 path implements precond ILU0_MIXED and NONE; the working-"
-            "precision ILU(0) ('ilu0') is listed in SURVEY.md section 8f")
+            "working-precision ILU(0) ('ilu0') on the B200 path: real field, "
+            "CGS / BiCGSTAB / GPBiCG")
     if cfg.spmv_mode == "full":
         # full SpMV on a matrix whose values are exactly binary64 IS the mixed
         # computation bit for bit (reference tests/test_sparse.py:130-147);
@@ -140,7 +140,8 @@ def _device_solve(A, b: DenseVector, cfg: SolverConfig, hist_cap: int | None = N
     x = DenseVector.zeros(n, cfg.precision, A.field)
     hist = np.zeros((max(hist_cap, 1), k))
     rep = _lib.MpkReport()
-    with _lib.precond_scope(d.ctx, cfg.precond == PrecondMode.ILU0_MIXED):
+    pre = {PrecondMode.NONE: 0, PrecondMode.ILU0_MIXED: 1, PrecondMode.ILU0_FULL: 2}[cfg.precond]
+    with _lib.precond_scope(d.ctx, pre):
         rc = _lib.lib().mpk_solve(
             d.h, ctypes.c_int(_lib.METHOD_CODE[cfg.method]), ctypes.c_int(k),
             ctypes.c_double(cfg.eps_rel), ctypes.c_double(cfg.eps_abs),
@@ -208,8 +209,8 @@ def _unit(x: DenseVector, v: float):
 def _method(name: str, A, b, cfg: SolverConfig, M=None) -> SolveReport:
     if M is None or isinstance(M, IdentityPreconditioner):  # M = I (reference default)
         pre = PrecondMode.NONE
-    elif isinstance(M, Ilu0Preconditioner) and M.mixed:
-        pre = PrecondMode.ILU0_MIXED
+    elif isinstance(M, Ilu0Preconditioner):
+        pre = PrecondMode.ILU0_MIXED if M.mixed else PrecondMode.ILU0_FULL
     else:
         raise NotImplementedError(
             f"{name}(M=...) on the B200 path takes M=None or an ILU(0)-mixed "

@@ -382,6 +382,71 @@ def gen_solver_none():
     np.savez_compressed(HERE / "solver_none.npz", **data)
 
 
+def gen_ilu_full():
+    """working-precision ILU(0) ('ilu0', ilu.py:279-281)
+    factors, applies and solves on the solver_small real system, plus the
+    cfg1 (convection-diffusion, k=2) factors and one apply."""
+    data = {}
+    rng = np.random.default_rng(31)
+    A64 = random_dd(rng, 60, 0.12, False)
+    n = A64.n
+    xt = rng.uniform(-1, 1, n)
+    r2 = np.random.default_rng(7)
+    for k in (2, 3, 4):
+        vre = np.zeros((len(A64.col_idx), k))
+        vre[:, 0] = A64.val_re[:, 0]
+        A = sparse.CsrMatrix(n, A64.row_ptr, A64.col_idx, vre, None, PREC[k])
+        F = ilu.ilu0_factorize(A)
+        data[f"k{k}_lu"] = F.val_re
+        rv = np.array([rand_mc(r2, k) for _ in range(n)])
+        data[f"k{k}_r"] = rv
+        data[f"k{k}_z"] = ilu.ilu0_apply(F, sparse.DenseVector(rv.copy(), None, PREC[k])).re
+        if k in (2, 3):
+            b = rhs(A64.val_re[:, 0], None, A64.row_ptr, A64.col_idx, n, k, x_true=xt)
+            tol = {2: 1e-25, 3: 1e-40}[k]
+            for m in ("cgs", "bicgstab", "gpbicg"):
+                o = run_ref(A64.val_re[:, 0], None, A64.row_ptr, A64.col_idx, n, b, m, k,
+                            tol, 1e-100, None, precond="ilu0")
+                for key, v in o.items():
+                    data[f"k{k}_{m}_{key}"] = v
+    p = problems.cfg1()
+    vre = np.zeros((p.nnz, 2))
+    vre[:, 0] = p.val_re
+    A = sparse.CsrMatrix(p.n, p.row_ptr, p.col_idx, vre, None, Precision.DD)
+    F = ilu.ilu0_factorize(A)
+    data["cfg1_lu"] = F.val_re
+    rv = np.array([rand_mc(r2, 2) for _ in range(p.n)])
+    data["cfg1_r"] = rv
+    data["cfg1_z"] = ilu.ilu0_apply(F, sparse.DenseVector(rv.copy(), None, Precision.DD)).re
+    np.savez_compressed(HERE / "ilu_full.npz", **data)
+
+
+def gen_mc_fused():
+    """_mcfast fused sweep primitives (rmulsubK / rmulK) of the working-
+    precision ILU(0) on seeded MC operands, incl. cancellation a ~ b*c."""
+    from mpkrylov import _mcfast
+
+    data = {}
+    rng = np.random.default_rng(91)
+    for k in (2, 3, 4):
+        A, B, C, MS, MU = [], [], [], [], []
+        for t in range(400):
+            a, b, c = rand_mc(rng, k, 10.0 ** rng.integers(-8, 9)), rand_mc(rng, k), rand_mc(rng, k)
+            if t % 4 == 1:  # near-total cancellation
+                a = _mcfast._RMUL[k](b, c)
+                a = _mccore.renorm_terms(list(a) + [rng.standard_normal() * 1e-40], k)
+            if t % 8 == 3:
+                a = (0.0,) * k
+            A.append(a)
+            B.append(b)
+            C.append(c)
+            MS.append(_mcfast._RMULSUB[k](a, b, c))
+            MU.append(_mcfast._RMUL[k](a, b))
+        data[f"k{k}_a"], data[f"k{k}_b"], data[f"k{k}_c"] = np.array(A), np.array(B), np.array(C)
+        data[f"k{k}_mulsub"], data[f"k{k}_mul"] = np.array(MS), np.array(MU)
+    np.savez_compressed(HERE / "mc_fused.npz", **data)
+
+
 def mm_texts():
     """Synthetic Matrix Market files for the f3 fixtures: every field /
     symmetry, duplicated entries (exact MC sums), comments, blank lines."""
@@ -509,6 +574,12 @@ if __name__ == "__main__":
     if "small" in what:
         gen_solver_small()
         print("solver_small done", time.time() - t0, flush=True)
+    if "ilufull" in what:
+        gen_ilu_full()
+        print("ilufull done", time.time() - t0, flush=True)
+    if "fused" in what:
+        gen_mc_fused()
+        print("fused done", time.time() - t0, flush=True)
     if "mm" in what:
         gen_mm()
         print("mm done", time.time() - t0, flush=True)

@@ -555,3 +555,66 @@ def test_device_precond_none_per_method_entry(pkg):
     cfg = pkg.SolverConfig(method="bicgstab", precision=P, eps_rel=1e-25, eps_abs=1e-100)
     rep = pkg.bicgstab(A.promoted(P), b, cfg, M=None)
     assert rep.iterations == int(gn["r2_none_bicgstab_iterations"])
+
+
+# ---------------------------------------------------------------------------
+# working-precision ILU(0) (precond 'ilu0', csrc/ilu_mc.cu)
+# against the reference's own factors / applies / solves (ilu_full.npz,
+# mc_fused.npz): bitwise.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_device_fused_ops_bitwise(L, k):
+    g = golden("mc_fused.npz")
+    A, B, C = g[f"k{k}_a"], g[f"k{k}_b"], g[f"k{k}_c"]
+    ms = dev_mc(L, 11, k, A, B, ai=C)
+    mu = dev_mc(L, 12, k, A, B)
+    assert bits_equal(ms, g[f"k{k}_mulsub"])
+    assert bits_equal(mu, g[f"k{k}_mul"])
+
+
+def _small_real(pkg, k):
+    g = golden("solver_small.npz")
+    rp, ci, v = g["r_rp"], g["r_ci"], g["r_vre"]
+    P = getattr(pkg.Precision, PREC_OF[k])
+    return _csr(pkg, rp, ci, v, None).promoted(P), g, P
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_device_ilu0_full_factors_and_apply(pkg, k):
+    gf = golden("ilu_full.npz")
+    A, g, P = _small_real(pkg, k)
+    F = pkg.ilu0_factorize(A)
+    assert bits_equal(F.val_re, gf[f"k{k}_lu"])
+    z = pkg.ilu0_apply(F, pkg.DenseVector(gf[f"k{k}_r"].copy(), None, P))
+    assert bits_equal(z.re, gf[f"k{k}_z"])
+
+
+def test_device_ilu0_full_cfg1(pkg):
+    from paper_2504_14498_b200 import problems
+
+    gf = golden("ilu_full.npz")
+    p = problems.cfg1()
+    A = pkg.CsrMatrix.from_binary64(p.n, p.row_ptr, p.col_idx, p.val_re, None, pkg.Precision.DD)
+    F = pkg.ilu0_factorize(A)
+    assert bits_equal(F.val_re, gf["cfg1_lu"])
+    z = pkg.ilu0_apply(F, pkg.DenseVector(gf["cfg1_r"].copy(), None, pkg.Precision.DD))
+    assert bits_equal(z.re, gf["cfg1_z"])
+
+
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("method", ["cgs", "bicgstab", "gpbicg"])
+def test_device_ilu0_full_solve(pkg, k, method):
+    gf = golden("ilu_full.npz")
+    A, g, P = _small_real(pkg, k)
+    b = pkg.DenseVector(g[f"r{k}_b_re"].copy(), None, P)
+    cfg = pkg.SolverConfig(method=method, precision=P, precond=pkg.PrecondMode.ILU0_FULL,
+                           spmv_mode="mixed", eps_rel=TOL[k], eps_abs=1e-100)
+    pre = f"k{k}_{method}"
+    with pkg.reduction_mode("sequential"):
+        twin = pkg.solve(A, b, cfg)
+    assert twin.iterations == int(gf[f"{pre}_iterations"]) and twin.converged
+    assert bits_equal(np.asarray(twin.history), gf[f"{pre}_hist"])
+    assert bits_equal(twin.x.re, gf[f"{pre}_x_re"])
+    rep = pkg.solve(A, b, cfg)
+    assert rep.iterations == int(gf[f"{pre}_iterations"])
+    _hist_check(rep.history, gf[f"{pre}_hist"], k)
