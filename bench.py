@@ -74,6 +74,16 @@ def cells_for(config: str, rank: int, world: int):
     return [(p, m, lab[pr]) for pr in p.precisions for m in p.methods]
 
 
+PRECOND_CODE = {"none": 0, "ilu0-mixed": 1, "ilu0": 2}
+
+
+def precond_supports(precond: str, p, method: str) -> bool:
+    """The working-precision ILU(0) runs real CGS / BiCGSTAB / GPBiCG."""
+    if precond == "ilu0":
+        return p.val_im is None and method != "bicg"
+    return True
+
+
 def algorithmic_apply_bytes(p) -> float:
     """ILU apply = nnz(8c+4) + 4(n+1) + 4n + 4F."""
     c = 2 if p.val_im is not None else 1
@@ -270,12 +280,20 @@ def run_ours(args, rank, world, local_rank):
     # one context (= CUDA stream) per cell: the cells of a step are independent
     # solves and run concurrently, like the reference harness's thread pool
     # over cells (bench.py:211-215)
+    pre = PRECOND_CODE[args.precond]
+
     def new_ctx():
         h = ctypes.c_void_p()
         _lib.check(L.mpk_ctx_create(ctypes.c_int(local_rank), ctypes.byref(h)), "ctx")
+        _lib.check(L.mpk_ctx_set_option(h, ctypes.c_int(_lib.MPK_OPT_PRECOND),
+                                        ctypes.c_int64(pre)), "precond")
         return h
+    if not args.concurrent:
+        _lib.check(L.mpk_ctx_set_option(ctx, ctypes.c_int(_lib.MPK_OPT_PRECOND),
+                                        ctypes.c_int64(pre)), "precond")
     cells = [Cell(L, _lib, p, m, k, new_ctx() if args.concurrent else ctx)
-             for (p, m, k) in cells_for(args.config, rank, world)]
+             for (p, m, k) in cells_for(args.config, rank, world)
+             if precond_supports(args.precond, p, m)]
     dist = world > 1
     if dist:
         import torch.distributed as tdist
@@ -375,6 +393,9 @@ def run_ours(args, rank, world, local_rank):
             continue
         seen.add(key)
         avg = ctypes.c_double(0)
+        if args.precond != "ilu0-mixed":  # the probe times the binary64 apply
+            bad, stc = ctypes.c_int64(0), ctypes.c_int32(0)
+            _lib.check(L.mpk_ilu0_factor(c.m, ctypes.byref(bad), ctypes.byref(stc)), "factor")
         _lib.check(L.mpk_bench_apply(c.m, ctypes.c_int(c.k), ctypes.c_int(20),
                                      ctypes.byref(avg)), "bench_apply")
         probe.append((c, avg.value))
@@ -577,6 +598,7 @@ def run_reference(args):
 def config_dict(args):
     d = {"workload": args.config, "l2_policy": "inputs L2-resident (cfg2 working set "
                                               "< 126 MB); no flush, iterations are chained"}
+
     if args.config == "cfg2":
         d.update({"system": "random nonsymmetric n=20000, 12 off-diag/row, seed 2",
                   "cells": "bicg,cgs,bicgstab,gpbicg x td,qd", "precond": "ilu0-mixed",
@@ -584,6 +606,9 @@ def config_dict(args):
     elif args.config == "cfg5":
         d.update({"system": "8 random nonsymmetric n=50000 systems per GPU",
                   "cells": "cgs,bicgstab x qd", "tol": 1e-40})
+    if args.precond != "ilu0-mixed":
+        d["precond"] = args.precond + (" (real CGS/BiCGSTAB/GPBiCG cells only)"
+                                       if args.precond == "ilu0" else "")
     return d
 
 
@@ -595,6 +620,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precond", default="ilu0-mixed", choices=list(PRECOND_CODE),
+                    help="preconditioner of every cell (the paper's ILU(0)_d = ilu0-mixed, "
+                         "ILU(0) = ilu0 at working precision, or none)")
     ap.add_argument("--shard", action="store_true",
                     help="cfg4: the row-block sharded path also at N=1")
     ap.add_argument("--serial", dest="concurrent", action="store_false",
