@@ -123,6 +123,8 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural);
 int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *structural);
 int mpk_ilu0_download_full(mpk_matrix *m, int k, double *lu);
 int mpk_ilu0_apply_full(mpk_matrix *m, int k, const double *r, double *z);
+/* adjoint != 0: ilu0_apply_adjoint (ilu.py:423-433) */
+int mpk_ilu0_apply_full_ex(mpk_matrix *m, int k, const double *r, double *z, int adjoint);
 /* IluFactors.val_re / val_im as (nnz,) arrays (bitwise parity tests) */
 int mpk_ilu0_download(mpk_matrix *m, double *lu_re, double *lu_im);
 /* ilu0_apply on binary64 vectors (ilu.py:410-433): z = U^-1 L^-1 r, or the

@@ -51,6 +51,7 @@ EXPORTS = (
     "mpk_comm_unique_id", "mpk_comm_create", "mpk_comm_create_local", "mpk_comm_destroy",
     "mpk_comm_rank", "mpk_comm_world", "mpk_solve_dev_sharded",
     "mpk_ilu0_factor_full", "mpk_ilu0_download_full", "mpk_ilu0_apply_full",
+    "mpk_ilu0_apply_full_ex",
 )
 
 MPK_OPT_REDUCTION = 1

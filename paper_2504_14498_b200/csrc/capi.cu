@@ -1015,6 +1015,7 @@ void mpk_csr_free(mpk_matrix *m) {
   if (A.lu_mc) cudaFree(A.lu_mc);
   if (A.rcp_mc) cudaFree(A.rcp_mc);
   if (A.sw_mc) cudaFree(A.sw_mc);
+  if (A.sw_mc2) cudaFree(A.sw_mc2);
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete m;
@@ -1122,10 +1123,12 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
     if (A.lu_mc) cudaFree(A.lu_mc);
     if (A.rcp_mc) cudaFree(A.rcp_mc);
     if (A.sw_mc) cudaFree(A.sw_mc);
-    A.lu_mc = A.rcp_mc = A.sw_mc = nullptr;
+    if (A.sw_mc2) cudaFree(A.sw_mc2);
+    A.lu_mc = A.rcp_mc = A.sw_mc = A.sw_mc2 = nullptr;
     CKR(cudaMalloc(&A.lu_mc, sizeof(double) * k * (A.nnz ? A.nnz : 1)));
     CKR(cudaMalloc(&A.rcp_mc, sizeof(double) * k * (A.n ? A.n : 1)));
     CKR(cudaMalloc(&A.sw_mc, sizeof(double) * k * L + 16));
+    CKR(cudaMalloc(&A.sw_mc2, sizeof(double) * k * L + 16));
     A.lu_mc_k = k;
   }
   A.mc_factored = false;
@@ -1183,9 +1186,14 @@ int mpk_ilu0_download_full(mpk_matrix *m, int k, double *lu) {
   return MPK_OK;
 }
 
-// ilu0_apply (ilu.py:410-420) at working precision, (n,k) host arrays
+// ilu0_apply / ilu0_apply_adjoint (ilu.py:410-433) at working precision,
+// (n,k) host arrays
 int mpk_ilu0_apply_full(mpk_matrix *m, int k, const double *r, double *z) {
+  return mpk_ilu0_apply_full_ex(m, k, r, z, 0);
+}
+int mpk_ilu0_apply_full_ex(mpk_matrix *m, int k, const double *r, double *z, int adjoint) {
   DMat &A = m->A;
+  if (adjoint) ensure_adjoint(A, m->ctx->stream);
   if (!A.mc_factored || A.lu_mc_k != k) return fail(MPK_INVALID, "no working-precision factors");
   CKR(cudaSetDevice(m->ctx->device));
   cudaStream_t st = m->ctx->stream;
@@ -1211,6 +1219,13 @@ int mpk_ilu0_apply_full(mpk_matrix *m, int k, const double *r, double *z) {
   a.tick = A.tick;
   a.err = A.err;
   a.done = nullptr;
+  a.adjoint = adjoint;
+  a.ut_rp = A.ut_rp;
+  a.ut_ci = A.ut_ci;
+  a.ut_perm = A.ut_perm;
+  a.lt_rp = A.lt_rp;
+  a.lt_ci = A.lt_ci;
+  a.lt_perm = A.lt_perm;
   launch_sweep_mc(a, k, st);
   launch_from_planar(n, k, dz, stage, nullptr, st);
   CKR(cudaMemcpyAsync(z, stage, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
@@ -1628,9 +1643,8 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   const bool ilu = pre != MPK_PRECOND_NONE;
   if (pre != MPK_PRECOND_ILU0_MIXED && ex)
     return fail(MPK_INVALID, "sharded solve: ILU(0)-mixed only");
-  if (pre == MPK_PRECOND_ILU0_FULL && (m->A.cx || method == MPK_BICG))
-    return fail(MPK_INVALID,
-                "working-precision ILU(0) on the B200 path: real field, CGS / BiCGSTAB / GPBiCG");
+  if (pre == MPK_PRECOND_ILU0_FULL && m->A.cx)
+    return fail(MPK_INVALID, "working-precision ILU(0) on the B200 path: real field");
   int rc = MPK_OK;
   if (pre == MPK_PRECOND_ILU0_MIXED)
     rc = mpk_ilu0_factor(m, &bad, &structural);

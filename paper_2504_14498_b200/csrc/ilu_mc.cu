@@ -200,6 +200,64 @@ __global__ void __launch_bounds__(256) sweep_mc_kernel(SweepMcArgs a) {
   mc_exit(a.tick);
 }
 
+// (LU)^-T at working precision, real (ilu.py:346-371, ilu0_apply_adjoint
+// :423-433): U^T forward in gather form -- row c folds the scatter
+// contributions of rows j < c in ascending j, then RealDiag.solve; L^T
+// backward -- row c folds rows j > c in descending j, no division.
+template <int K>
+__global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
+  if (a.done && *a.done) return;
+  const int lane = threadIdx.x & 31;
+  const int n = a.n;
+  const long long ld = a.ld;
+  for (;;) {
+    const int base = mc_grab(a.tick);
+    if (base >= 2 * n) break;
+    const int t = base + lane;
+    if (t < n) {
+      const int c = t;
+      double acc[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) acc[q] = a.in[q * ld + c];
+      for (int p = a.ut_rp[c]; p < a.ut_rp[c + 1]; ++p) {
+        double y[K], u[K], r[K];
+        poll_mc<K>(a.y, ld, a.ut_ci[p], y);
+        const long long e = a.ut_perm[p];
+#pragma unroll
+        for (int q = 0; q < K; ++q) u[q] = a.lu[e * K + q];
+        fmulsub<K>(acc, u, y, r);
+#pragma unroll
+        for (int q = 0; q < K; ++q) acc[q] = r[q];
+      }
+      double rc[K], o[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) rc[q] = a.rcp[(size_t)c * K + q];
+      fmul<K>(acc, rc, o);
+      pub_mc<K>(a.y, ld, c, o);
+    } else if (t < 2 * n) {
+      const int c = 2 * n - 1 - t;
+      double acc[K];
+      poll_mc<K>(a.y, ld, c, acc);
+      for (int p = a.lt_rp[c]; p < a.lt_rp[c + 1]; ++p) {
+        double z[K], l[K], r[K];
+        poll_mc<K>(a.z, ld, a.lt_ci[p], z);
+        const long long e = a.lt_perm[p];
+#pragma unroll
+        for (int q = 0; q < K; ++q) l[q] = a.lu[e * K + q];
+        fmulsub<K>(acc, l, z, r);
+#pragma unroll
+        for (int q = 0; q < K; ++q) acc[q] = r[q];
+      }
+      bool fin = true;
+#pragma unroll
+      for (int q = 0; q < K; ++q) fin = fin && isfin(acc[q]);
+      if (!fin) atomicOr(a.err, 1);
+      pub_mc<K>(a.z, ld, c, acc);
+    }
+  }
+  mc_exit(a.tick);
+}
+
 template <int K>
 __global__ void reset_mc_kernel(double *y, double *z, int n, const int *done) {
   if (done && *done) return;
@@ -244,6 +302,12 @@ void launch_sweep_mc(const SweepMcArgs &a, int k, cudaStream_t st) {
   long long blocks = (warps + 7) / 8;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 6) blocks = 148 * 6;
+  if (a.adjoint) {
+    if (k == 2) sweep_mc_adj_kernel<2><<<(int)blocks, 256, 0, st>>>(a);
+    if (k == 3) sweep_mc_adj_kernel<3><<<(int)blocks, 256, 0, st>>>(a);
+    if (k == 4) sweep_mc_adj_kernel<4><<<(int)blocks, 256, 0, st>>>(a);
+    return;
+  }
   if (k == 2) sweep_mc_kernel<2><<<(int)blocks, 256, 0, st>>>(a);
   if (k == 3) sweep_mc_kernel<3><<<(int)blocks, 256, 0, st>>>(a);
   if (k == 4) sweep_mc_kernel<4><<<(int)blocks, 256, 0, st>>>(a);

@@ -25,6 +25,10 @@ struct SweepMcArgs {
   int *tick;
   int *err;
   const int *done;
+  // adjoint (BiCG, ilu.py:346-371): gathers over U^T (ascending source
+  // rows) and L^T (descending), values at lu[perm[q]]
+  int adjoint;
+  const int *ut_rp, *ut_ci, *ut_perm, *lt_rp, *lt_ci, *lt_perm;
 };
 void launch_factor_mc(const FactorMcArgs &a, int k, cudaStream_t st);
 void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k,

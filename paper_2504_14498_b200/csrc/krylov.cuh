@@ -76,7 +76,7 @@ struct DMat {
   bool smat_built = false, smat_adj_built = false;
   // working-precision ILU(0) (precond 'ilu0', ilu_mc.cu): [nnz][K] factors,
   // [n][K] reciprocal diagonals, planar K-component sweep scratch
-  double *lu_mc = nullptr, *rcp_mc = nullptr, *sw_mc = nullptr;
+  double *lu_mc = nullptr, *rcp_mc = nullptr, *sw_mc = nullptr, *sw_mc2 = nullptr;
   int lu_mc_k = 0;
   bool mc_factored = false;
   int *tick = nullptr;  // 4 ints: [0..1] sweep A, [2..3] sweep B

@@ -295,7 +295,7 @@ struct Solver : PlanBase {
     if (nopre) {
       (void)in_im;
       if (p.precond_ilu == 2) {  // working-precision ILU(0) (ilu_mc.cu)
-        mc_sweep(in_re, z, which, after_loop, st);
+        mc_sweep(in_re, z, which, after_loop, st, adjoint);
         return;
       }
       // M = I (and M^H = I): the MC vector itself
@@ -314,8 +314,15 @@ struct Solver : PlanBase {
   }
   // z = U^-1 L^-1 in at working precision (real; planar K-component)
   void mc_sweep(const double *in, double *z, int which, bool after_loop,
-                cudaStream_t s_) {
+                cudaStream_t s_, bool adjoint = false) {
     SweepMcArgs a{};
+    a.adjoint = adjoint ? 1 : 0;
+    a.ut_rp = A.ut_rp;
+    a.ut_ci = A.ut_ci;
+    a.ut_perm = A.ut_perm;
+    a.lt_rp = A.lt_rp;
+    a.lt_ci = A.lt_ci;
+    a.lt_perm = A.lt_perm;
     a.n = n;
     a.ld = ld;
     a.rp = A.rp;
@@ -324,7 +331,7 @@ struct Solver : PlanBase {
     a.lu = A.lu_mc;
     a.rcp = A.rcp_mc;
     a.in = in;
-    a.y = A.sw_mc;
+    a.y = which ? A.sw_mc2 : A.sw_mc;  // BiCG runs both applies concurrently
     a.z = z;
     a.tick = A.tick + 2 * which;
     a.err = A.err;
@@ -342,7 +349,7 @@ struct Solver : PlanBase {
                 bool after_loop = false) {
     if (nopre) {
       if (p.precond_ilu == 2) {
-        mc_sweep(in_re, z, which, after_loop, s_);
+        mc_sweep(in_re, z, which, after_loop, s_, adjoint);
         return;
       }
       cudaMemcpyAsync(z, in_re, sizeof(double) * K * (CX ? 2 : 1) * ld,

@@ -191,25 +191,31 @@ def _apply_f64(F: IluFactors, r: DenseVector, adjoint: bool) -> DenseVector:
                        Precision.F64)
 
 
+def _apply_full(F, r: DenseVector, adjoint: bool) -> DenseVector:
+    _check_apply(F, r)
+    if F.precision != r.precision:
+        raise ValueError("factor precision must match the vector precision")
+    k = F.precision.k
+    z = np.zeros((F.n, k))
+    rc = _lib.lib().mpk_ilu0_apply_full_ex(F._dev.h, ctypes.c_int(k), _lib.dptr(_lib.f64(r.re)),
+                                           _lib.dptr(z), ctypes.c_int(int(adjoint)))
+    if rc == _lib.MPK_NUMERIC_BREAKDOWN:
+        raise NumericBreakdownError("non-finite value in triangular sweep")
+    _lib.check(rc, "mpk_ilu0_apply_full_ex")
+    return DenseVector(z, None, F.precision)
+
+
 def ilu0_apply(F: IluFactors, r: DenseVector) -> DenseVector:
     """z = U^-1 (L^-1 r) at the factors' precision (ilu.py:410-420)."""
     if isinstance(F, IluFactorsMC):
-        _check_apply(F, r)
-        if F.precision != r.precision:
-            raise ValueError("factor precision must match the vector precision")
-        k = F.precision.k
-        z = np.zeros((F.n, k))
-        rc = _lib.lib().mpk_ilu0_apply_full(F._dev.h, ctypes.c_int(k),
-                                            _lib.dptr(_lib.f64(r.re)), _lib.dptr(z))
-        if rc == _lib.MPK_NUMERIC_BREAKDOWN:
-            raise NumericBreakdownError("non-finite value in triangular sweep")
-        _lib.check(rc, "mpk_ilu0_apply_full")
-        return DenseVector(z, None, F.precision)
+        return _apply_full(F, r, False)
     return _apply_f64(F, r, False)
 
 
 def ilu0_apply_adjoint(F: IluFactors, r: DenseVector) -> DenseVector:
     """z = (LU)^-H r (ilu.py:423-433)."""
+    if isinstance(F, IluFactorsMC):
+        return _apply_full(F, r, True)
     return _apply_f64(F, r, True)
 
 

@@ -401,10 +401,12 @@ def gen_ilu_full():
         rv = np.array([rand_mc(r2, k) for _ in range(n)])
         data[f"k{k}_r"] = rv
         data[f"k{k}_z"] = ilu.ilu0_apply(F, sparse.DenseVector(rv.copy(), None, PREC[k])).re
+        data[f"k{k}_zadj"] = ilu.ilu0_apply_adjoint(
+            F, sparse.DenseVector(rv.copy(), None, PREC[k])).re
         if k in (2, 3):
             b = rhs(A64.val_re[:, 0], None, A64.row_ptr, A64.col_idx, n, k, x_true=xt)
             tol = {2: 1e-25, 3: 1e-40}[k]
-            for m in ("cgs", "bicgstab", "gpbicg"):
+            for m in ("bicg", "cgs", "bicgstab", "gpbicg"):
                 o = run_ref(A64.val_re[:, 0], None, A64.row_ptr, A64.col_idx, n, b, m, k,
                             tol, 1e-100, None, precond="ilu0")
                 for key, v in o.items():

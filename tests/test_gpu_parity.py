@@ -587,6 +587,8 @@ def test_device_ilu0_full_factors_and_apply(pkg, k):
     assert bits_equal(F.val_re, gf[f"k{k}_lu"])
     z = pkg.ilu0_apply(F, pkg.DenseVector(gf[f"k{k}_r"].copy(), None, P))
     assert bits_equal(z.re, gf[f"k{k}_z"])
+    za = pkg.ilu0_apply_adjoint(F, pkg.DenseVector(gf[f"k{k}_r"].copy(), None, P))
+    assert bits_equal(za.re, gf[f"k{k}_zadj"])
 
 
 def test_device_ilu0_full_cfg1(pkg):
@@ -602,7 +604,7 @@ def test_device_ilu0_full_cfg1(pkg):
 
 
 @pytest.mark.parametrize("k", [2, 3])
-@pytest.mark.parametrize("method", ["cgs", "bicgstab", "gpbicg"])
+@pytest.mark.parametrize("method", ["bicg", "cgs", "bicgstab", "gpbicg"])
 def test_device_ilu0_full_solve(pkg, k, method):
     gf = golden("ilu_full.npz")
     A, g, P = _small_real(pkg, k)
