@@ -96,8 +96,8 @@ void *mpk_ctx_stream(mpk_ctx *ctx);
 #define MPK_PRECOND_ILU0_MIXED 1
 /* MPK_PRECOND_ILU0_FULL: ILU(0) at the working precision (ilu.py:279-281;
  * factors and sweeps in k-component arithmetic with the _mcfast fused
- * a - b*c, _mcfast.py:80-183, 390-402); real field, CGS / BiCGSTAB /
- * GPBiCG */
+ * a - b*c and diagonal solvers, _mcfast.py:80-439); all four methods,
+ * real and complex */
 #define MPK_PRECOND_ILU0_FULL 2
 int mpk_ctx_set_option(mpk_ctx *ctx, int option, int64_t value);
 
@@ -118,8 +118,9 @@ int mpk_csr_set_values(mpk_matrix *m, const double *val_re,
  * MPK_NUMERIC_BREAKDOWN for non-finite factors. */
 int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural);
 /* ilu0_factorize (ilu.py:279-281) of the uploaded binary64 matrix promoted
- * to k = 2..4 components (real); factors downloadable as (nnz,k) and
- * applicable to (n,k) vectors (ilu0_apply, ilu.py:410-420) */
+ * to k = 2..4 components; factors downloadable as (nnz,k) (complex:
+ * (nnz,2k) rows re[k] | im[k]) and applicable to (n,k) vectors (complex:
+ * the (n,k) re block followed by the (n,k) im block) */
 int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *structural);
 int mpk_ilu0_download_full(mpk_matrix *m, int k, double *lu);
 int mpk_ilu0_apply_full(mpk_matrix *m, int k, const double *r, double *z);

@@ -1096,10 +1096,16 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   return MPK_OK;
 }
 
-__global__ void promote_vals_kernel(long long nnz, int k, const double *v, double *o) {
+// binary64 values (complex: interleaved re, im) -> flat K-component
+// entries (complex: re[K], im[K]) with zero tails
+__global__ void promote_vals_kernel(long long nnz, int k, int cx, const double *v, double *o) {
+  const int w = cx ? 2 * k : k;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < nnz;
        p += (long long)gridDim.x * blockDim.x)
-    for (int c = 0; c < k; ++c) o[p * k + c] = c == 0 ? v[p] : 0.0;
+    for (int c = 0; c < w; ++c) {
+      const bool head = (c % k) == 0;
+      o[p * w + c] = !head ? 0.0 : (cx ? v[2 * p + c / k] : v[p]);
+    }
 }
 
 // ilu0_factorize (ilu.py:279-281 -> _factorize_tuples at precision k > 1) of
@@ -1108,7 +1114,7 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
   DMat &A = m->A;
   cudaStream_t st = m->ctx->stream;
   if (k < 2 || k > 4) return fail(MPK_INVALID, "working-precision ILU(0): k = 2..4");
-  if (A.cx) return fail(MPK_INVALID, "working-precision ILU(0): real field only");
+  const int W = A.cx ? 2 * k : k;
   CKR(cudaSetDevice(m->ctx->device));
   for (int i = 0; i < A.n; ++i) {  // _structural_check ilu.py:172-175
     if (A.h_dp[i] < 0) {
@@ -1125,16 +1131,16 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
     if (A.sw_mc) cudaFree(A.sw_mc);
     if (A.sw_mc2) cudaFree(A.sw_mc2);
     A.lu_mc = A.rcp_mc = A.sw_mc = A.sw_mc2 = nullptr;
-    CKR(cudaMalloc(&A.lu_mc, sizeof(double) * k * (A.nnz ? A.nnz : 1)));
-    CKR(cudaMalloc(&A.rcp_mc, sizeof(double) * k * (A.n ? A.n : 1)));
-    CKR(cudaMalloc(&A.sw_mc, sizeof(double) * k * L + 16));
-    CKR(cudaMalloc(&A.sw_mc2, sizeof(double) * k * L + 16));
+    CKR(cudaMalloc(&A.lu_mc, sizeof(double) * W * (A.nnz ? A.nnz : 1)));
+    CKR(cudaMalloc(&A.rcp_mc, sizeof(double) * (A.cx ? 2 * (2 * k + 1) : k) * (A.n ? A.n : 1)));
+    CKR(cudaMalloc(&A.sw_mc, sizeof(double) * W * L + 16));
+    CKR(cudaMalloc(&A.sw_mc2, sizeof(double) * W * L + 16));
     A.lu_mc_k = k;
   }
   A.mc_factored = false;
   if (A.nnz > 0) {
     ++tl_launches;
-    promote_vals_kernel<<<148 * 4, 256, 0, st>>>(A.nnz, k, A.val, A.lu_mc);
+    promote_vals_kernel<<<148 * 4, 256, 0, st>>>(A.nnz, k, A.cx ? 1 : 0, A.val, A.lu_mc);
   }
   CKR(cudaMemsetAsync(m->rowflag, 0, sizeof(int) * (A.n + 1), st));
   if (!m->hres) CKR(cudaMallocHost(&m->hres, sizeof(int) * 8));
@@ -1146,6 +1152,7 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
   CKR(cudaMemcpyAsync(m->fscratch, init, sizeof(int) * 4, cudaMemcpyHostToDevice, st));
   FactorMcArgs fa{};
   fa.n = A.n;
+  fa.cx = A.cx ? 1 : 0;
   fa.rp = A.rp;
   fa.ci = A.ci;
   fa.dp = A.dp;
@@ -1173,7 +1180,7 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
                                         std::to_string(res[2]) + "]");
   }
   if (res[3]) return fail(MPK_NUMERIC_BREAKDOWN, "non-finite value in ILU(0) factors");
-  launch_recip_mc(A.n, A.dp, A.lu_mc, A.rcp_mc, k, st);
+  launch_recip_mc(A.n, A.dp, A.lu_mc, A.rcp_mc, k, A.cx, st);
   A.mc_factored = true;
   return MPK_OK;
 }
@@ -1182,7 +1189,8 @@ int mpk_ilu0_download_full(mpk_matrix *m, int k, double *lu) {
   DMat &A = m->A;
   if (!A.mc_factored || A.lu_mc_k != k) return fail(MPK_INVALID, "no working-precision factors");
   CKR(cudaSetDevice(m->ctx->device));
-  CKR(cudaMemcpy(lu, A.lu_mc, sizeof(double) * k * A.nnz, cudaMemcpyDeviceToHost));
+  CKR(cudaMemcpy(lu, A.lu_mc, sizeof(double) * (A.cx ? 2 * k : k) * A.nnz,
+                 cudaMemcpyDeviceToHost));
   return MPK_OK;
 }
 
@@ -1199,11 +1207,12 @@ int mpk_ilu0_apply_full_ex(mpk_matrix *m, int k, const double *r, double *z, int
   cudaStream_t st = m->ctx->stream;
   const long long n = A.n, L = plane_ld(A.n);
   double *din = nullptr, *dz = nullptr, *stage = nullptr;
-  CKR(cudaMalloc(&din, sizeof(double) * k * L + 16));
-  CKR(cudaMalloc(&dz, sizeof(double) * k * L + 16));
-  CKR(cudaMalloc(&stage, sizeof(double) * k * (n ? n : 1)));
-  CKR(cudaMemcpyAsync(stage, r, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
-  launch_to_planar(n, k, stage, nullptr, din, st);
+  const int c2 = A.cx ? 2 : 1;
+  CKR(cudaMalloc(&din, sizeof(double) * c2 * k * L + 16));
+  CKR(cudaMalloc(&dz, sizeof(double) * c2 * k * L + 16));
+  CKR(cudaMalloc(&stage, sizeof(double) * c2 * k * (n ? n : 1)));
+  CKR(cudaMemcpyAsync(stage, r, sizeof(double) * n * k * c2, cudaMemcpyHostToDevice, st));
+  launch_to_planar(n, k, stage, A.cx ? stage + n * k : nullptr, din, st);
   CKR(cudaMemsetAsync(A.err, 0, sizeof(int), st));
   SweepMcArgs a{};
   a.n = A.n;
@@ -1220,6 +1229,7 @@ int mpk_ilu0_apply_full_ex(mpk_matrix *m, int k, const double *r, double *z, int
   a.err = A.err;
   a.done = nullptr;
   a.adjoint = adjoint;
+  a.cx = A.cx ? 1 : 0;
   a.ut_rp = A.ut_rp;
   a.ut_ci = A.ut_ci;
   a.ut_perm = A.ut_perm;
@@ -1227,8 +1237,8 @@ int mpk_ilu0_apply_full_ex(mpk_matrix *m, int k, const double *r, double *z, int
   a.lt_ci = A.lt_ci;
   a.lt_perm = A.lt_perm;
   launch_sweep_mc(a, k, st);
-  launch_from_planar(n, k, dz, stage, nullptr, st);
-  CKR(cudaMemcpyAsync(z, stage, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
+  launch_from_planar(n, k, dz, stage, A.cx ? stage + n * k : nullptr, st);
+  CKR(cudaMemcpyAsync(z, stage, sizeof(double) * n * k * c2, cudaMemcpyDeviceToHost, st));
   int e = 0;
   CKR(cudaMemcpyAsync(&e, A.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   CKR(cudaStreamSynchronize(st));
@@ -1643,8 +1653,6 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   const bool ilu = pre != MPK_PRECOND_NONE;
   if (pre != MPK_PRECOND_ILU0_MIXED && ex)
     return fail(MPK_INVALID, "sharded solve: ILU(0)-mixed only");
-  if (pre == MPK_PRECOND_ILU0_FULL && m->A.cx)
-    return fail(MPK_INVALID, "working-precision ILU(0) on the B200 path: real field");
   int rc = MPK_OK;
   if (pre == MPK_PRECOND_ILU0_MIXED)
     rc = mpk_ilu0_factor(m, &bad, &structural);

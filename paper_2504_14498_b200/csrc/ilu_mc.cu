@@ -1,6 +1,6 @@
 // ilu_mc.cu -- working-precision ILU(0) (precond 'ilu0'):
 // factorization in K-component arithmetic and its forward / backward
-// sweeps on K-component vectors, real field.
+// sweeps on K-component vectors, real and complex fields.
 //
 // Reference: ilu.py:178-276 (_factorize_tuples with k > 1: lik = mc_div,
 // a_ij = _mcfast.rmulsubK(a_ij, lik, u_kj)), ilu.py:322-343 (sweeps:
@@ -74,8 +74,38 @@ __device__ __forceinline__ void pub_mc(double *v, long long ld, int j,
   str(v + j, unsent(x[0]));
 }
 
-template <int K>
+// value helpers on flat (re..., im...) arrays of W = K or 2K components
+template <int K, bool CX>
+__device__ __forceinline__ void mc_mulsub(const double *a, const double *b,
+                                          const double *c, double *o) {
+  if constexpr (CX) {
+    double ar[K], ai[K], br[K], bi[K], cr[K], ci[K], orr[K], oi[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      ar[q] = a[q]; ai[q] = a[K + q]; br[q] = b[q]; bi[q] = b[K + q];
+      cr[q] = c[q]; ci[q] = c[K + q];
+    }
+    fcmulsub<K>(ar, ai, br, bi, cr, ci, orr, oi);  // _mcfast.cmulsubK
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      o[q] = orr[q];
+      o[K + q] = oi[q];
+    }
+  } else {
+    double x[K], y[K], z[K], r[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      x[q] = a[q]; y[q] = b[q]; z[q] = c[q];
+    }
+    fmulsub<K>(x, y, z, r);  // _mcfast.rmulsubK
+#pragma unroll
+    for (int q = 0; q < K; ++q) o[q] = r[q];
+  }
+}
+
+template <int K, bool CX>
 __device__ void factor_mc_row(const FactorMcArgs &a, int i) {
+  constexpr int W = CX ? 2 * K : K;
   const int lo = a.rp[i], hi = a.rp[i + 1], d = a.dp[i];
   double *lu = a.lu;
   for (int t = lo; t < d; ++t) {
@@ -83,129 +113,176 @@ __device__ void factor_mc_row(const FactorMcArgs &a, int i) {
     while (ldri(&a.rowflag[kc]) == 0) __nanosleep(32);
     __threadfence();
     const int uk = a.dp[kc], kend = a.rp[kc + 1];
-    double at[K], ukk[K], l[K];
+    double at[W], ukk[W], l[W];
 #pragma unroll
-    for (int c = 0; c < K; ++c) {
-      at[c] = __ldcg(&lu[(size_t)t * K + c]);
-      ukk[c] = __ldcg(&lu[(size_t)uk * K + c]);
+    for (int c = 0; c < W; ++c) {
+      at[c] = __ldcg(&lu[(size_t)t * W + c]);
+      ukk[c] = __ldcg(&lu[(size_t)uk * W + c]);
     }
-    div<K>(at, ukk, l);  // mc_div (_mccore.py:222-237)
+    if constexpr (CX) {  // cx_div (_mccore.py:328-347), flat pair
+      double xr[K], xi[K], yr[K], yi[K], qr[K], qi[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) __stcg(&lu[(size_t)t * K + c], l[c]);
+      for (int q = 0; q < K; ++q) {
+        xr[q] = at[q]; xi[q] = at[K + q]; yr[q] = ukk[q]; yi[q] = ukk[K + q];
+      }
+      cdiv<K>(xr, xi, yr, yi, qr, qi);
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        l[q] = qr[q];
+        l[K + q] = qi[q];
+      }
+    } else {
+      double x[K], y[K], q2[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        x[q] = at[q];
+        y[q] = ukk[q];
+      }
+      div<K>(x, y, q2);  // mc_div (_mccore.py:222-237)
+#pragma unroll
+      for (int q = 0; q < K; ++q) l[q] = q2[q];
+    }
+#pragma unroll
+    for (int c = 0; c < W; ++c) __stcg(&lu[(size_t)t * W + c], l[c]);
     int q = t + 1;
     for (int s = uk + 1; s < kend; ++s) {
       const int col = a.ci[s];
       while (q < hi && a.ci[q] < col) ++q;
       if (q < hi && a.ci[q] == col) {
-        double v[K], u[K], r[K];
+        double v[W], u[W], r[W];
 #pragma unroll
-        for (int c = 0; c < K; ++c) {
-          v[c] = __ldcg(&lu[(size_t)q * K + c]);
-          u[c] = __ldcg(&lu[(size_t)s * K + c]);
+        for (int c = 0; c < W; ++c) {
+          v[c] = __ldcg(&lu[(size_t)q * W + c]);
+          u[c] = __ldcg(&lu[(size_t)s * W + c]);
         }
-        fmulsub<K>(v, l, u, r);  // _mcfast.rmulsubK(a_ij, lik, u_kj)
+        mc_mulsub<K, CX>(v, l, u, r);  // mulsub(a_ij, lik, u_kj)
 #pragma unroll
-        for (int c = 0; c < K; ++c) __stcg(&lu[(size_t)q * K + c], r[c]);
+        for (int c = 0; c < W; ++c) __stcg(&lu[(size_t)q * W + c], r[c]);
       }
     }
   }
   bool zero = true, fin = true;
 #pragma unroll
-  for (int c = 0; c < K; ++c) zero = zero && __ldcg(&lu[(size_t)d * K + c]) == 0.0;
+  for (int c = 0; c < W; ++c) zero = zero && __ldcg(&lu[(size_t)d * W + c]) == 0.0;
   for (int p = lo; p < hi; ++p)
-    for (int c = 0; c < K; ++c) fin = fin && isfin(__ldcg(&lu[(size_t)p * K + c]));
+    for (int c = 0; c < W; ++c) fin = fin && isfin(__ldcg(&lu[(size_t)p * W + c]));
   if (zero) atomicMin(a.bad_row, i);
   if (!fin) atomicOr(a.nonfinite, 1);
   __threadfence();
   atomicExch(&a.rowflag[i], 1);
 }
 
-template <int K>
+template <int K, bool CX>
 __global__ void __launch_bounds__(256) factor_mc_kernel(FactorMcArgs a) {
   const int lane = threadIdx.x & 31;
   for (;;) {
     const int base = mc_grab(a.tick);
     if (base >= a.n) break;
     const int t = base + lane;
-    if (t < a.n) factor_mc_row<K>(a, t);
+    if (t < a.n) factor_mc_row<K, CX>(a, t);
   }
   mc_exit(a.tick);
 }
 
-// RealDiag.recip = mc_div((1, 0..), U_ii) per row (_mcfast.py:390-402)
+// Diagonal solvers of the backward sweeps, per row (_mcfast.py:386-439):
+// real RealDiag.recip = mc_div(1, U_ii) [K]; complex ComplexDiag (Smith):
+// {t [K], recip [K], swapped} = 2K+1 values, for the plain sweep and, at
+// offset n*(2K+1), for the adjoint sweep (built from conj(U_ii)).
 template <int K>
+__device__ void complex_diag(const double (&dr)[K], const double (&di)[K], double *o) {
+  double one[K], t[K], den[K], tmp[K], rc[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) one[q] = q == 0 ? 1.0 : 0.0;
+  const bool swapped = !(fabs(dr[0]) >= fabs(di[0]));
+  if (!swapped) {
+    div<K>(di, dr, t);
+    mul<K>(di, t, tmp);
+    add<K>(dr, tmp, den);
+  } else {
+    div<K>(dr, di, t);
+    mul<K>(dr, t, tmp);
+    add<K>(tmp, di, den);
+  }
+  div<K>(one, den, rc);
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    o[q] = t[q];
+    o[K + q] = rc[q];
+  }
+  o[2 * K] = swapped ? 1.0 : 0.0;
+}
+
+template <int K, bool CX>
 __global__ void recip_mc_kernel(int n, const int *dp, const double *lu, double *rcp) {
+  constexpr int W = CX ? 2 * K : K;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double one[K], u[K], r[K];
+    if constexpr (CX) {
+      double dr[K], di[K], nd[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) {
-      one[c] = c == 0 ? 1.0 : 0.0;
-      u[c] = lu[(size_t)dp[i] * K + c];
+      for (int q = 0; q < K; ++q) {
+        dr[q] = lu[(size_t)dp[i] * W + q];
+        di[q] = lu[(size_t)dp[i] * W + K + q];
+        nd[q] = -di[q];
+      }
+      complex_diag<K>(dr, di, rcp + (size_t)i * (2 * K + 1));
+      complex_diag<K>(dr, nd, rcp + ((size_t)n + i) * (2 * K + 1));
+    } else {
+      double one[K], u[K], r[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        one[c] = c == 0 ? 1.0 : 0.0;
+        u[c] = lu[(size_t)dp[i] * K + c];
+      }
+      div<K>(one, u, r);
+#pragma unroll
+      for (int c = 0; c < K; ++c) rcp[(size_t)i * K + c] = r[c];
     }
-    div<K>(one, u, r);
-#pragma unroll
-    for (int c = 0; c < K; ++c) rcp[(size_t)i * K + c] = r[c];
   }
 }
 
-template <int K>
+// acc / U_ii through the precomputed diagonal solver (flat W components)
+template <int K, bool CX>
+__device__ __forceinline__ void diag_solve(const double *acc, const double *dg, double *o) {
+  if constexpr (CX) {  // ComplexDiag.solve
+    double xr[K], xi[K], nxr[K], nxi[K], t[K], rc[K], nr[K], ni[K], qr[K], qi[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      xr[q] = acc[q]; xi[q] = acc[K + q]; nxr[q] = -xr[q]; nxi[q] = -xi[q];
+      t[q] = dg[q]; rc[q] = dg[K + q];
+    }
+    if (dg[2 * K] == 0.0) {
+      fmulsub<K>(xr, nxi, t, nr);   // xr + xi*t
+      fmulsub<K>(xi, xr, t, ni);    // xi - xr*t
+    } else {
+      fmulsub<K>(xi, nxr, t, nr);   // xi + xr*t
+      fmulsub<K>(nxr, nxi, t, ni);  // xi*t - xr
+    }
+    fmul<K>(nr, rc, qr);
+    fmul<K>(ni, rc, qi);
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      o[q] = qr[q];
+      o[K + q] = qi[q];
+    }
+  } else {  // RealDiag.solve
+    double x[K], rc[K], q2[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      x[q] = acc[q];
+      rc[q] = dg[q];
+    }
+    fmul<K>(x, rc, q2);
+#pragma unroll
+    for (int q = 0; q < K; ++q) o[q] = q2[q];
+  }
+}
+
+template <int K, bool CX>
 __global__ void __launch_bounds__(256) sweep_mc_kernel(SweepMcArgs a) {
-  if (a.done && *a.done) return;
-  const int lane = threadIdx.x & 31;
-  const int n = a.n;
-  const long long ld = a.ld;
-  for (;;) {
-    const int base = mc_grab(a.tick);
-    if (base >= 2 * n) break;
-    const int t = base + lane;
-    if (t < n) {  // _sweep_forward ilu.py:322-331
-      const int i = t;
-      double acc[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) acc[c] = a.in[c * ld + i];
-      for (int p = a.rp[i]; p < a.dp[i]; ++p) {
-        double y[K], l[K], r[K];
-        poll_mc<K>(a.y, ld, a.ci[p], y);
-#pragma unroll
-        for (int c = 0; c < K; ++c) l[c] = a.lu[(size_t)p * K + c];
-        fmulsub<K>(acc, l, y, r);
-#pragma unroll
-        for (int c = 0; c < K; ++c) acc[c] = r[c];
-      }
-      pub_mc<K>(a.y, ld, i, acc);
-    } else if (t < 2 * n) {  // _sweep_backward ilu.py:334-343
-      const int i = 2 * n - 1 - t;
-      double acc[K];
-      poll_mc<K>(a.y, ld, i, acc);
-      for (int p = a.dp[i] + 1; p < a.rp[i + 1]; ++p) {
-        double z[K], u[K], r[K];
-        poll_mc<K>(a.z, ld, a.ci[p], z);
-#pragma unroll
-        for (int c = 0; c < K; ++c) u[c] = a.lu[(size_t)p * K + c];
-        fmulsub<K>(acc, u, z, r);
-#pragma unroll
-        for (int c = 0; c < K; ++c) acc[c] = r[c];
-      }
-      double rc[K], q[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) rc[c] = a.rcp[(size_t)i * K + c];
-      fmul<K>(acc, rc, q);  // RealDiag.solve
-      bool fin = true;
-#pragma unroll
-      for (int c = 0; c < K; ++c) fin = fin && isfin(q[c]);
-      if (!fin) atomicOr(a.err, 1);
-      pub_mc<K>(a.z, ld, i, q);
-    }
-  }
-  mc_exit(a.tick);
-}
-
-// (LU)^-T at working precision, real (ilu.py:346-371, ilu0_apply_adjoint
-// :423-433): U^T forward in gather form -- row c folds the scatter
-// contributions of rows j < c in ascending j, then RealDiag.solve; L^T
-// backward -- row c folds rows j > c in descending j, no division.
-template <int K>
-__global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
+  // _sweep_forward / _sweep_backward ilu.py:322-343 (flat W components;
+  // planar vectors: component q at q*ld, complex = K real then K imag)
+  constexpr int W = CX ? 2 * K : K;
+  constexpr int DW = CX ? 2 * K + 1 : K;
   if (a.done && *a.done) return;
   const int lane = threadIdx.x & 31;
   const int n = a.n;
@@ -215,50 +292,105 @@ __global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
     if (base >= 2 * n) break;
     const int t = base + lane;
     if (t < n) {
-      const int c = t;
-      double acc[K];
+      const int i = t;
+      double acc[W];
 #pragma unroll
-      for (int q = 0; q < K; ++q) acc[q] = a.in[q * ld + c];
-      for (int p = a.ut_rp[c]; p < a.ut_rp[c + 1]; ++p) {
-        double y[K], u[K], r[K];
-        poll_mc<K>(a.y, ld, a.ut_ci[p], y);
-        const long long e = a.ut_perm[p];
+      for (int c = 0; c < W; ++c) acc[c] = a.in[c * ld + i];
+      for (int p = a.rp[i]; p < a.dp[i]; ++p) {
+        double y[W], l[W], r[W];
+        poll_mc<W>(a.y, ld, a.ci[p], y);
 #pragma unroll
-        for (int q = 0; q < K; ++q) u[q] = a.lu[e * K + q];
-        fmulsub<K>(acc, u, y, r);
+        for (int c = 0; c < W; ++c) l[c] = a.lu[(size_t)p * W + c];
+        mc_mulsub<K, CX>(acc, l, y, r);
 #pragma unroll
-        for (int q = 0; q < K; ++q) acc[q] = r[q];
+        for (int c = 0; c < W; ++c) acc[c] = r[c];
       }
-      double rc[K], o[K];
-#pragma unroll
-      for (int q = 0; q < K; ++q) rc[q] = a.rcp[(size_t)c * K + q];
-      fmul<K>(acc, rc, o);
-      pub_mc<K>(a.y, ld, c, o);
+      pub_mc<W>(a.y, ld, i, acc);
     } else if (t < 2 * n) {
-      const int c = 2 * n - 1 - t;
-      double acc[K];
-      poll_mc<K>(a.y, ld, c, acc);
-      for (int p = a.lt_rp[c]; p < a.lt_rp[c + 1]; ++p) {
-        double z[K], l[K], r[K];
-        poll_mc<K>(a.z, ld, a.lt_ci[p], z);
-        const long long e = a.lt_perm[p];
+      const int i = 2 * n - 1 - t;
+      double acc[W];
+      poll_mc<W>(a.y, ld, i, acc);
+      for (int p = a.dp[i] + 1; p < a.rp[i + 1]; ++p) {
+        double z[W], u[W], r[W];
+        poll_mc<W>(a.z, ld, a.ci[p], z);
 #pragma unroll
-        for (int q = 0; q < K; ++q) l[q] = a.lu[e * K + q];
-        fmulsub<K>(acc, l, z, r);
+        for (int c = 0; c < W; ++c) u[c] = a.lu[(size_t)p * W + c];
+        mc_mulsub<K, CX>(acc, u, z, r);
 #pragma unroll
-        for (int q = 0; q < K; ++q) acc[q] = r[q];
+        for (int c = 0; c < W; ++c) acc[c] = r[c];
       }
+      double q[W];
+      diag_solve<K, CX>(acc, a.rcp + (size_t)i * DW, q);
       bool fin = true;
 #pragma unroll
-      for (int q = 0; q < K; ++q) fin = fin && isfin(acc[q]);
+      for (int c = 0; c < W; ++c) fin = fin && isfin(q[c]);
       if (!fin) atomicOr(a.err, 1);
-      pub_mc<K>(a.z, ld, c, acc);
+      pub_mc<W>(a.z, ld, i, q);
     }
   }
   mc_exit(a.tick);
 }
 
-template <int K>
+// (LU)^-H at working precision (ilu.py:346-371, ilu0_apply_adjoint
+// :423-433): U^H forward in gather form -- row c folds the scatter
+// contributions of rows j < c in ascending j with conjugated values, then
+// the diagonal solver of conj(U_cc); L^H backward -- row c folds rows j > c
+// in descending j, no division.
+template <int K, bool CX>
+__global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
+  constexpr int W = CX ? 2 * K : K;
+  constexpr int DW = CX ? 2 * K + 1 : K;
+  if (a.done && *a.done) return;
+  const int lane = threadIdx.x & 31;
+  const int n = a.n;
+  const long long ld = a.ld;
+  const double *dg0 = a.rcp + (CX ? (size_t)n * DW : 0);
+  for (;;) {
+    const int base = mc_grab(a.tick);
+    if (base >= 2 * n) break;
+    const int t = base + lane;
+    if (t < n) {
+      const int c = t;
+      double acc[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) acc[q] = a.in[q * ld + c];
+      for (int p = a.ut_rp[c]; p < a.ut_rp[c + 1]; ++p) {
+        double y[W], u[W], r[W];
+        poll_mc<W>(a.y, ld, a.ut_ci[p], y);
+        const long long e = a.ut_perm[p];
+#pragma unroll
+        for (int q = 0; q < W; ++q) u[q] = (CX && q >= K) ? -a.lu[e * W + q] : a.lu[e * W + q];
+        mc_mulsub<K, CX>(acc, u, y, r);
+#pragma unroll
+        for (int q = 0; q < W; ++q) acc[q] = r[q];
+      }
+      double o[W];
+      diag_solve<K, CX>(acc, dg0 + (size_t)c * DW, o);
+      pub_mc<W>(a.y, ld, c, o);
+    } else if (t < 2 * n) {
+      const int c = 2 * n - 1 - t;
+      double acc[W];
+      poll_mc<W>(a.y, ld, c, acc);
+      for (int p = a.lt_rp[c]; p < a.lt_rp[c + 1]; ++p) {
+        double z[W], l[W], r[W];
+        poll_mc<W>(a.z, ld, a.lt_ci[p], z);
+        const long long e = a.lt_perm[p];
+#pragma unroll
+        for (int q = 0; q < W; ++q) l[q] = (CX && q >= K) ? -a.lu[e * W + q] : a.lu[e * W + q];
+        mc_mulsub<K, CX>(acc, l, z, r);
+#pragma unroll
+        for (int q = 0; q < W; ++q) acc[q] = r[q];
+      }
+      bool fin = true;
+#pragma unroll
+      for (int q = 0; q < W; ++q) fin = fin && isfin(acc[q]);
+      if (!fin) atomicOr(a.err, 1);
+      pub_mc<W>(a.z, ld, c, acc);
+    }
+  }
+  mc_exit(a.tick);
+}
+
 __global__ void reset_mc_kernel(double *y, double *z, int n, const int *done) {
   if (done && *done) return;
   const double s = sent_val();
@@ -276,41 +408,55 @@ void launch_factor_mc(const FactorMcArgs &a, int k, cudaStream_t st) {
   long long blocks = (warps + 7) / 8;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 6) blocks = 148 * 6;
-  if (k == 2) factor_mc_kernel<2><<<(int)blocks, 256, 0, st>>>(a);
-  if (k == 3) factor_mc_kernel<3><<<(int)blocks, 256, 0, st>>>(a);
-  if (k == 4) factor_mc_kernel<4><<<(int)blocks, 256, 0, st>>>(a);
+  const int g = (int)blocks;
+  const bool cx = a.cx != 0;
+  if (k == 2 && !cx) factor_mc_kernel<2, false><<<g, 256, 0, st>>>(a);
+  if (k == 3 && !cx) factor_mc_kernel<3, false><<<g, 256, 0, st>>>(a);
+  if (k == 4 && !cx) factor_mc_kernel<4, false><<<g, 256, 0, st>>>(a);
+  if (k == 2 && cx) factor_mc_kernel<2, true><<<g, 256, 0, st>>>(a);
+  if (k == 3 && cx) factor_mc_kernel<3, true><<<g, 256, 0, st>>>(a);
+  if (k == 4 && cx) factor_mc_kernel<4, true><<<g, 256, 0, st>>>(a);
 }
 
-void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k,
+void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k, bool cx,
                      cudaStream_t st) {
   if (n <= 0) return;
   ++tl_launches;
   const int g = (n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8;
-  if (k == 2) recip_mc_kernel<2><<<g, 256, 0, st>>>(n, dp, lu, rcp);
-  if (k == 3) recip_mc_kernel<3><<<g, 256, 0, st>>>(n, dp, lu, rcp);
-  if (k == 4) recip_mc_kernel<4><<<g, 256, 0, st>>>(n, dp, lu, rcp);
+  if (k == 2 && !cx) recip_mc_kernel<2, false><<<g, 256, 0, st>>>(n, dp, lu, rcp);
+  if (k == 3 && !cx) recip_mc_kernel<3, false><<<g, 256, 0, st>>>(n, dp, lu, rcp);
+  if (k == 4 && !cx) recip_mc_kernel<4, false><<<g, 256, 0, st>>>(n, dp, lu, rcp);
+  if (k == 2 && cx) recip_mc_kernel<2, true><<<g, 256, 0, st>>>(n, dp, lu, rcp);
+  if (k == 3 && cx) recip_mc_kernel<3, true><<<g, 256, 0, st>>>(n, dp, lu, rcp);
+  if (k == 4 && cx) recip_mc_kernel<4, true><<<g, 256, 0, st>>>(n, dp, lu, rcp);
 }
 
 void launch_sweep_mc(const SweepMcArgs &a, int k, cudaStream_t st) {
-  const int g = (a.n + 255) / 256 < 148 * 8 ? ((a.n + 255) / 256 > 0 ? (a.n + 255) / 256 : 1)
-                                              : 148 * 8;
+  const int nb = (a.n + 255) / 256 > 0 ? (a.n + 255) / 256 : 1;
+  const int g = nb < 148 * 8 ? nb : 148 * 8;
   tl_launches += 2;
-  if (k == 2) reset_mc_kernel<2><<<g, 256, 0, st>>>(a.y, a.z, a.n, a.done);
-  if (k == 3) reset_mc_kernel<3><<<g, 256, 0, st>>>(a.y, a.z, a.n, a.done);
-  if (k == 4) reset_mc_kernel<4><<<g, 256, 0, st>>>(a.y, a.z, a.n, a.done);
+  reset_mc_kernel<<<g, 256, 0, st>>>(a.y, a.z, a.n, a.done);
   long long warps = (2LL * a.n + 31) / 32;
   long long blocks = (warps + 7) / 8;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 6) blocks = 148 * 6;
+  const int gb = (int)blocks;
+  const bool cx = a.cx != 0;
   if (a.adjoint) {
-    if (k == 2) sweep_mc_adj_kernel<2><<<(int)blocks, 256, 0, st>>>(a);
-    if (k == 3) sweep_mc_adj_kernel<3><<<(int)blocks, 256, 0, st>>>(a);
-    if (k == 4) sweep_mc_adj_kernel<4><<<(int)blocks, 256, 0, st>>>(a);
+    if (k == 2 && !cx) sweep_mc_adj_kernel<2, false><<<gb, 256, 0, st>>>(a);
+    if (k == 3 && !cx) sweep_mc_adj_kernel<3, false><<<gb, 256, 0, st>>>(a);
+    if (k == 4 && !cx) sweep_mc_adj_kernel<4, false><<<gb, 256, 0, st>>>(a);
+    if (k == 2 && cx) sweep_mc_adj_kernel<2, true><<<gb, 256, 0, st>>>(a);
+    if (k == 3 && cx) sweep_mc_adj_kernel<3, true><<<gb, 256, 0, st>>>(a);
+    if (k == 4 && cx) sweep_mc_adj_kernel<4, true><<<gb, 256, 0, st>>>(a);
     return;
   }
-  if (k == 2) sweep_mc_kernel<2><<<(int)blocks, 256, 0, st>>>(a);
-  if (k == 3) sweep_mc_kernel<3><<<(int)blocks, 256, 0, st>>>(a);
-  if (k == 4) sweep_mc_kernel<4><<<(int)blocks, 256, 0, st>>>(a);
+  if (k == 2 && !cx) sweep_mc_kernel<2, false><<<gb, 256, 0, st>>>(a);
+  if (k == 3 && !cx) sweep_mc_kernel<3, false><<<gb, 256, 0, st>>>(a);
+  if (k == 4 && !cx) sweep_mc_kernel<4, false><<<gb, 256, 0, st>>>(a);
+  if (k == 2 && cx) sweep_mc_kernel<2, true><<<gb, 256, 0, st>>>(a);
+  if (k == 3 && cx) sweep_mc_kernel<3, true><<<gb, 256, 0, st>>>(a);
+  if (k == 4 && cx) sweep_mc_kernel<4, true><<<gb, 256, 0, st>>>(a);
 }
 
 }  // namespace mpk

@@ -7,6 +7,7 @@ namespace mpk {
 
 struct FactorMcArgs {
   int n;
+  int cx;          // complex field: values are flat (re[K], im[K])
   const int *rp, *ci, *dp;
   double *lu;      // [nnz][K]: in A promoted, out the factors (in place)
   int *rowflag;    // per-row completion flags (zeroed)
@@ -16,10 +17,12 @@ struct FactorMcArgs {
 };
 struct SweepMcArgs {
   int n;
+  int cx;
   long long ld;          // plane stride of in / y / z
   const int *rp, *ci, *dp;
   const double *lu;      // [nnz][K] factors
-  const double *rcp;     // [n][K] mc_div(1, U_ii)
+  const double *rcp;     // real [n][K] mc_div(1, U_ii); complex [2n][2K+1]
+                         // Smith diagonals (plain, then adjoint)
   const double *in;      // planar K-component input
   double *y, *z;         // planar scratch / output (plane 0 sentinel-reset here)
   int *tick;
@@ -31,7 +34,7 @@ struct SweepMcArgs {
   const int *ut_rp, *ut_ci, *ut_perm, *lt_rp, *lt_ci, *lt_perm;
 };
 void launch_factor_mc(const FactorMcArgs &a, int k, cudaStream_t st);
-void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k,
+void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k, bool cx,
                      cudaStream_t st);
 void launch_sweep_mc(const SweepMcArgs &a, int k, cudaStream_t st);
 

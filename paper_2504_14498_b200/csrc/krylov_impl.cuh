@@ -317,6 +317,7 @@ struct Solver : PlanBase {
                 cudaStream_t s_, bool adjoint = false) {
     SweepMcArgs a{};
     a.adjoint = adjoint ? 1 : 0;
+    a.cx = CX ? 1 : 0;
     a.ut_rp = A.ut_rp;
     a.ut_ci = A.ut_ci;
     a.ut_perm = A.ut_perm;

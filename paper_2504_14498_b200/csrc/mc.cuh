@@ -988,4 +988,102 @@ MPK_HD void fmul(const double (&a)[K], const double (&b)[K], double (&out)[K]) {
   }
 }
 
+// complex fused a - b*c on (re, im) component arrays (_mcfast.py:195-377):
+// the real and imaginary parts are each ONE renormalisation of their
+// partial-product term list (cmulsub2/3; k = 4 via _rmulsub4_pair / _pair2)
+template <int K>
+MPK_HD void fcmulsub(const double (&ar)[K], const double (&ai)[K],
+                     const double (&br)[K], const double (&bi)[K],
+                     const double (&cr)[K], const double (&ci)[K],
+                     double (&orr)[K], double (&oi)[K]) {
+  static_assert(K >= 2 && K <= 4, "fused ops: k = 2..4");
+  if constexpr (K == 2) {
+    double p1, e1, p2, e2, p3, e3, p4, e4;
+    two_prod(br[0], cr[0], p1, e1);
+    two_prod(bi[0], ci[0], p2, e2);
+    const double tr = dadd(-dadd(dmul(br[0], cr[1]), dmul(br[1], cr[0])),
+                           dadd(dmul(bi[0], ci[1]), dmul(bi[1], ci[0])));
+    double t1[7] = {ar[0], -p1, p2, ar[1], tr, -e1, e2};
+    renorm<7, 2>(t1, orr);
+    two_prod(br[0], ci[0], p3, e3);
+    two_prod(bi[0], cr[0], p4, e4);
+    const double ti = -dadd(dadd(dadd(dmul(br[0], ci[1]), dmul(br[1], ci[0])), dmul(bi[0], cr[1])),
+                            dmul(bi[1], cr[0]));
+    double t2[7] = {ai[0], -p3, -p4, ai[1], ti, -e3, -e4};
+    renorm<7, 2>(t2, oi);
+  } else if constexpr (K == 3) {
+    double q00, f00, q01, f01, q10, f10, s00, g00, s01, g01, s10, g10;
+    two_prod(br[0], cr[0], q00, f00);
+    two_prod(br[0], cr[1], q01, f01);
+    two_prod(br[1], cr[0], q10, f10);
+    two_prod(bi[0], ci[0], s00, g00);
+    two_prod(bi[0], ci[1], s01, g01);
+    two_prod(bi[1], ci[0], s10, g10);
+    const double tr = dadd(-dadd(dadd(dmul(br[0], cr[2]), dmul(br[1], cr[1])), dmul(br[2], cr[0])),
+                           dadd(dadd(dmul(bi[0], ci[2]), dmul(bi[1], ci[1])), dmul(bi[2], ci[0])));
+    double t1[16] = {ar[0], -q00, s00, ar[1], -q01, -q10, s01, s10,
+                     -f00, g00, ar[2], tr, -f01, -f10, g01, g10};
+    renorm<16, 3>(t1, orr);
+    two_prod(br[0], ci[0], q00, f00);
+    two_prod(br[0], ci[1], q01, f01);
+    two_prod(br[1], ci[0], q10, f10);
+    two_prod(bi[0], cr[0], s00, g00);
+    two_prod(bi[0], cr[1], s01, g01);
+    two_prod(bi[1], cr[0], s10, g10);
+    const double ti =
+        -dadd(dadd(dadd(dadd(dadd(dmul(br[0], ci[2]), dmul(br[1], ci[1])), dmul(br[2], ci[0])),
+                        dmul(bi[0], cr[2])),
+                   dmul(bi[1], cr[1])),
+              dmul(bi[2], cr[0]));
+    double t2[16] = {ai[0], -q00, -s00, ai[1], -q01, -q10, -s01, -s10,
+                     -f00, -g00, ai[2], ti, -f01, -f10, -g01, -g10};
+    renorm<16, 3>(t2, oi);
+  } else {
+    // re = a_r - br*cr + bi*ci (pair), im = a_i - br*ci - bi*cr (pair2)
+    auto pair = [](const double (&a)[4], const double (&b)[4], const double (&c)[4],
+                   const double (&d)[4], const double (&e)[4], double sgn,
+                   double (&o)[4]) {
+      double p00, f00, p01, f01, p10, f10, p02, f02, p11, f11, p20, f20;
+      double q00, g00, q01, g01, q10, g10, q02, g02, q11, g11, q20, g20;
+      two_prod(b[0], c[0], p00, f00);
+      two_prod(b[0], c[1], p01, f01);
+      two_prod(b[1], c[0], p10, f10);
+      two_prod(b[0], c[2], p02, f02);
+      two_prod(b[1], c[1], p11, f11);
+      two_prod(b[2], c[0], p20, f20);
+      two_prod(d[0], e[0], q00, g00);
+      two_prod(d[0], e[1], q01, g01);
+      two_prod(d[1], e[0], q10, g10);
+      two_prod(d[0], e[2], q02, g02);
+      two_prod(d[1], e[1], q11, g11);
+      two_prod(d[2], e[0], q20, g20);
+      const double sb = dadd(dadd(dadd(dmul(b[0], c[3]), dmul(b[1], c[2])), dmul(b[2], c[1])),
+                             dmul(b[3], c[0]));
+      const double sd = dadd(dadd(dadd(dmul(d[0], e[3]), dmul(d[1], e[2])), dmul(d[2], e[1])),
+                             dmul(d[3], e[0]));
+      // sgn = +1: -(sb) + (sd); sgn = -1: -(sb) - (sd)
+      const double top = sgn > 0 ? dadd(-sb, sd) : dsub(-sb, sd);
+      const double s = sgn;  // q / g terms enter with this sign
+      double t[29] = {a[0], -p00, s * q00, a[1], -p01, -p10, s * q01, s * q10, -f00, s * g00,
+                      a[2], -p02, -p11, -p20, s * q02, s * q11, s * q20, -f01, -f10,
+                      s * g01, s * g10, a[3], top, -f02, -f11, -f20, s * g02, s * g11,
+                      s * g20};
+      renorm<29, 4>(t, o);
+    };
+    double a4r[4], a4i[4], b4r[4], b4i[4], c4r[4], c4i[4], o4r[4], o4i[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a4r[q] = ar[q]; a4i[q] = ai[q]; b4r[q] = br[q]; b4i[q] = bi[q];
+      c4r[q] = cr[q]; c4i[q] = ci[q];
+    }
+    pair(a4r, b4r, c4r, b4i, c4i, 1.0, o4r);
+    pair(a4i, b4r, c4i, b4i, c4r, -1.0, o4i);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      orr[q] = o4r[q];
+      oi[q] = o4i[q];
+    }
+  }
+}
+
 }  // namespace mpk

@@ -126,8 +126,8 @@ def ilu0_factorize_demoted(A) -> IluFactors:
 
 
 class IluFactorsMC(IluFactors):
-    """Working-precision factors (k = 2..4, real) resident on the device
-    (csrc/ilu_mc.cu); ``val_re`` downloads them as (nnz, k).  The device
+    """Working-precision factors (k = 2..4) resident on the device
+    (csrc/ilu_mc.cu); ``val_re`` / ``val_im`` download them as (nnz, k).  The device
     matrix keeps one such set (the latest k factorised)."""
 
     def __init__(self, A, dev, precision):
@@ -137,15 +137,20 @@ class IluFactorsMC(IluFactors):
     def _download(self):
         if self._host is None:
             k = self.precision.k
-            lu = np.zeros((self.nnz, k))
+            lu = np.zeros((self.nnz, 2 * k if self._cx else k))
             _lib.check(_lib.lib().mpk_ilu0_download_full(self._dev.h, ctypes.c_int(k),
                                                          _lib.dptr(lu)), "download_full")
-            self._host = (lu, None)
+            self._host = (np.ascontiguousarray(lu[:, :k]),
+                          np.ascontiguousarray(lu[:, k:]) if self._cx else None)
         return self._host
 
     @property
     def val_re(self) -> np.ndarray:
         return self._download()[0]
+
+    @property
+    def val_im(self):
+        return self._download()[1]
 
 
 def ilu0_factorize(A) -> IluFactors:
@@ -154,9 +159,10 @@ def ilu0_factorize(A) -> IluFactors:
     a - b*c (real field, binary64-valued matrices on the device path)."""
     if A.precision.k == 1:
         return _factor(A)
-    if A.val_im is not None or np.any(np.asarray(A.val_re)[:, 1:]):
+    if np.any(np.asarray(A.val_re)[:, 1:]) or (
+            A.val_im is not None and np.any(np.asarray(A.val_im)[:, 1:])):
         raise NotImplementedError(
-            "working-precision ILU(0) on the B200 path: real, binary64-valued matrices")
+            "working-precision ILU(0) on the B200 path: binary64-valued matrices")
     d = device_matrix(A)
     bad = ctypes.c_int64(-1)
     st = ctypes.c_int32(0)
@@ -196,12 +202,16 @@ def _apply_full(F, r: DenseVector, adjoint: bool) -> DenseVector:
     if F.precision != r.precision:
         raise ValueError("factor precision must match the vector precision")
     k = F.precision.k
-    z = np.zeros((F.n, k))
-    rc = _lib.lib().mpk_ilu0_apply_full_ex(F._dev.h, ctypes.c_int(k), _lib.dptr(_lib.f64(r.re)),
+    cx = F._cx
+    rin = np.concatenate([r.re, r.im]) if cx else r.re
+    z = np.zeros((2 * F.n if cx else F.n, k))
+    rc = _lib.lib().mpk_ilu0_apply_full_ex(F._dev.h, ctypes.c_int(k), _lib.dptr(_lib.f64(rin)),
                                            _lib.dptr(z), ctypes.c_int(int(adjoint)))
     if rc == _lib.MPK_NUMERIC_BREAKDOWN:
         raise NumericBreakdownError("non-finite value in triangular sweep")
     _lib.check(rc, "mpk_ilu0_apply_full_ex")
+    if cx:
+        return DenseVector(z[:F.n].copy(), z[F.n:].copy(), F.precision)
     return DenseVector(z, None, F.precision)
 
 

@@ -117,9 +117,6 @@ def _device_solve(A, b: DenseVector, cfg: SolverConfig, hist_cap: int | None = N
         raise ValueError(f"field mismatch: matrix {A.field}, vector {b.field}")
     if b.precision != cfg.precision:
         raise ValueError("vector precision must match cfg.precision")
-    if cfg.precond == PrecondMode.ILU0_FULL and A.field == "complex":
-        raise NotImplementedError(
-            "working-precision ILU(0) ('ilu0') on the B200 path: real field")
     if cfg.spmv_mode == "full":
         # full SpMV on a matrix whose values are exactly binary64 IS the mixed
         # computation bit for bit (reference tests/test_sparse.py:130-147);

@@ -411,6 +411,35 @@ def gen_ilu_full():
                             tol, 1e-100, None, precond="ilu0")
                 for key, v in o.items():
                     data[f"k{k}_{m}_{key}"] = v
+    # complex: the solver_small "c" system
+    rng = np.random.default_rng(32)
+    C64 = random_dd(rng, 60, 0.12, True)
+    nc = C64.n
+    xtc = rng.uniform(-1, 1, nc) + 1j * rng.uniform(-1, 1, nc)
+    for k in (2, 3, 4):
+        vre = np.zeros((len(C64.col_idx), k))
+        vim = np.zeros((len(C64.col_idx), k))
+        vre[:, 0] = C64.val_re[:, 0]
+        vim[:, 0] = C64.val_im[:, 0]
+        A = sparse.CsrMatrix(nc, C64.row_ptr, C64.col_idx, vre, vim, PREC[k])
+        F = ilu.ilu0_factorize(A)
+        data[f"c{k}_lu_re"], data[f"c{k}_lu_im"] = F.val_re, F.val_im
+        rr = np.array([rand_mc(r2, k) for _ in range(nc)])
+        ri = np.array([rand_mc(r2, k) for _ in range(nc)])
+        data[f"c{k}_r_re"], data[f"c{k}_r_im"] = rr, ri
+        z = ilu.ilu0_apply(F, sparse.DenseVector(rr.copy(), ri.copy(), PREC[k]))
+        data[f"c{k}_z_re"], data[f"c{k}_z_im"] = z.re, z.im
+        za = ilu.ilu0_apply_adjoint(F, sparse.DenseVector(rr.copy(), ri.copy(), PREC[k]))
+        data[f"c{k}_zadj_re"], data[f"c{k}_zadj_im"] = za.re, za.im
+        if k in (2, 3):
+            b = rhs(C64.val_re[:, 0], C64.val_im[:, 0], C64.row_ptr, C64.col_idx, nc, k,
+                    x_true=xtc)
+            tol = {2: 1e-25, 3: 1e-40}[k]
+            for m in ("bicg", "cgs", "bicgstab", "gpbicg"):
+                o = run_ref(C64.val_re[:, 0], C64.val_im[:, 0], C64.row_ptr, C64.col_idx, nc, b,
+                            m, k, tol, 1e-100, None, precond="ilu0")
+                for key, v in o.items():
+                    data[f"c{k}_{m}_{key}"] = v
     p = problems.cfg1()
     vre = np.zeros((p.nnz, 2))
     vre[:, 0] = p.val_re

@@ -620,3 +620,39 @@ def test_device_ilu0_full_solve(pkg, k, method):
     rep = pkg.solve(A, b, cfg)
     assert rep.iterations == int(gf[f"{pre}_iterations"])
     _hist_check(rep.history, gf[f"{pre}_hist"], k)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_device_ilu0_full_complex_factors_and_applies(pkg, k):
+    gf = golden("ilu_full.npz")
+    g = golden("solver_small.npz")
+    P = getattr(pkg.Precision, PREC_OF[k])
+    A = _csr(pkg, g["c_rp"], g["c_ci"], g["c_vre"], g["c_vim"]).promoted(P)
+    F = pkg.ilu0_factorize(A)
+    assert bits_equal(F.val_re, gf[f"c{k}_lu_re"]) and bits_equal(F.val_im, gf[f"c{k}_lu_im"])
+    r = pkg.DenseVector(gf[f"c{k}_r_re"].copy(), gf[f"c{k}_r_im"].copy(), P)
+    z = pkg.ilu0_apply(F, r)
+    assert bits_equal(z.re, gf[f"c{k}_z_re"]) and bits_equal(z.im, gf[f"c{k}_z_im"])
+    za = pkg.ilu0_apply_adjoint(F, r)
+    assert bits_equal(za.re, gf[f"c{k}_zadj_re"]) and bits_equal(za.im, gf[f"c{k}_zadj_im"])
+
+
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("method", ["bicg", "cgs", "bicgstab", "gpbicg"])
+def test_device_ilu0_full_complex_solve(pkg, k, method):
+    gf = golden("ilu_full.npz")
+    g = golden("solver_small.npz")
+    P = getattr(pkg.Precision, PREC_OF[k])
+    A = _csr(pkg, g["c_rp"], g["c_ci"], g["c_vre"], g["c_vim"]).promoted(P)
+    b = pkg.DenseVector(g[f"c{k}_b_re"].copy(), g[f"c{k}_b_im"].copy(), P)
+    cfg = pkg.SolverConfig(method=method, precision=P, precond=pkg.PrecondMode.ILU0_FULL,
+                           spmv_mode="mixed", eps_rel=TOL[k], eps_abs=1e-100)
+    pre = f"c{k}_{method}"
+    with pkg.reduction_mode("sequential"):
+        twin = pkg.solve(A, b, cfg)
+    assert twin.iterations == int(gf[f"{pre}_iterations"]) and twin.converged
+    assert bits_equal(np.asarray(twin.history), gf[f"{pre}_hist"])
+    assert bits_equal(twin.x.re, gf[f"{pre}_x_re"]) and bits_equal(twin.x.im, gf[f"{pre}_x_im"])
+    rep = pkg.solve(A, b, cfg)
+    assert rep.iterations == int(gf[f"{pre}_iterations"])
+    _hist_check(rep.history, gf[f"{pre}_hist"], k)
