@@ -382,6 +382,45 @@ def gen_solver_none():
     np.savez_compressed(HERE / "solver_none.npz", **data)
 
 
+def gen_grid():
+    """the reference harness's problem construction
+    (bench.build_problem) and its default grid on a small real matrix."""
+    from mpkrylov import bench as rbench
+
+    data = {}
+    rp, ci, v = problems.convdiff5(8, 10.0)[:3]
+    n = len(rp) - 1
+    crp, cci, cvr, cvi = problems.helmholtz7(4, 7)[:4]
+    nc = len(crp) - 1
+    for k in (2, 3):
+        vre = np.zeros((len(ci), k))
+        vre[:, 0] = v
+        A = sparse.CsrMatrix(n, rp, ci, vre, None, PREC[k])
+        pr = rbench.build_problem(A, PREC[k], "cd5_8")
+        data[f"r{k}_xstar"], data[f"r{k}_b"] = pr.x_star.re, pr.b.re
+        vr = np.zeros((len(cci), k))
+        vi = np.zeros((len(cci), k))
+        vr[:, 0], vi[:, 0] = cvr, cvi
+        C = sparse.CsrMatrix(nc, crp, cci, vr, vi, PREC[k])
+        pc = rbench.build_problem(C, PREC[k], "helm4")
+        data[f"c{k}_xstar_re"], data[f"c{k}_xstar_im"] = pc.x_star.re, pc.x_star.im
+        data[f"c{k}_b_re"], data[f"c{k}_b_im"] = pc.b.re, pc.b.im
+    vre = np.zeros((len(ci), 2))
+    vre[:, 0] = v
+    A = sparse.CsrMatrix(n, rp, ci, vre, None, Precision.DD)
+    pr = rbench.build_problem(A, Precision.DD, "cd5_8")
+    suite = [(A, pr, solvers.SolverConfig(method=m, precision=p, precond=pre, spmv_mode=mode,
+                                          eps_rel=1e-20))
+             for m, p, pre, mode in rbench.default_grid(precisions=[Precision.DD])]
+    rows = rbench.run_benchmark(suite)
+    data["grid_iterations"] = np.array([r.iterations for r in rows])
+    data["grid_converged"] = np.array([r.converged for r in rows])
+    data["grid_keys"] = np.array([f"{r.method}|{r.precond}|{r.spmv_mode}" for r in rows])
+    data["grid_true_relres"] = np.array([r.true_relres for r in rows])
+    data["grid_err2"] = np.array([r.err2 for r in rows])
+    np.savez_compressed(HERE / "grid_small.npz", **data)
+
+
 def gen_ilu_full():
     """working-precision ILU(0) ('ilu0', ilu.py:279-281)
     factors, applies and solves on the solver_small real system, plus the
@@ -605,6 +644,9 @@ if __name__ == "__main__":
     if "small" in what:
         gen_solver_small()
         print("solver_small done", time.time() - t0, flush=True)
+    if "grid" in what:
+        gen_grid()
+        print("grid done", time.time() - t0, flush=True)
     if "ilufull" in what:
         gen_ilu_full()
         print("ilufull done", time.time() - t0, flush=True)
