@@ -141,10 +141,8 @@ __device__ __forceinline__ double wf_fast_div(double a, double d, double r, bool
   // r = __drcp_rn(d), precomputed per factorization (wf_gather_kernel)
   const double q0 = __dmul_rn(a, r);
   const double e0 = fma(-q0, d, a);
-  const double q1 = fma(e0, r, q0);
-  const double e1 = fma(-q1, d, a);
-  const double q2 = fma(e1, r, q1);
-  const double e2 = fma(-q2, d, a);
+  const double q2 = fma(e0, r, q0);   // one Markstein correction
+  const double e2 = fma(-q2, d, a);   // exact residual of the candidate
   const unsigned long long qb = (unsigned long long)__double_as_longlong(q2);
   const unsigned long long ab = (unsigned long long)__double_as_longlong(a);
   const unsigned long long db = (unsigned long long)__double_as_longlong(d);
