@@ -103,6 +103,59 @@ __device__ void factor_row(const FactorArgs &a, int i) {
   atomicExch(&a.rowflag[i], 1);
 }
 
+// Real rows of at most kFactRow entries: the row lives in registers / local
+// memory for the whole elimination and each pivot row's upper part is
+// fetched in independent batches (the merge-walk of factor_row issues one
+// dependent L2 load per entry).  Same operations in the same order.
+constexpr int kFactRow = 32;
+constexpr int kFactBatch = 8;
+
+__device__ void factor_row_local(const FactorArgs &a, int i) {
+  const int lo = a.rp[i], hi = a.rp[i + 1], d = a.dp[i];
+  const int len = hi - lo;
+  int cols[kFactRow];
+  double vals[kFactRow];
+  for (int q = 0; q < len; ++q) {
+    cols[q] = a.ci[lo + q];
+    vals[q] = __ldcg(&a.lu[lo + q]);
+  }
+  for (int t = 0; t < d - lo; ++t) {
+    const int kc = cols[t];
+    while (ld_volatile_i(&a.rowflag[kc]) == 0) __nanosleep(32);
+    __threadfence();
+    const int uk = a.dp[kc], kend = a.rp[kc + 1];
+    const double l = ddiv(vals[t], __ldcg(&a.lu[uk]));
+    vals[t] = l;
+    int q = t + 1;
+    for (int s0 = uk + 1; s0 < kend; s0 += kFactBatch) {
+      int cb[kFactBatch];
+      double ub[kFactBatch];
+#pragma unroll
+      for (int b = 0; b < kFactBatch; ++b) {
+        const int s = s0 + b;
+        cb[b] = s < kend ? __ldcg(&a.ci[s]) : INT_MAX;
+        ub[b] = s < kend ? __ldcg(&a.lu[s]) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < kFactBatch; ++b) {
+        const int col = cb[b];
+        if (col == INT_MAX) break;
+        while (q < len && cols[q] < col) ++q;
+        if (q < len && cols[q] == col) vals[q] = dsub(vals[q], dmul(l, ub[b]));
+      }
+    }
+  }
+  bool fin = true;
+  for (int q = 0; q < len; ++q) {
+    __stcg(&a.lu[lo + q], vals[q]);
+    fin = fin && isfin(vals[q]);
+  }
+  if (vals[d - lo] == 0.0) atomicMin(a.bad_row, i);
+  if (!fin) atomicOr(a.nonfinite, 1);
+  __threadfence();
+  atomicExch(&a.rowflag[i], 1);
+}
+
 template <bool CX>
 __global__ void __launch_bounds__(kBlock) factor_kernel(FactorArgs a) {
   const int lane = threadIdx.x & 31;
@@ -110,7 +163,13 @@ __global__ void __launch_bounds__(kBlock) factor_kernel(FactorArgs a) {
     const int base = grab_ticket(a.tick);
     if (base >= a.n) break;
     const int t = base + lane;
-    if (t < a.n) factor_row<CX>(a, a.ord ? a.ord[t] : t);
+    if (t < a.n) {
+      const int row = a.ord ? a.ord[t] : t;
+      if (!CX && a.rp[row + 1] - a.rp[row] <= kFactRow)
+        factor_row_local(a, row);
+      else
+        factor_row<CX>(a, row);
+    }
   }
   exit_protocol(a.tick);
 }
