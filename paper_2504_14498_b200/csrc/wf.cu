@@ -342,6 +342,16 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
   // c the three most recent groups (rhs(c+3), deps(c+1), rhs(c+2)) may
   // still be pending: deps(c) and rhs(c) are complete
   rec_wait(0);
+  if constexpr (!FWD) {
+    // the backward right-hand sides are forward results: request them once
+    // the forward phase's last row (the sink of its DAG for grid stencils)
+    // is published, instead of re-polling stale requests row by row
+    if (j == 0) {
+      double r0, m0;
+      wf_poll<CX>(a.y, n - 1, r0, m0);
+    }
+    __syncwarp();
+  }
   deps_issue(0);
   rhs_issue(0);
   rhs_issue(1);
