@@ -393,7 +393,7 @@ __device__ __forceinline__ void wf_group(const SweepArgs &a, const WPhase &P,
     for (int t = 0; t < kWfT; ++t) {
       const int s = c * kWfT + t;
       if (dbgstep && j == 0 && s < 3072) wf_dbg2[s] = wf_gtime();
-      if (dbgcnt && dbgg == 1 && j == 0 && s < 3072) wf_dbg4[s] = wf_gtime();
+      if (dbgcnt && dbgg == (FWD ? 1 : P.ngroups) && j == 0 && s < 3072) wf_dbg4[s] = wf_gtime();
       const int pp = p0 + s;
       const bool act = (unsigned)(s + pos0) < (unsigned)Lc && pp < n;
       double vr[kWfEM], vi[kWfEM], cl[kWfEM], cm[kWfEM];

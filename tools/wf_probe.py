@@ -82,3 +82,8 @@ if g1[100] > 0 and g0[200] > 0:
     print("group1 step x minus group0 step x+63 (us):", [round((g1[x] - g0[x + 63]) / 1e3, 2) for x in xs])
     tau0 = np.median(np.diff(g0[:2000])); tau1 = np.median(np.diff(g1[:2000]))
     print("median step ns g0/g1:", tau0, tau1, " lag in steps at x=1000:", round((g1[1000] - g0[1000]) / tau0, 1))
+
+d4 = np.diff(g1[:2000]) if g1[10] > 0 else None
+if d4 is not None:
+    print("bwd group 0 step ns: median", np.median(d4), "mean", round(d4.mean(), 1),
+          "by t%8:", [int(np.median(d4[t::8])) for t in range(8)])
