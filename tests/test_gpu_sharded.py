@@ -39,7 +39,7 @@ def _dev(h, h0):
                for a, o in zip(h[:41], h0[:41]))
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
 def test_sharded_virtual_ranks_match_single(world):
     import paper_2504_14498_b200 as mpk
     from paper_2504_14498_b200.sharded import Communicator, solve_sharded
