@@ -8,9 +8,9 @@
 // _mcfast.RealDiag = rmulK(acc, mc_div(1, U_ii))), ilu.py:374-420.
 // Scheduling is the sync-free ticket scheme of ilu.cu (one row per thread,
 // rows claimed in dependency-compatible order, a row waits only on rows
-// with smaller tickets).  A K-component value is published by writing
-// components 1..K-1, a fence, then component 0 over its signalling-NaN
-// sentinel; a reader polls component 0, fences, then reads the rest.
+// with smaller tickets).  Every component plane of the outputs starts as
+// signalling-NaN sentinels; a value is complete when none of its
+// components is a sentinel (each changes exactly once per sweep).
 #include <climits>
 
 #include "ilu_mc.cuh"
@@ -51,27 +51,56 @@ __device__ __forceinline__ int ldri(const int *p) {
   return v;
 }
 
-// K-component value j of a planar vector (stride ld), published by another row
+// K-component value j of a planar vector (stride ld), published by another
+// row: EVERY component plane is sentinel-reset before the sweep and each
+// component changes once (sentinel -> final value), so a value is complete
+// when no component still carries the sentinel -- no fence on either side.
+template <int W>
+__device__ __forceinline__ bool any_sent(const double (&o)[W]) {
+  bool b = false;
+#pragma unroll
+  for (int c = 0; c < W; ++c) b |= is_sent(o[c]);
+  return b;
+}
+template <int W>
+__device__ __forceinline__ void load_mc(const double *v, long long ld, int j, double (&o)[W]) {
+#pragma unroll
+  for (int c = 0; c < W; ++c) o[c] = ldr(v + c * ld + j);
+}
 template <int K>
 __device__ __forceinline__ void poll_mc(const double *v, long long ld, int j,
                                         double (&o)[K]) {
-  double h = ldr(v + j);
-  while (is_sent(h)) {
+  load_mc<K>(v, ld, j, o);
+  while (any_sent<K>(o)) {
     __nanosleep(32);
-    h = ldr(v + j);
+    load_mc<K>(v, ld, j, o);
   }
-  __threadfence();
-  o[0] = h;
-#pragma unroll
-  for (int c = 1; c < K; ++c) o[c] = ldr(v + c * ld + j);
 }
 template <int K>
 __device__ __forceinline__ void pub_mc(double *v, long long ld, int j,
                                        const double (&x)[K]) {
 #pragma unroll
-  for (int c = 1; c < K; ++c) str(v + c * ld + j, x[c]);
-  __threadfence();
-  str(v + j, unsent(x[0]));
+  for (int c = 0; c < K; ++c) str(v + c * ld + j, unsent(x[c]));
+}
+
+// Up to kMcBatch published values at cols[0..m) requested together (all
+// components); the caller consumes them in order through wait_mc, so the
+// later requests are in flight while the earlier products are computed.
+constexpr int kMcBatch = 4;
+template <int W>
+__device__ __forceinline__ void gather_mc(const double *v, long long ld, const int *cols,
+                                          int m, double (&o)[kMcBatch][W]) {
+#pragma unroll
+  for (int b = 0; b < kMcBatch; ++b)
+    if (b < m) load_mc<W>(v, ld, cols[b], o[b]);
+}
+template <int W>
+__device__ __forceinline__ void wait_mc(const double *v, long long ld, int col,
+                                        double (&o)[W]) {
+  while (any_sent<W>(o)) {
+    __nanosleep(32);
+    load_mc<W>(v, ld, col, o);
+  }
 }
 
 // value helpers on flat (re..., im...) arrays of W = K or 2K components
@@ -296,28 +325,48 @@ __global__ void __launch_bounds__(256) sweep_mc_kernel(SweepMcArgs a) {
       double acc[W];
 #pragma unroll
       for (int c = 0; c < W; ++c) acc[c] = a.in[c * ld + i];
-      for (int p = a.rp[i]; p < a.dp[i]; ++p) {
-        double y[W], l[W], r[W];
-        poll_mc<W>(a.y, ld, a.ci[p], y);
+      for (int p0 = a.rp[i]; p0 < a.dp[i]; p0 += kMcBatch) {
+        const int m = min(kMcBatch, a.dp[i] - p0);
+        int cols[kMcBatch];
+        double yv[kMcBatch][W];
 #pragma unroll
-        for (int c = 0; c < W; ++c) l[c] = a.lu[(size_t)p * W + c];
-        mc_mulsub<K, CX>(acc, l, y, r);
+        for (int b = 0; b < kMcBatch; ++b) cols[b] = b < m ? a.ci[p0 + b] : 0;
+        gather_mc<W>(a.y, ld, cols, m, yv);
 #pragma unroll
-        for (int c = 0; c < W; ++c) acc[c] = r[c];
+        for (int b = 0; b < kMcBatch; ++b)
+          if (b < m) {
+            double l[W], r[W];
+#pragma unroll
+            for (int c = 0; c < W; ++c) l[c] = a.lu[(size_t)(p0 + b) * W + c];
+            wait_mc<W>(a.y, ld, cols[b], yv[b]);
+            mc_mulsub<K, CX>(acc, l, yv[b], r);
+#pragma unroll
+            for (int c = 0; c < W; ++c) acc[c] = r[c];
+          }
       }
       pub_mc<W>(a.y, ld, i, acc);
     } else if (t < 2 * n) {
       const int i = 2 * n - 1 - t;
       double acc[W];
       poll_mc<W>(a.y, ld, i, acc);
-      for (int p = a.dp[i] + 1; p < a.rp[i + 1]; ++p) {
-        double z[W], u[W], r[W];
-        poll_mc<W>(a.z, ld, a.ci[p], z);
+      for (int p0 = a.dp[i] + 1; p0 < a.rp[i + 1]; p0 += kMcBatch) {
+        const int m = min(kMcBatch, a.rp[i + 1] - p0);
+        int cols[kMcBatch];
+        double zv[kMcBatch][W];
 #pragma unroll
-        for (int c = 0; c < W; ++c) u[c] = a.lu[(size_t)p * W + c];
-        mc_mulsub<K, CX>(acc, u, z, r);
+        for (int b = 0; b < kMcBatch; ++b) cols[b] = b < m ? a.ci[p0 + b] : 0;
+        gather_mc<W>(a.z, ld, cols, m, zv);
 #pragma unroll
-        for (int c = 0; c < W; ++c) acc[c] = r[c];
+        for (int b = 0; b < kMcBatch; ++b)
+          if (b < m) {
+            double u[W], r[W];
+#pragma unroll
+            for (int c = 0; c < W; ++c) u[c] = a.lu[(size_t)(p0 + b) * W + c];
+            wait_mc<W>(a.z, ld, cols[b], zv[b]);
+            mc_mulsub<K, CX>(acc, u, zv[b], r);
+#pragma unroll
+            for (int c = 0; c < W; ++c) acc[c] = r[c];
+          }
       }
       double q[W];
       diag_solve<K, CX>(acc, a.rcp + (size_t)i * DW, q);
@@ -354,15 +403,25 @@ __global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
       double acc[W];
 #pragma unroll
       for (int q = 0; q < W; ++q) acc[q] = a.in[q * ld + c];
-      for (int p = a.ut_rp[c]; p < a.ut_rp[c + 1]; ++p) {
-        double y[W], u[W], r[W];
-        poll_mc<W>(a.y, ld, a.ut_ci[p], y);
-        const long long e = a.ut_perm[p];
+      for (int p0 = a.ut_rp[c]; p0 < a.ut_rp[c + 1]; p0 += kMcBatch) {
+        const int m = min(kMcBatch, a.ut_rp[c + 1] - p0);
+        int cols[kMcBatch];
+        double yv[kMcBatch][W];
 #pragma unroll
-        for (int q = 0; q < W; ++q) u[q] = (CX && q >= K) ? -a.lu[e * W + q] : a.lu[e * W + q];
-        mc_mulsub<K, CX>(acc, u, y, r);
+        for (int b = 0; b < kMcBatch; ++b) cols[b] = b < m ? a.ut_ci[p0 + b] : 0;
+        gather_mc<W>(a.y, ld, cols, m, yv);
 #pragma unroll
-        for (int q = 0; q < W; ++q) acc[q] = r[q];
+        for (int b = 0; b < kMcBatch; ++b)
+          if (b < m) {
+            double u[W], r[W];
+            const long long e = a.ut_perm[p0 + b];
+#pragma unroll
+            for (int q = 0; q < W; ++q) u[q] = (CX && q >= K) ? -a.lu[e * W + q] : a.lu[e * W + q];
+            wait_mc<W>(a.y, ld, cols[b], yv[b]);
+            mc_mulsub<K, CX>(acc, u, yv[b], r);
+#pragma unroll
+            for (int q = 0; q < W; ++q) acc[q] = r[q];
+          }
       }
       double o[W];
       diag_solve<K, CX>(acc, dg0 + (size_t)c * DW, o);
@@ -371,15 +430,25 @@ __global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
       const int c = 2 * n - 1 - t;
       double acc[W];
       poll_mc<W>(a.y, ld, c, acc);
-      for (int p = a.lt_rp[c]; p < a.lt_rp[c + 1]; ++p) {
-        double z[W], l[W], r[W];
-        poll_mc<W>(a.z, ld, a.lt_ci[p], z);
-        const long long e = a.lt_perm[p];
+      for (int p0 = a.lt_rp[c]; p0 < a.lt_rp[c + 1]; p0 += kMcBatch) {
+        const int m = min(kMcBatch, a.lt_rp[c + 1] - p0);
+        int cols[kMcBatch];
+        double zv[kMcBatch][W];
 #pragma unroll
-        for (int q = 0; q < W; ++q) l[q] = (CX && q >= K) ? -a.lu[e * W + q] : a.lu[e * W + q];
-        mc_mulsub<K, CX>(acc, l, z, r);
+        for (int b = 0; b < kMcBatch; ++b) cols[b] = b < m ? a.lt_ci[p0 + b] : 0;
+        gather_mc<W>(a.z, ld, cols, m, zv);
 #pragma unroll
-        for (int q = 0; q < W; ++q) acc[q] = r[q];
+        for (int b = 0; b < kMcBatch; ++b)
+          if (b < m) {
+            double l[W], r[W];
+            const long long e = a.lt_perm[p0 + b];
+#pragma unroll
+            for (int q = 0; q < W; ++q) l[q] = (CX && q >= K) ? -a.lu[e * W + q] : a.lu[e * W + q];
+            wait_mc<W>(a.z, ld, cols[b], zv[b]);
+            mc_mulsub<K, CX>(acc, l, zv[b], r);
+#pragma unroll
+            for (int q = 0; q < W; ++q) acc[q] = r[q];
+          }
       }
       bool fin = true;
 #pragma unroll
@@ -391,13 +460,15 @@ __global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
   mc_exit(a.tick);
 }
 
-__global__ void reset_mc_kernel(double *y, double *z, int n, const int *done) {
+__global__ void reset_mc_kernel(double *y, double *z, int n, long long ld, int w,
+                                const int *done) {
   if (done && *done) return;
   const double s = sent_val();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    y[i] = s;
-    z[i] = s;
-  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int c = 0; c < w; ++c) {
+      y[c * ld + i] = s;
+      z[c * ld + i] = s;
+    }
 }
 
 }  // namespace
@@ -435,7 +506,7 @@ void launch_sweep_mc(const SweepMcArgs &a, int k, cudaStream_t st) {
   const int nb = (a.n + 255) / 256 > 0 ? (a.n + 255) / 256 : 1;
   const int g = nb < 148 * 8 ? nb : 148 * 8;
   tl_launches += 2;
-  reset_mc_kernel<<<g, 256, 0, st>>>(a.y, a.z, a.n, a.done);
+  reset_mc_kernel<<<g, 256, 0, st>>>(a.y, a.z, a.n, a.ld, (a.cx ? 2 : 1) * k, a.done);
   long long warps = (2LL * a.n + 31) / 32;
   long long blocks = (warps + 7) / 8;
   if (blocks < 1) blocks = 1;
