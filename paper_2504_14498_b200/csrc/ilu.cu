@@ -355,8 +355,18 @@ __device__ void bwd_row_adj(const SweepArgs &a, int c) {
 
 template <bool CX, bool ADJ, int PREF, bool REL>
 __global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs a) {
-  if (a.done && *a.done) return;
   const int lane = threadIdx.x & 31;
+  // solve already stopped (the flag may flip while the grid launches, e.g.
+  // from a finalize on a side stream): skip the work but still take part in
+  // the exit count, so the ticket is reset for the next launch
+  {
+    int d = 0;
+    if (lane == 0 && a.done) d = ld_volatile_i(a.done);
+    if (__shfl_sync(kFull, d, 0)) {
+      exit_protocol(a.tick);
+      return;
+    }
+  }
   const int n = a.n;
   for (;;) {
     const int base = grab_ticket(a.tick);

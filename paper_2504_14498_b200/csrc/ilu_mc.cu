@@ -312,7 +312,14 @@ __global__ void __launch_bounds__(256) sweep_mc_kernel(SweepMcArgs a) {
   // planar vectors: component q at q*ld, complex = K real then K imag)
   constexpr int W = CX ? 2 * K : K;
   constexpr int DW = CX ? 2 * K + 1 : K;
-  if (a.done && *a.done) return;
+  {  // stopped solve: skip, but count this warp out (ticket reset)
+    int d = 0;
+    if ((threadIdx.x & 31) == 0 && a.done) d = ldri(a.done);
+    if (__shfl_sync(kFullM, d, 0)) {
+      mc_exit(a.tick);
+      return;
+    }
+  }
   const int lane = threadIdx.x & 31;
   const int n = a.n;
   const long long ld = a.ld;
@@ -389,7 +396,14 @@ template <int K, bool CX>
 __global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
   constexpr int W = CX ? 2 * K : K;
   constexpr int DW = CX ? 2 * K + 1 : K;
-  if (a.done && *a.done) return;
+  {  // stopped solve: skip, but count this warp out (ticket reset)
+    int d = 0;
+    if ((threadIdx.x & 31) == 0 && a.done) d = ldri(a.done);
+    if (__shfl_sync(kFullM, d, 0)) {
+      mc_exit(a.tick);
+      return;
+    }
+  }
   const int lane = threadIdx.x & 31;
   const int n = a.n;
   const long long ld = a.ld;

@@ -503,7 +503,20 @@ __device__ long long wf_dbg[2 * 8192];
 template <bool CX>
 __global__ void __launch_bounds__(32, 1)
     wsweep_kernel(SweepArgs a, WPhase F, WPhase B, int bufsz, int dbg) {
-  if (a.done && *a.done) return;
+  {  // stopped solve: skip, but count this CTA out (ticket reset)
+    int d = 0;
+    if (threadIdx.x == 0 && a.done) d = *(volatile const int *)a.done;
+    if (__shfl_sync(kFullW, d, 0)) {
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&a.tick[1], 1) == (int)gridDim.x - 1) {
+          atomicExch(&a.tick[0], 0);
+          atomicExch(&a.tick[1], 0);
+        }
+      }
+      return;
+    }
+  }
   using Lt = WfLayout<CX>;
   extern __shared__ __align__(128) unsigned char wsm[];
   const int j = threadIdx.x & 31;

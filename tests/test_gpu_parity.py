@@ -656,3 +656,24 @@ def test_device_ilu0_full_complex_solve(pkg, k, method):
     rep = pkg.solve(A, b, cfg)
     assert rep.iterations == int(gf[f"{pre}_iterations"])
     _hist_check(rep.history, gf[f"{pre}_hist"], k)
+
+
+def test_device_repeated_solves_same_matrix(pkg):
+    """Regression: a solve that stops while a ticket-scheduled sweep grid is
+    still launching (BiCG's concurrent finalize) must leave the sweep ticket
+    reset for the next solve on the same matrix (the early-exit path counts
+    itself out).  Three BiCG ilu0 solves on one n = 20000 matrix converge
+    identically."""
+    from paper_2504_14498_b200 import problems
+
+    rp, ci, v, xt = problems.random_nonsym(20000, 12, 2)
+    P = pkg.Precision.TD
+    A = pkg.CsrMatrix.from_binary64(20000, rp, ci, v, None, P)
+    b = pkg.spmv_mixed(A.demoted(), pkg.DenseVector.from_float64(xt, P))
+    for pre in (pkg.PrecondMode.ILU0_FULL, pkg.PrecondMode.ILU0_MIXED):
+        cfg = pkg.SolverConfig(method="bicg", precision=P, precond=pre, spmv_mode="mixed",
+                               eps_rel=1e-30, max_iter=300)
+        reps = [pkg.solve(A, b, cfg) for _ in range(3)]
+        assert all(r.converged and r.iterations == reps[0].iterations for r in reps)
+        assert all(np.array_equal(np.asarray(r.history), np.asarray(reps[0].history))
+                   for r in reps)
