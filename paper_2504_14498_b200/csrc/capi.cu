@@ -1161,6 +1161,7 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
   fa.tick = m->fscratch;
   fa.bad_row = m->fscratch + 2;
   fa.nonfinite = m->fscratch + 3;
+  fa.ord = A.ord_f;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -1236,6 +1237,8 @@ int mpk_ilu0_apply_full_ex(mpk_matrix *m, int k, const double *r, double *z, int
   a.lt_rp = A.lt_rp;
   a.lt_ci = A.lt_ci;
   a.lt_perm = A.lt_perm;
+  a.ord_f = adjoint ? A.ord_fa : A.ord_f;
+  a.ord_b = adjoint ? A.ord_ba : A.ord_b;
   launch_sweep_mc(a, k, st);
   launch_from_planar(n, k, dz, stage, A.cx ? stage + n * k : nullptr, st);
   CKR(cudaMemcpyAsync(z, stage, sizeof(double) * n * k * c2, cudaMemcpyDeviceToHost, st));

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256) factor_mc_kernel(FactorMcArgs a) {
     const int base = mc_grab(a.tick);
     if (base >= a.n) break;
     const int t = base + lane;
-    if (t < a.n) factor_mc_row<K, CX>(a, t);
+    if (t < a.n) factor_mc_row<K, CX>(a, a.ord ? a.ord[t] : t);
   }
   mc_exit(a.tick);
 }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(256) sweep_mc_kernel(SweepMcArgs a) {
     if (base >= 2 * n) break;
     const int t = base + lane;
     if (t < n) {
-      const int i = t;
+      const int i = a.ord_f ? a.ord_f[t] : t;
       double acc[W];
 #pragma unroll
       for (int c = 0; c < W; ++c) acc[c] = a.in[c * ld + i];
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(256) sweep_mc_kernel(SweepMcArgs a) {
       }
       pub_mc<W>(a.y, ld, i, acc);
     } else if (t < 2 * n) {
-      const int i = 2 * n - 1 - t;
+      const int i = a.ord_b ? a.ord_b[t - n] : 2 * n - 1 - t;
       double acc[W];
       poll_mc<W>(a.y, ld, i, acc);
       for (int p0 = a.dp[i] + 1; p0 < a.rp[i + 1]; p0 += kMcBatch) {
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
     if (base >= 2 * n) break;
     const int t = base + lane;
     if (t < n) {
-      const int c = t;
+      const int c = a.ord_f ? a.ord_f[t] : t;
       double acc[W];
 #pragma unroll
       for (int q = 0; q < W; ++q) acc[q] = a.in[q * ld + c];
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(256) sweep_mc_adj_kernel(SweepMcArgs a) {
       diag_solve<K, CX>(acc, dg0 + (size_t)c * DW, o);
       pub_mc<W>(a.y, ld, c, o);
     } else if (t < 2 * n) {
-      const int c = 2 * n - 1 - t;
+      const int c = a.ord_b ? a.ord_b[t - n] : 2 * n - 1 - t;
       double acc[W];
       poll_mc<W>(a.y, ld, c, acc);
       for (int p0 = a.lt_rp[c]; p0 < a.lt_rp[c + 1]; p0 += kMcBatch) {

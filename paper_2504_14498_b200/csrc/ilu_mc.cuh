@@ -14,6 +14,7 @@ struct FactorMcArgs {
   int *tick;       // [0] ticket, [1] exit counter
   int *bad_row;    // atomicMin of zero-pivot rows (init INT_MAX)
   int *nonfinite;  // set if any factor is non-finite
+  const int *ord;  // tickets -> rows in level order of the L DAG (or null)
 };
 struct SweepMcArgs {
   int n;
@@ -32,6 +33,9 @@ struct SweepMcArgs {
   // rows) and L^T (descending), values at lu[perm[q]]
   int adjoint;
   const int *ut_rp, *ut_ci, *ut_perm, *lt_rp, *lt_ci, *lt_perm;
+  // tickets -> rows in level order of the phase's DAG (null: natural order);
+  // a warp's 32 rows then rarely depend on each other
+  const int *ord_f, *ord_b;
 };
 void launch_factor_mc(const FactorMcArgs &a, int k, cudaStream_t st);
 void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k, bool cx,

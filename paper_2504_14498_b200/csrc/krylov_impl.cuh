@@ -324,6 +324,8 @@ struct Solver : PlanBase {
     a.lt_rp = A.lt_rp;
     a.lt_ci = A.lt_ci;
     a.lt_perm = A.lt_perm;
+    a.ord_f = adjoint ? A.ord_fa : A.ord_f;
+    a.ord_b = adjoint ? A.ord_ba : A.ord_b;
     a.n = n;
     a.ld = ld;
     a.rp = A.rp;
