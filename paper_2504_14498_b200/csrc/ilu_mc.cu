@@ -67,13 +67,12 @@ __device__ __forceinline__ void load_mc(const double *v, long long ld, int j, do
 #pragma unroll
   for (int c = 0; c < W; ++c) o[c] = ldr(v + c * ld + j);
 }
-__constant__ unsigned c_mc_sleep = 32;  // EXPERIMENT
 template <int K>
 __device__ __forceinline__ void poll_mc(const double *v, long long ld, int j,
                                         double (&o)[K]) {
   load_mc<K>(v, ld, j, o);
   while (any_sent<K>(o)) {
-    __nanosleep(c_mc_sleep);
+    __nanosleep(32);
     load_mc<K>(v, ld, j, o);
   }
 }
@@ -99,7 +98,7 @@ template <int W>
 __device__ __forceinline__ void wait_mc(const double *v, long long ld, int col,
                                         double (&o)[W]) {
   while (any_sent<W>(o)) {
-    __nanosleep(c_mc_sleep);
+    __nanosleep(32);
     load_mc<W>(v, ld, col, o);
   }
 }
@@ -140,7 +139,7 @@ __device__ void factor_mc_row(const FactorMcArgs &a, int i) {
   double *lu = a.lu;
   for (int t = lo; t < d; ++t) {
     const int kc = a.ci[t];
-    while (ldri(&a.rowflag[kc]) == 0) __nanosleep(c_mc_sleep);
+    while (ldri(&a.rowflag[kc]) == 0) __nanosleep(32);
     __threadfence();
     const int uk = a.dp[kc], kend = a.rp[kc + 1];
     double at[W], ukk[W], l[W];
@@ -518,14 +517,6 @@ void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k,
 }
 
 void launch_sweep_mc(const SweepMcArgs &a, int k, cudaStream_t st) {
-  static bool once = false;
-  if (!once) {
-    once = true;
-    if (const char *e = getenv("MPK_MC_SLEEP")) {
-      unsigned v = (unsigned)atoi(e);
-      cudaMemcpyToSymbol(c_mc_sleep, &v, sizeof(v));
-    }
-  }
   const int nb = (a.n + 255) / 256 > 0 ? (a.n + 255) / 256 : 1;
   const int g = nb < 148 * 8 ? nb : 148 * 8;
   tl_launches += 2;
