@@ -487,12 +487,25 @@ __global__ void reset_mc_kernel(double *y, double *z, int n, long long ld, int w
 
 }  // namespace
 
+// Ticket grids of the K-component factor / sweeps: one 8-warp CTA per SM
+// (≈ 38 k rows in flight) is enough to keep every level of a stencil busy;
+// more resident warps only add sentinel polls to L2 (cfg4 apply 1.6x slower
+// at 6 CTAs per SM).  MPK_MC_BLOCKS overrides.
+static int mc_grid_cap() {
+  static const int cap = [] {
+    const char *e = getenv("MPK_MC_BLOCKS");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 148;
+  }();
+  return cap;
+}
+
 void launch_factor_mc(const FactorMcArgs &a, int k, cudaStream_t st) {
   ++tl_launches;
   long long warps = (a.n + 31) / 32;
   long long blocks = (warps + 7) / 8;
   if (blocks < 1) blocks = 1;
-  if (blocks > 148 * 6) blocks = 148 * 6;
+  if (blocks > mc_grid_cap()) blocks = mc_grid_cap();
   const int g = (int)blocks;
   const bool cx = a.cx != 0;
   if (k == 2 && !cx) factor_mc_kernel<2, false><<<g, 256, 0, st>>>(a);
@@ -524,7 +537,7 @@ void launch_sweep_mc(const SweepMcArgs &a, int k, cudaStream_t st) {
   long long warps = (2LL * a.n + 31) / 32;
   long long blocks = (warps + 7) / 8;
   if (blocks < 1) blocks = 1;
-  if (blocks > 148 * 6) blocks = 148 * 6;
+  if (blocks > mc_grid_cap()) blocks = mc_grid_cap();
   const int gb = (int)blocks;
   const bool cx = a.cx != 0;
   if (a.adjoint) {
