@@ -644,6 +644,7 @@ static void free_sweeps(SweepMats &sm) {
   free_cplan(sm.cs);
   free_rplan(sm.rs);
   free_wsweep(sm.wf);
+  free_ssweep(sm.ss);
 }
 
 // Average device time of one plain ILU(0) apply (sentinel reset + sweep)
@@ -988,6 +989,31 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
     }
     CKR(cudaGetLastError());
   }
+  // shuffle-wavefront plan (swf.cu) for stencil-structured real sweeps:
+  // kept when it beats the plan chosen above (MPK_SWEEP_PICK=swf forces it)
+  {
+    SSweep ss;
+    if (build_ssweep(ss, (int)n, A.cx, A.h_rp.data(), A.h_ci.data(), A.h_dp.data(), st)) {
+      const char *pick = getenv("MPK_SWEEP_PICK");
+      const bool force = pick && !strcmp(pick, "swf");
+      const bool other = pick && !force;
+      float tb = 1e30f, ts = 0.f;
+      if (!force && !other) tb = time_apply_plan(A, st);
+      gather_ssweep(A.val, ss, st);  // timing values (regathered after factorization)
+      A.smat.ss = ss;
+      if (!force && !other) ts = time_apply_plan(A, st);
+      if (other || !(ts < tb)) free_ssweep(A.smat.ss);
+      if (getenv("MPK_VERBOSE"))
+        fprintf(stderr,
+                "[mpk] shuffle-wavefront plan n=%lld: fwd Lc=%d lag=%d groups=%d S=%d pat=%d, "
+                "bwd Lc=%d lag=%d groups=%d S=%d pat=%d, W=%d smem=%zu; apply %.4f ms vs "
+                "%.4f ms (other plan) -> %s\n",
+                (long long)n, ss.f.Lc, ss.f.lag, ss.f.ngroups, ss.f.S, ss.f.pat, ss.b.Lc,
+                ss.b.lag, ss.b.ngroups, ss.b.S, ss.b.pat, ss.W, ss.smem, ts, tb,
+                A.smat.ss.on ? "shuffle-wavefront" : "other");
+    }
+    CKR(cudaGetLastError());
+  }
   *out = m;
   return MPK_OK;
 }
@@ -1093,6 +1119,7 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   gather_csweep(A.lu, A.smat.cs, A.cx, m->ctx->stream);
   gather_rsweep(A.lu, A.smat.rs, A.cx, m->ctx->stream);
   gather_wsweep(A.lu, A.smat.wf, A.cx, m->ctx->stream);
+  gather_ssweep(A.lu, A.smat.ss, m->ctx->stream);
   return MPK_OK;
 }
 

@@ -151,6 +151,7 @@ struct SweepMats {
   CSweep cs;          // cluster plan (cs.C > 0 when built)
   RSweep rs;          // ring plan (rs.nchunks > 0 when built)
   WSweep wf;          // lane-chunk wavefront plan (wf.on when kept; wf.cu)
+  SSweep ss;          // shuffle-wavefront plan (ss.on when kept; swf.cu)
 };
 // wavefront plan (wf.cuh): analysis at upload, values gathered per factorization
 bool build_wsweep(WSweep &w, int n, bool cx, const int *rp, const int *ci,
@@ -158,6 +159,12 @@ bool build_wsweep(WSweep &w, int n, bool cx, const int *rp, const int *ci,
 void gather_wsweep(const double *lu, const WSweep &w, bool cx, cudaStream_t st);
 void launch_wsweep(const SweepArgs &a, const WSweep &w, bool cx, cudaStream_t st);
 void free_wsweep(WSweep &w);
+// shuffle-wavefront plan (swf.cu): stencil-structured real sweeps
+bool build_ssweep(SSweep &w, int n, bool cx, const int *rp, const int *ci, const int *dp,
+                  cudaStream_t st);
+void gather_ssweep(const double *lu, const SSweep &w, cudaStream_t st);
+void launch_ssweep(const SweepArgs &a, const SSweep &w, cudaStream_t st);
+void free_ssweep(SSweep &w);
 void launch_rsweep(const SweepArgs &a, const RSweep &p, bool cx, bool adjoint,
                    cudaStream_t st);
 void gather_rsweep(const double *lu, const RSweep &p, bool cx, cudaStream_t st);

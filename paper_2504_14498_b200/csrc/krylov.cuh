@@ -94,7 +94,9 @@ inline void do_sweep(const DMat &A, const SweepArgs &a, bool adjoint,
   const bool mats = adjoint ? A.smat_adj_built : A.smat_built;
   const CSweep &cs = adjoint ? A.smat_adj.cs : A.smat.cs;
   const RSweep &rs = adjoint ? A.smat_adj.rs : A.smat.rs;
-  if (!adjoint && A.smat.wf.on)
+  if (!adjoint && A.smat.ss.on)
+    launch_ssweep(a, A.smat.ss, st);
+  else if (!adjoint && A.smat.wf.on)
     launch_wsweep(a, A.smat.wf, A.cx, st);
   else if (rs.nchunks > 0)
     launch_rsweep(a, rs, A.cx, adjoint, st);

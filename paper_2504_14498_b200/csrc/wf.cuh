@@ -64,3 +64,38 @@ struct WSweep {
 };
 
 }  // namespace mpk
+
+namespace mpk {
+
+// Shuffle-wavefront plan (swf.cu): stencil-structured real sweeps, one
+// phase per launch.  Records: per (group, chunk of kSwfT steps) the steps'
+// factor values [step][nk/2][32 lanes][2] (+ backward: [32][divisor, RN
+// reciprocal]) -- chunkb bytes, streamed by one TMA bulk copy per chunk.
+constexpr int kSwfT = 16;
+constexpr int kSwfMaxW = 2;
+
+struct SPhase {
+  int fwd = 1;
+  int Lc = 0, lag = 0, nlanes = 0, ngroups = 0;
+  int S = 0, nch = 0;     // steps per group (multiple of kSwfT), chunks
+  int pat = 0, nk = 0;    // key pattern (swf.cu kPat), value slots per row
+  int chunkb = 0;         // bytes per chunk record
+  int wbytes = 0;         // shared memory per warp
+  int rhs16 = 0;          // 16-byte right-hand-side copies possible
+  int rpf = 0;            // L2 prefetch distance of the right-hand sides (chunks, 0: off)
+  int pf = 0;             // L2 prefetch distance of the records (chunks, 0: off)
+  unsigned char *rec = nullptr;
+  int *esrc = nullptr;    // value slot ((g*S+s)*nk+e)*32+j -> lu index / -1
+  int *dsrc = nullptr;    // divisor slot (g*S+s)*32+j -> lu index / -1
+  long long nslots = 0, ndslots = 0;
+};
+
+struct SSweep {
+  int on = 0;
+  SPhase f, b;
+  int W = 0;           // warps (groups) per CTA
+  size_t smem = 0;     // dynamic shared memory per CTA
+  long long cost = 0;  // modelled critical path (steps)
+};
+
+}  // namespace mpk

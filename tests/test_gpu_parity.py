@@ -352,6 +352,7 @@ SWEEP_PATHS = {
     "dflow8": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "8"},
     "dflow16": {"MPK_RSWEEP": "0", "MPK_CSWEEP_C": "16"},
     "wavefront": {"MPK_SWEEP_PICK": "wf"},
+    "shuffle_wavefront": {"MPK_SWEEP_PICK": "swf"},
 }
 
 
@@ -397,7 +398,7 @@ WF_MATS = {
 
 
 @pytest.mark.parametrize("mat", list(WF_MATS))
-@pytest.mark.parametrize("pick", ["wf", "auto"])
+@pytest.mark.parametrize("pick", ["wf", "swf", "auto"])
 def test_device_wavefront_sweep_bitwise(pkg, monkeypatch, mat, pick):
     """The lane-chunk wavefront plan (wf.cu; grid stencils in natural order,
     5-/9-point 2D real, 7-point 3D complex, grids not a multiple of a warp)
@@ -406,8 +407,8 @@ def test_device_wavefront_sweep_bitwise(pkg, monkeypatch, mat, pick):
     import oracle.oracle as orc
     from paper_2504_14498_b200 import problems
 
-    if pick == "wf":
-        monkeypatch.setenv("MPK_SWEEP_PICK", "wf")
+    if pick != "auto":
+        monkeypatch.setenv("MPK_SWEEP_PICK", pick)
     rp, ci, vre, vim = WF_MATS[mat](problems)
     n = len(rp) - 1
     A = _csr(pkg, rp, ci, vre, vim)
@@ -427,11 +428,12 @@ def test_device_wavefront_sweep_bitwise(pkg, monkeypatch, mat, pick):
             assert bits_equal(z.im, zi), (mat, pick, rep)
 
 
-def test_device_wavefront_solve_cfg1(pkg, monkeypatch):
-    """cfg1 DD BiCGSTAB with the wavefront plan inside the captured solver
+@pytest.mark.parametrize("pick", ["wf", "swf"])
+def test_device_wavefront_solve_cfg1(pkg, monkeypatch, pick):
+    """cfg1 DD BiCGSTAB with the wavefront plans inside the captured solver
     graph: the reference's iteration count, and in twin mode a residual
     history bit-identical to the golden fixture."""
-    monkeypatch.setenv("MPK_SWEEP_PICK", "wf")
+    monkeypatch.setenv("MPK_SWEEP_PICK", pick)
     from paper_2504_14498_b200 import problems
 
     g = golden("solver_cfg1.npz")
