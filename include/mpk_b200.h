@@ -200,6 +200,12 @@ int mpk_from_planar(mpk_ctx *ctx, int64_t n, int k, const double *dev,
  * kernel) of a k-component input, over reps launches.  Needs factors. */
 int mpk_bench_apply(mpk_matrix *m, int k, int reps, double *ms_avg);
 
+/* Kernel probe for the SpMV roofline: average device time of one mixed
+ * SpMV y = A x (binary64 A, x an exactly promoted binary64 "F" vector -- an
+ * ILU(0)-mixed output, as BiCGSTAB/CGS/GPBiCG multiply -- y k-component),
+ * the kernel behind spmv_mixed (sparse.py:465-480, _kernels.py:243-263). */
+int mpk_bench_spmv(mpk_matrix *m, int k, int reps, double *ms_avg);
+
 /* A batch of independent solves run concurrently, one native thread per
  * job, each on its matrix's own context/stream (the reference harness runs
  * cells in a thread pool, bench.py:179-216).  device_resident = 0: b/x are

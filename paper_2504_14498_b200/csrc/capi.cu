@@ -1662,6 +1662,45 @@ int mpk_bench_apply(mpk_matrix *m, int k, int reps, double *ms_avg) {
   return MPK_OK;
 }
 
+int mpk_bench_spmv(mpk_matrix *m, int k, int reps, double *ms_avg) {
+  DMat &A = m->A;
+  if (k < 2 || k > 4 || reps < 1) return fail(MPK_INVALID, "bad k/reps");
+  CKR(cudaSetDevice(m->ctx->device));
+  cudaStream_t st = m->ctx->stream;
+  const long long L = plane_ld(A.n);
+  const size_t c = A.cx ? 2 : 1;
+  double *dx = nullptr, *dy = nullptr;
+  // x: an F vector (binary64 head, the output of an ILU(0)-mixed apply, as
+  // in BiCGSTAB/CGS/GPBiCG); y: a k-component planar MC vector
+  CKR(cudaMalloc(&dx, sizeof(double) * c * L));
+  CKR(cudaMalloc(&dy, sizeof(double) * c * k * L));
+  CKR(cudaMemsetAsync(dx, 0, sizeof(double) * c * L, st));
+  CKR(cudaMemcpyAsync(dx, A.val, sizeof(double) * (A.n < A.nnz ? A.n : A.nnz),
+                      cudaMemcpyDeviceToDevice, st));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double tot = 0.0;
+  int rc = 0;
+  for (int r = 0; r < reps && rc == 0; ++r) {
+    cudaEventRecord(e0, st);
+    rc = unit_spmv(A, k, false, true, dx, dy, st);
+    cudaEventRecord(e1, st);
+    CKR(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    tot += ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(dx);
+  cudaFree(dy);
+  CKR(cudaGetLastError());
+  if (rc) return fail(MPK_INVALID, "spmv dispatch");
+  *ms_avg = tot / reps;
+  return MPK_OK;
+}
+
 static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
                       double eps_abs, int64_t max_iter, const double *d_b,
                       double *d_x, double *d_hist, int64_t hist_cap,

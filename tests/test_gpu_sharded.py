@@ -3,8 +3,11 @@ mode) on ONE GPU: W virtual ranks in this process (each on its own thread
 and stream; the all-gathers are device copies ordered by events, no kernel
 waits on another rank's kernel).  Every rank must take the same decisions
 (iteration count, residual history bit for bit across ranks) and agree
-with the single-GPU solve within the north-star DD bound (the partial
-blocks differ: W*Gl instead of one grid, so the tree differs in rounding)."""
+with the single-GPU solve and with the CPU oracle (the reference restated,
+tests/test_oracle_golden.py) within the north-star DD bound (the partial
+blocks differ: W*Gl instead of one grid, so the tree differs in rounding);
+at full cfg4 size the sharded solve is held to the REFERENCE's own
+20-iteration history (tests/golden/cfg4_ref.npz)."""
 
 from __future__ import annotations
 
@@ -71,6 +74,59 @@ def test_sharded_virtual_ranks_match_single(world):
         assert np.array_equal(np.asarray(rep.history), np.asarray(out[0].history))
         assert np.array_equal(rep.x.re, out[0].x.re)
     assert _dev(out[0].history, single.history) <= 1e-25
+    # against the oracle (the reference's algorithm on the CPU)
+    import oracle.oracle as orc
+
+    orep, _, _, ohist = orc.solve(A.n, A.row_ptr, A.col_idx, np.asarray(A.val_re)[:, 0], None,
+                                  "bicgstab", 2, b.re, eps_rel=1e-20, max_iter=400)
+    assert out[0].iterations == orep.iterations
+    assert _dev(out[0].history, ohist) <= 1e-25
+
+
+def _run_ranks(A, b, cfg, world):
+    from paper_2504_14498_b200.sharded import Communicator, solve_sharded
+
+    comms = Communicator.local(world)
+    out = [None] * world
+    err = []
+
+    def run(r):
+        try:
+            out[r] = solve_sharded(A, b, cfg, comms[r])
+        except Exception as e:  # surfaced below
+            err.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for c in comms:
+        c.close()
+    assert not err, err
+    return out
+
+
+def test_sharded_cfg4_full_size_vs_reference():
+    """cfg4 at full size (n = 4,194,304), rows sharded over 2 virtual ranks:
+    20 DD BiCGSTAB iterations within 1e-25 of the reference's history."""
+    import paper_2504_14498_b200 as mpk
+    from paper_2504_14498_b200 import problems
+
+    from conftest import golden
+
+    g = golden("cfg4_ref.npz")
+    p = problems.cfg4()
+    P = mpk.Precision.DD
+    A = mpk.CsrMatrix.from_binary64(p.n, p.row_ptr, p.col_idx, p.val_re, None, P)
+    b = mpk.spmv_mixed(A.demoted(), mpk.DenseVector.from_float64(p.x_true, P))
+    cfg = mpk.SolverConfig(method="bicgstab", precision=P, precond=mpk.PrecondMode.ILU0_MIXED,
+                           spmv_mode="mixed", eps_rel=p.eps_rel, eps_abs=p.eps_abs, max_iter=20)
+    out = _run_ranks(A, b, cfg, 2)
+    for rep in out:
+        assert rep.iterations == 20
+        assert np.array_equal(np.asarray(rep.history), np.asarray(out[0].history))
+    assert _dev(out[0].history, g["bicgstab_dd_hist"]) <= 1e-25
 
 
 def test_sharded_nccl_world1_and_bad_shapes():
