@@ -206,6 +206,16 @@ int mpk_bench_apply(mpk_matrix *m, int k, int reps, double *ms_avg);
  * the kernel behind spmv_mixed (sparse.py:465-480, _kernels.py:243-263). */
 int mpk_bench_spmv(mpk_matrix *m, int k, int reps, double *ms_avg);
 
+/* Sweep plan of an uploaded pattern: info[0..1] = DAG levels of the forward
+ * (L) and backward (U) phases; info[2] = plan kept by the upload-time
+ * autotuning (0 sync-free global, 1 single-CTA, 2 cluster, 3 ring,
+ * 4 lane-chunk wavefront, 5 shuffle wavefront); for plan 5, info[3..11] =
+ * line length, forward lag, groups, forward steps per group, backward lag,
+ * backward steps, warps per CTA, forward / backward record bytes per chunk.
+ * (Diagnostics for the bench's critical-path roofline; no reference
+ * counterpart.) */
+int mpk_sweep_info(mpk_matrix *m, int64_t *info, int ninfo);
+
 /* A batch of independent solves run concurrently, one native thread per
  * job, each on its matrix's own context/stream (the reference harness runs
  * cells in a thread pool, bench.py:179-216).  device_resident = 0: b/x are

@@ -46,7 +46,7 @@ EXPORTS = (
     "mpk_ilu0_download", "mpk_ilu0_apply_f64", "mpk_ilu0_apply_mixed",
     "mpk_spmv_mixed", "mpk_hdot", "mpk_norm2", "mpk_axpy", "mpk_mc_elementwise",
     "mpk_mc_host", "mpk_solve", "mpk_plane_ld", "mpk_solve_dev", "mpk_to_planar",
-    "mpk_from_planar", "mpk_solve_batch", "mpk_ctx_stream", "mpk_bench_apply", "mpk_bench_spmv",
+    "mpk_from_planar", "mpk_solve_batch", "mpk_ctx_stream", "mpk_bench_apply", "mpk_bench_spmv", "mpk_sweep_info",
     "mpk_csr_set_values", "mpk_run_jobs", "mpk_ctx_set_option",
     "mpk_comm_unique_id", "mpk_comm_create", "mpk_comm_create_local", "mpk_comm_destroy",
     "mpk_comm_rank", "mpk_comm_world", "mpk_solve_dev_sharded",

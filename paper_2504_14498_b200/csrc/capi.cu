@@ -1662,6 +1662,29 @@ int mpk_bench_apply(mpk_matrix *m, int k, int reps, double *ms_avg) {
   return MPK_OK;
 }
 
+int mpk_sweep_info(mpk_matrix *m, int64_t *info, int ninfo) {
+  if (!m || !info || ninfo < 1) return fail(MPK_INVALID, "bad arguments");
+  const DMat &A = m->A;
+  const SweepMats &S = A.smat;
+  int64_t v[12] = {0};
+  v[0] = A.levels_f;
+  v[1] = A.levels_b;
+  v[2] = S.ss.on ? 5 : S.wf.on ? 4 : S.rs.nchunks > 0 ? 3 : S.cs.C > 0 ? 2 : A.smat_built ? 1 : 0;
+  if (S.ss.on) {
+    v[3] = S.ss.f.Lc;
+    v[4] = S.ss.f.lag;
+    v[5] = S.ss.f.ngroups;
+    v[6] = S.ss.f.S;
+    v[7] = S.ss.b.lag;
+    v[8] = S.ss.b.S;
+    v[9] = S.ss.W;
+    v[10] = S.ss.f.chunkb;
+    v[11] = S.ss.b.chunkb;
+  }
+  for (int i = 0; i < ninfo && i < 12; ++i) info[i] = v[i];
+  return MPK_OK;
+}
+
 int mpk_bench_spmv(mpk_matrix *m, int k, int reps, double *ms_avg) {
   DMat &A = m->A;
   if (k < 2 || k > 4 || reps < 1) return fail(MPK_INVALID, "bad k/reps");

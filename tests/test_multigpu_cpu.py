@@ -170,3 +170,23 @@ def test_gloo_two_ranks_sharded_exchange_layout():
     gl = blocks_per_rank(2)
     for s in range(2):
         assert np.array_equal(part[s, : 2 * gl, 0], 100 * s + np.arange(2 * gl))
+
+
+def test_bench_gpus_flag_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks
+    (torch.distributed.run, 127.0.0.1); the launch check runs the rank
+    plumbing over gloo and rank 0 reports n_gpus = 2."""
+    import json
+    import pathlib
+    import subprocess
+    import sys
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in __import__("os").environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--launch-check"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 2 and d["ranks_seen"] == 2
