@@ -60,9 +60,8 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kT = kSwfT;     // steps per chunk (record copy granularity)
-constexpr int kNB = 3;        // record buffers per warp
+constexpr int kNB = 4;        // record buffers (TMA) per group
 constexpr int kR = 128;       // previous-line ring slots (power of two)
-constexpr int kNF = 32;       // "producer chunk done" mbarriers per warp (power of two)
 
 __device__ __forceinline__ uint32_t s_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -135,6 +134,30 @@ __device__ __forceinline__ void g_pub(double *p, double v) {
   asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(w) : "memory");
 }
 
+// Split form of s_fast_div: the Markstein candidate (on the dependency
+// chain) and its RN proof (evaluated later, off the chain).
+__device__ __forceinline__ double s_markstein(double a, double d, double r) {
+  const double q0 = __dmul_rn(a, r);
+  const double e0 = fma(-q0, d, a);
+  return fma(e0, r, q0);
+}
+// Branch-free (no short circuits: the compiler must not put a branch
+// between a step's quotient and its shuffle).  Exponent fields in
+// (256, 1792): no under/overflow anywhere in the test; q not a power of
+// two (symmetric ulp); then q == RN(a/d) iff |a - q d| < |d| ulp(q)/2.
+__device__ __forceinline__ bool s_rn_proof(double a, double d, double q2) {
+  const double e2 = fma(-q2, d, a);
+  const unsigned qh = (unsigned)__double2hiint(q2), ql = (unsigned)__double2loint(q2);
+  const unsigned ah = (unsigned)__double2hiint(a), dh = (unsigned)__double2hiint(d);
+  const unsigned eq = (qh >> 20) & 0x7ff, ea = (ah >> 20) & 0x7ff, ed = (dh >> 20) & 0x7ff;
+  const unsigned range = (unsigned)(eq - 257u < 1535u) & (unsigned)(ea - 257u < 1535u) &
+                         (unsigned)(ed - 257u < 1535u);
+  const unsigned frac = (unsigned)(((qh & 0xFFFFFu) | ql) != 0u);
+  const double half_ulp = __hiloint2double((int)((eq - 53u) << 20), 0);
+  const unsigned tight = (unsigned)(fabs(e2) < __dmul_rn(fabs(d), half_ulp));
+  return (range & frac & tight) != 0u;
+}
+
 // a / d with the reference's RN semantics (= __ddiv_rn): Markstein
 // correction of a * RN(1/d), then an exact residual test that proves the
 // candidate is RN(a/d) (|a - q d| < |d| ulp(q)/2 with the residual exact by
@@ -160,17 +183,19 @@ __device__ __forceinline__ double s_fast_div(double a, double d, double r, bool 
 // chunk on its (rare) branch instead of if-converted into every chunk
 __device__ __noinline__ void swf_rerun_mark() { asm volatile("" ::: "memory"); }
 
-// per-warp shared-memory region: record mbarriers | producer-chunk mbarriers
-// | consumer progress | previous-line ring | rhs ring | records
-constexpr int kRD = 3;            // rhs ring depth (chunks)
-constexpr int kRhsRow = kT + 2;   // doubles per lane row (16-byte aligned)
+// Shared memory of one CTA (= one group: a compute warp and a helper warp):
+// record mbarriers | ready / done mbarriers | previous-line ring | rhs
+// staging | output staging | record buffers (TMA)
+constexpr int kQ = 4;             // rhs / output staging depth (chunks)
+constexpr int kRow = kT + 2;      // doubles per lane row (16-byte aligned)
 struct SwfSmem {
-  static constexpr int kBars = 0;
-  static constexpr int kFull = 64;
-  static constexpr int kProg = kFull + kNF * 8;
-  static constexpr int kRing = kProg + 64;
+  static constexpr int kRec = 0;                   // kNB mbarriers
+  static constexpr int kReady = 64;                // kQ mbarriers
+  static constexpr int kDone = kReady + kQ * 8;    // kQ mbarriers
+  static constexpr int kRing = 128;
   static constexpr int kRhs = kRing + kR * 8;
-  static constexpr int kBuf = kRhs + kRD * 32 * kRhsRow * 8;
+  static constexpr int kOut = kRhs + kQ * 32 * kRow * 8;
+  static constexpr int kBuf = (kOut + kQ * 32 * kRow * 8 + 127) / 128 * 128;
 };
 
 __host__ __device__ constexpr int swf_stepb(int nk, bool fwd) {
@@ -200,186 +225,50 @@ __device__ __forceinline__ long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// chunk-level clock stamps of groups 0 and 1 (swf_dbg_on == 2): per chunk
-// [top, after record wait, after rhs wait, after acquire, after steps, end]
+// chunk-level clock stamps of groups 0 and 1 (swf_dbg_on == 2), compute
+// warp: [top, after ready wait, after record wait, after steps, after
+// publish to staging, end]
 __device__ long long swf_dbgc[2][2][512][6];
 
+// Geometry of one group shared by its two warps.
+struct SwfGeo {
+  int n, Lc, lag, nch, g;
+  int j;               // lane (= line within the group)
+  long long lbase;     // global position of the lane's line start
+  int plim;            // active positions of the line: [0, plim)
+  bool has_prev;       // the group's first line has a predecessor
+  long long pbase;     // global position of the previous line's start
+  __device__ __forceinline__ SwfGeo(const SweepArgs &a, const SPhase &P, int g_) {
+    n = a.n;
+    Lc = P.Lc;
+    lag = P.lag;
+    nch = P.nch;
+    g = g_;
+    j = threadIdx.x & 31;
+    lbase = (long long)(g * 32 + j) * Lc;
+    plim = (g * 32 + j) < P.nlanes ? (int)min((long long)Lc, (long long)n - lbase) : 0;
+    has_prev = g > 0;
+    pbase = (long long)(g * 32 - 1) * Lc;
+  }
+};
+
+// ---------------------------------------------------------------------
+// compute warp: the rows of the group's 32 lines, T steps per chunk
+// ---------------------------------------------------------------------
 template <int NK, int KEYS, bool FWD>
-__device__ __forceinline__ void swf_group(const SweepArgs &a, const SPhase &P, int g,
-                                          int w, int W, unsigned char *wb,
-                                          unsigned char *sm) {
+__device__ __forceinline__ void swf_compute(const SweepArgs &a, const SPhase &P, int g,
+                                            unsigned char *sm) {
   constexpr int STEPB = swf_stepb(NK, FWD);
-  constexpr int H = swf_depth<NK, KEYS>();
-  const int j = threadIdx.x & 31;
-  const int n = a.n, Lc = P.Lc, lag = P.lag, nch = P.nch;
-  const long long lbase = (long long)(g * 32 + j) * Lc;
-  // active positions of this lane's line: [0, plim)
-  const int plim = (g * 32 + j) < P.nlanes ? (int)min((long long)Lc, (long long)n - lbase) : 0;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(wb + SwfSmem::kBars);
-  double *ring = reinterpret_cast<double *>(wb + SwfSmem::kRing);
-  double *rhsb = reinterpret_cast<double *>(wb + SwfSmem::kRhs);
-  unsigned char *buf = wb + SwfSmem::kBuf;
+  const SwfGeo G(a, P, g);
+  const int j = G.j, lag = G.lag, nch = G.nch;
+  uint64_t *rec_bar = reinterpret_cast<uint64_t *>(sm + SwfSmem::kRec);
+  uint64_t *ready = reinterpret_cast<uint64_t *>(sm + SwfSmem::kReady);
+  uint64_t *done = reinterpret_cast<uint64_t *>(sm + SwfSmem::kDone);
+  const double *ring = reinterpret_cast<const double *>(sm + SwfSmem::kRing);
+  unsigned char *buf = sm + SwfSmem::kBuf;
   const uint32_t cb = (uint32_t)P.chunkb;
-  const unsigned char *src = P.rec + (size_t)g * nch * cb;
-  double *out = FWD ? a.y : a.z;
-  const double *rin = FWD ? a.in_re : a.y;
-  // lane 31 feeds the next warp's ring when that group exists in this CTA:
-  // every step it stores its result into the consumer's ring, and at the end
-  // of each chunk it arrives on the consumer's "chunk done" mbarrier
-  // (release); the consumer sleeps on it (try_wait).
-  unsigned char *wnext = (w + 1 < W && g + 1 < P.ngroups)
-                             ? sm + (size_t)(w + 1) * P.wbytes
-                             : nullptr;
-  double *ring_next = wnext ? reinterpret_cast<double *>(wnext + SwfSmem::kRing) : nullptr;
-  uint64_t *full_next = wnext ? reinterpret_cast<uint64_t *>(wnext + SwfSmem::kFull) : nullptr;
-  const int *prog_next = wnext ? reinterpret_cast<const int *>(wnext + SwfSmem::kProg) : nullptr;
-  uint64_t *full_own = reinterpret_cast<uint64_t *>(wb + SwfSmem::kFull);
-  int *prog_own = reinterpret_cast<int *>(wb + SwfSmem::kProg);
-  const bool glob_prev = (w == 0);  // the previous line comes from global memory
-  const bool has_prev = g > 0;
-  const bool feed = (j == 31) && ring_next != nullptr;
-  // global index of position p of the previous line (lane 0's view)
-  const long long pbase = (long long)(g * 32 - 1) * Lc;
-  auto prow = [&](int p) -> long long {
-    const long long q = pbase + p;
-    return FWD ? q : (long long)n - 1 - q;
-  };
-  auto prev_ok = [&](int p) { return has_prev && p >= 0 && p < Lc; };
-  const bool r16 = P.rhs16 != 0;
-  // producer chunk whose completion covers positions up to c*T + T - 1 + lag
-  const int cshift = (32 * lag + kT - 1) / kT;
-
-  // ---- record stream: kNB chunks in flight (TMA), L2 prefetch pf ahead ----
-  const int pf = P.pf;
-  auto rec_prefetch = [&](int c) {
-    if (c < nch)
-      for (int off = j * 128; off < (int)cb; off += 32 * 128)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (size_t)c * cb + off));
-  };
-  if (j == 0) {
-    const int first = nch < kNB ? nch : kNB;
-    for (int c = 0; c < first; ++c) {
-      s_mbar_arrive_tx(bars + c, cb);
-      s_bulk(buf + (size_t)c * cb, src + (size_t)c * cb, cb, bars + c);
-    }
-  }
-  for (int c = kNB; c < pf; ++c) rec_prefetch(c);
-
-  // ---- right-hand sides: chunk c's T positions of the lane, copied by
-  // cp.async into a kRD-deep shared ring (one commit group per chunk, the
-  // 16-byte copies of chunk c+2 spread over the steps of chunk c); position t
-  // of a chunk sits at index t (forward) or T-1-t (backward: rows descend) ----
-  auto rhs_slot = [&](int c) { return rhsb + ((c % kRD) * 32 + j) * kRhsRow; };
-  auto rhs_full = [&](int c) {
-    const int p0 = c * kT - lag * j;
-    return r16 && c < nch && p0 >= 0 && p0 + kT <= plim;
-  };
-  auto rhs_gsrc = [&](int c) -> const double * {
-    const int p0 = c * kT - lag * j;
-    return FWD ? rin + lbase + p0 : rin + ((long long)n - kT - lbase - p0);
-  };
-  auto rhs_scalar = [&](int c) {  // partial / unaligned chunk: 8-byte copies
-    if (c >= nch || rhs_full(c)) return;
-    const int p0 = c * kT - lag * j;
-    double *d0 = rhs_slot(c);
-#pragma unroll
-    for (int t = 0; t < kT; ++t) {
-      const int p = p0 + t;
-      if (p >= 0 && p < plim) {
-        const long long row = FWD ? lbase + p : (long long)n - 1 - lbase - p;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_u32(d0 + (FWD ? t : kT - 1 - t))),
-                     "l"(rin + row)
-                     : "memory");
-      }
-    }
-  };
-  auto rhs_pair = [&](int c, int u) {  // 16-byte copy u of a full chunk
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s_u32(rhs_slot(c) + 2 * u)),
-                 "l"(rhs_gsrc(c) + 2 * u)
-                 : "memory");
-  };
-  auto rhs_issue_all = [&](int c) {
-    if (rhs_full(c)) {
-#pragma unroll
-      for (int u = 0; u < kT / 2; ++u) rhs_pair(c, u);
-    } else {
-      rhs_scalar(c);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  auto rhs_prefetch = [&](int c) {
-    const int p0 = c * kT - lag * j;
-    if (c < nch && p0 + kT > 0 && p0 < plim) {
-      const int pa = p0 < 0 ? 0 : p0;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(FWD ? rin + lbase + pa
-                                                        : rin + ((long long)n - 1 - lbase - pa)));
-    }
-  };
-  const int rpf = P.rpf;
-  for (int c = 0; c < kRD - 1; ++c) rhs_issue_all(c);
-  for (int c = kRD - 1; c <= rpf; ++c) rhs_prefetch(c);
-
-  // ---- the previous line (lane 31 sends it to lane 0) ----
-  // ring slot of position p: ring[p & (kR-1)].  Warp 0: lanes 0..T-1 load
-  // chunk c+2's positions from global memory at the top of chunk c and store
-  // them (checked: a sentinel is polled until published) at the top of chunk
-  // c+1.  Other warps: the previous warp's lane 31 stores every result.
-  double cv = 0.0;
-  int cvp = -1;
-  auto cross_load = [&](int c) {  // positions of chunk c: c*T + t + lag
-    cvp = -1;
-    if (glob_prev && has_prev && j < kT && c < nch) {
-      const int p = c * kT + j + lag;
-      if (p < Lc) {
-        cvp = p;
-        cv = ld_relaxed(out + prow(p));
-      }
-    }
-  };
-  auto cross_store = [&]() {  // the values loaded one chunk ago, checked
-    if (cvp >= 0) {
-      if (s_sent(cv)) {
-        // not yet published when loaded: wait, and build slack by waiting
-        // for the furthest position loaded so far too
-        int pa = cvp + 2 * kT;
-        if (pa >= Lc) pa = Lc - 1;
-        g_poll(out + prow(pa));
-        cv = g_poll(out + prow(cvp));
-      }
-      s_stv(ring + (cvp & (kR - 1)), cv);
-    }
-  };
-  // consumer side (w >= 1): producer chunk cp done <=> its mbarrier phase cp
-  auto wait_prod = [&](int cp) {
-    if (cp >= nch) cp = nch - 1;
-    if (!glob_prev && cp >= 0)
-      s_mbar_wait(full_own + (cp & (kNF - 1)), (uint32_t)((cp / kNF) & 1));
-  };
+  constexpr int H = swf_depth<NK, KEYS>();
   double o[4] = {0.0, 0.0, 0.0, 0.0}, q[4] = {0.0, 0.0, 0.0, 0.0};
-  if (glob_prev && has_prev) {
-    // pre-roll (lag-H .. lag-1) and chunk 0 (lag .. lag+T-1), polled until
-    // published; then wait 2 chunks further ahead so that the loads issued
-    // from here on find published values
-    const int p = lag - H + j;
-    if (j < H + kT && prev_ok(p)) s_stv(ring + (p & (kR - 1)), g_poll(out + prow(p)));
-    if (j == 0) {
-      int pa = lag + 3 * kT - 1;
-      if (pa >= Lc) pa = Lc - 1;
-      g_poll(out + prow(pa));
-    }
-    cross_load(1);
-  }
-  wait_prod(cshift);  // the pre-roll and chunk 0's positions
-  __syncwarp();
-  {
-    double pre[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int d = H; d >= 1; --d)
-      if (prev_ok(lag - d)) pre[(4 - d) & 3] = s_ldv(ring + ((lag - d) & (kR - 1)));
-#pragma unroll
-    for (int u = 0; u < 4; ++u) q[u] = j == 0 ? pre[u] : 0.0;
-  }
-
   double lv[NK], dv = 1.0, dr = 1.0;
   auto load_step = [&](const unsigned char *rec, int t) {
 #pragma unroll
@@ -394,67 +283,52 @@ __device__ __forceinline__ void swf_group(const SweepArgs &a, const SPhase &P, i
       dr = v.y;
     }
   };
-
   const bool dbc = swf_dbg_on == 2 && g < 2 && j == 0;
   long long *dbp = &swf_dbgc[FWD ? 0 : 1][g < 2 ? g : 0][0][0];
   for (int c = 0; c < nch; ++c) {
     const int p0 = c * kT - lag * j;  // this lane's position at step 0 of the chunk
+    const int sq = c % kQ;
     if (dbc && c < 512) dbp[c * 6] = clock64();
-    s_mbar_wait(bars + (c % kNB), (uint32_t)((c / kNB) & 1));
+    s_mbar_wait(ready + sq, (uint32_t)((c / kQ) & 1));  // rhs(c) staged, ring(c) filled
     if (dbc && c < 512) dbp[c * 6 + 1] = clock64();
-    asm volatile("cp.async.wait_group %0;" ::"n"(kRD - 2) : "memory");  // rhs(c) landed
-    if (glob_prev && has_prev) {
-      cross_store();  // chunk c+1's positions
-      cross_load(c + 2);
-    } else if (c > 0) {
-      wait_prod(c + cshift);
+    if (c == 0) {
+      // the window's previous-line entries before step 0 (pre-roll)
+      double pre[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int d = H; d >= 1; --d) pre[(4 - d) & 3] = ring[(lag - d) & (kR - 1)];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = j == 0 ? pre[u] : 0.0;
     }
-    if (pf) rec_prefetch(c + pf);
-    if (rpf) rhs_prefetch(c + rpf);
-    const bool fullnext = rhs_full(c + kRD - 1);
-    if (!fullnext) rhs_scalar(c + kRD - 1);
-    __syncwarp();
+    s_mbar_wait(rec_bar + (c % kNB), (uint32_t)((c / kNB) & 1));
     if (dbc && c < 512) dbp[c * 6 + 2] = clock64();
-    if (dbc && c < 512) dbp[c * 6 + 3] = clock64();
     const unsigned char *rec = buf + (size_t)(c % kNB) * cb;
-    const double *rh = rhs_slot(c);
-    double *op = out + (FWD ? lbase + p0 : (long long)n - 1 - lbase - p0);
-    // lane 31: the previous line's value of step t (sent to lane 0)
-    const int pc0 = c * kT + lag;
+    const double *rh = reinterpret_cast<const double *>(sm + SwfSmem::kRhs) + (sq * 32 + j) * kRow;
+    double *ob = reinterpret_cast<double *>(sm + SwfSmem::kOut) + (sq * 32 + j) * kRow;
+    const int pc0 = c * kT + lag;  // previous line's position of step 0 (lane 0's view)
     // One chunk of T steps.  EXACT = false: the backward division uses the
     // Markstein quotient speculatively (its RN proof is accumulated in
-    // `okall` off the critical path); the chunk's results are published
-    // after the warp's proofs hold, else the chunk is re-run with EXACT =
-    // true (__ddiv_rn) from the saved windows.  Stores and copies of other
-    // chunks are interleaved into the steps' latency slots.
-    auto run_chunk = [&](auto exact_tag, bool &okall, double (&xo)[kT], bool first) {
+    // `okall` off the critical path); the results are handed to the helper
+    // only after the warp's proofs hold, else the chunk is re-run with
+    // EXACT = true (__ddiv_rn) from the saved windows.
+    auto run_chunk = [&](auto exact_tag, bool &okall, double (&xo)[kT]) {
       constexpr bool EXACT = decltype(exact_tag)::value;
       load_step(rec, 0);
       double rr0 = 0.0, rr1 = 0.0;
 #pragma unroll
       for (int t = 0; t < kT; ++t) {
-        const bool act = (unsigned)(p0 + t) < (unsigned)plim;
+        const bool act = (unsigned)(p0 + t) < (unsigned)G.plim;
         double l[NK];
 #pragma unroll
         for (int e = 0; e < NK; ++e) l[e] = lv[e];
         const double d0 = dv, r0 = dr;
         if (t + 1 < kT) load_step(rec, t + 1);  // next step's values, off the chain
-        if ((t & 1) == 0) {  // right-hand sides of steps t, t+1
-          if constexpr (FWD) {  // position t at index t
-            const double2 v = reinterpret_cast<const double2 *>(rh)[t / 2];
-            rr0 = v.x;
-            rr1 = v.y;
-          } else {  // position t at index T-1-t
-            const double2 v = reinterpret_cast<const double2 *>(rh)[(kT - 2 - t) / 2];
-            rr0 = v.y;
-            rr1 = v.x;
-          }
+        if ((t & 1) == 0) {  // right-hand sides of steps t, t+1 (position order)
+          const double2 v = reinterpret_cast<const double2 *>(rh)[t / 2];
+          rr0 = v.x;
+          rr1 = v.y;
         }
-        if (first && fullnext && t < kT / 2) rhs_pair(c + kRD - 1, t);
-        // previous line's value of this step, for lane 31 to send
-        const int pc = pc0 + t;
-        double av = 0.0;
-        if (j == 31 && prev_ok(pc)) av = ring[pc & (kR - 1)];
+        // lane 31 sends the previous line's value of this step to lane 0
+        const double av = ring[(pc0 + t) & (kR - 1)];
         double acc = (t & 1) ? rr1 : rr0;
 #pragma unroll
         for (int e = 0; e < NK; ++e) {
@@ -468,29 +342,28 @@ __device__ __forceinline__ void swf_group(const SweepArgs &a, const SPhase &P, i
           if constexpr (EXACT) {
             x = __ddiv_rn(acc, d0);
           } else {
-            bool ok;
-            x = s_fast_div(acc, d0, r0, ok);
-            okall &= ok || !act;
+            x = s_markstein(acc, d0, r0);
           }
         }
         const double xv = act ? x : 0.0;
         o[t & 3] = xv;
         q[t & 3] = __shfl_sync(kFull, (act && j != 31) ? x : av, (j + 31) & 31);
-        if constexpr (FWD) {  // publish in the step's latency slots
-          if (act) {
-            asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(op + t), "d"(xv)
-                         : "memory");
-            if (feed) ring_next[(p0 + t) & (kR - 1)] = xv;
-          }
+        if constexpr (FWD) {
+          ob[t] = xv;  // to the helper's output staging
         } else {
           xo[t] = xv;
+          if constexpr (!EXACT) {
+            // the RN proof of this step's quotient, after its shuffle: off
+            // the dependency chain of the next step
+            okall = okall & ((!act) | s_rn_proof(acc, d0, x));
+          }
         }
       }
     };
     bool okall = true;
     double xo[kT];
     if constexpr (FWD) {
-      run_chunk(std::false_type{}, okall, xo, true);
+      run_chunk(std::false_type{}, okall, xo);
     } else {
       double os[4], qs[4];
 #pragma unroll
@@ -498,7 +371,7 @@ __device__ __forceinline__ void swf_group(const SweepArgs &a, const SPhase &P, i
         os[u] = o[u];
         qs[u] = q[u];
       }
-      run_chunk(std::false_type{}, okall, xo, true);
+      run_chunk(std::false_type{}, okall, xo);
       if (swf_dbg_on == 3) okall = false;  // test hook: force the exact re-run
       if (__any_sync(kFull, !okall)) {     // rare: some quotient not proven RN
 #pragma unroll
@@ -507,46 +380,198 @@ __device__ __forceinline__ void swf_group(const SweepArgs &a, const SPhase &P, i
           q[u] = qs[u];
         }
         swf_rerun_mark();
-        run_chunk(std::true_type{}, okall, xo, false);
+        run_chunk(std::true_type{}, okall, xo);
       }
-      // publish the proven chunk (non-finite results: NumericBreakdownError)
-      double nfin = 0.0;
+      double nfin = 0.0;  // NaN iff a result is non-finite (NumericBreakdownError)
 #pragma unroll
-      for (int t = 0; t < kT; ++t) {
-        if ((unsigned)(p0 + t) < (unsigned)plim) {
-          asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(op - t), "d"(xo[t])
-                       : "memory");
-          if (feed) ring_next[(p0 + t) & (kR - 1)] = xo[t];
-        }
-        nfin = fma(xo[t], 0.0, nfin);
+      for (int t = 0; t < kT; t += 2) {
+        reinterpret_cast<double2 *>(ob)[t / 2] = make_double2(xo[t], xo[t + 1]);
+        nfin = fma(xo[t], 0.0, fma(xo[t + 1], 0.0, nfin));
       }
       if (!isfinite(nfin)) atomicOr(a.err, 1);
     }
-    if (dbc && c < 512) dbp[c * 6 + 4] = clock64();
-    asm volatile("cp.async.commit_group;" ::: "memory");  // rhs(c + kRD - 1)
-    if (feed) {
-      // throttle: the consumer must have taken the ring slots the next
-      // chunks overwrite, and must not fall kNF phases behind
-      while (c + 1 > s_ldv_i(prog_next) + cshift + 6) __nanosleep(64);
-      s_mbar_arrive_rel(full_next + (c & (kNF - 1)));
-    }
-    if (!glob_prev && j == 31) s_stv_i(prog_own, c);  // ring positions of chunk c consumed
-    __syncwarp();
+    if (dbc && c < 512) dbp[c * 6 + 3] = clock64();
+    s_mbar_arrive_rel(done + sq);  // (count 32) outputs staged, buffers free
     if (dbc && c < 512) dbp[c * 6 + 5] = clock64();
-    // record chunk c consumed: refill its buffer with chunk c + kNB
+  }
+}
+
+// ---------------------------------------------------------------------
+// helper warp: records (TMA), right-hand sides (cp.async), the previous
+// line (polled in global memory), publication of the results
+// ---------------------------------------------------------------------
+template <bool FWD>
+__device__ __forceinline__ void swf_helper(const SweepArgs &a, const SPhase &P, int g,
+                                           unsigned char *sm) {
+  const SwfGeo G(a, P, g);
+  const int j = G.j, lag = G.lag, nch = G.nch, n = G.n, Lc = G.Lc;
+  uint64_t *rec_bar = reinterpret_cast<uint64_t *>(sm + SwfSmem::kRec);
+  uint64_t *ready = reinterpret_cast<uint64_t *>(sm + SwfSmem::kReady);
+  uint64_t *done = reinterpret_cast<uint64_t *>(sm + SwfSmem::kDone);
+  double *ring = reinterpret_cast<double *>(sm + SwfSmem::kRing);
+  unsigned char *buf = sm + SwfSmem::kBuf;
+  const uint32_t cb = (uint32_t)P.chunkb;
+  const unsigned char *src = P.rec + (size_t)g * nch * cb;
+  double *out = FWD ? a.y : a.z;
+  const double *rin = FWD ? a.in_re : a.y;
+  const bool r16 = P.rhs16 != 0;
+  constexpr int HMAX = 4;
+
+  // rows of the lane's positions p0 .. p0+T-1 of chunk c
+  auto rowp = [&](int c) -> long long {
+    const int p0 = c * kT - lag * j;
+    return FWD ? G.lbase + p0 : (long long)n - kT - G.lbase - p0;  // lowest row (bwd)
+  };
+  auto full = [&](int c) {
+    const int p0 = c * kT - lag * j;
+    return p0 >= 0 && p0 + kT <= G.plim;
+  };
+  // chunk c's right-hand sides into staging slot c % kQ in POSITION order
+  auto rhs_issue = [&](int c) {
+    if (c < nch) {
+      double *d0 = reinterpret_cast<double *>(sm + SwfSmem::kRhs) + ((c % kQ) * 32 + j) * kRow;
+      const int p0 = c * kT - lag * j;
+      if (FWD && r16 && full(c)) {
+        const double *g0 = rin + rowp(c);
+#pragma unroll
+        for (int u = 0; u < kT / 2; ++u)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s_u32(d0 + 2 * u)),
+                       "l"(g0 + 2 * u)
+                       : "memory");
+      } else {
+#pragma unroll
+        for (int t = 0; t < kT; ++t) {
+          const int p = p0 + t;
+          if (p >= 0 && p < G.plim) {
+            const long long row = FWD ? G.lbase + p : (long long)n - 1 - G.lbase - p;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_u32(d0 + t)),
+                         "l"(rin + row)
+                         : "memory");
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // previous line's value of position p (lane 0's view), polled until published
+  auto prev_val = [&](int p) -> double {
+    if (!G.has_prev || p < 0 || p >= Lc) return 0.0;
+    const long long q = G.pbase + p;
+    return g_poll(out + (FWD ? q : (long long)n - 1 - q));
+  };
+  // chunk c's previous-line positions (c*T + lag + t) into the ring; chunk
+  // 0 also the pre-roll (lag - H .. lag - 1), polled until published
+  auto ring_fill = [&](int c) {
+    if (j < kT) {
+      const int p = c * kT + lag + j;
+      ring[p & (kR - 1)] = prev_val(p);
+    }
+    if (c == 0 && j >= kT && j < kT + HMAX) {
+      const int p = lag - (j - kT) - 1;
+      ring[p & (kR - 1)] = prev_val(p);
+    }
+  };
+  // steady state: lanes 0..T-1 LOAD chunk c's positions one iteration
+  // before they are stored (pv, pp) so the load latency overlaps the wait
+  // for the compute warp; a value still holding the sentinel is polled, and
+  // then the lane also waits for the furthest position of the next chunk to
+  // build slack
+  double pv = 0.0;
+  int pp = -1;
+  auto prev_load = [&](int c) {
+    pp = -1;
+    if (j < kT && c < nch && G.has_prev) {
+      const int p = c * kT + lag + j;
+      if (p < Lc) {
+        const long long q = G.pbase + p;
+        pp = p;
+        pv = ld_relaxed(out + (FWD ? q : (long long)n - 1 - q));
+      }
+    }
+  };
+  auto prev_store = [&](int c) {
+    if (j < kT) {
+      const int p = c * kT + lag + j;
+      double v = 0.0;
+      if (pp == p) {
+        v = pv;
+        if (s_sent(v)) {
+          int pa = p + kT;
+          if (pa >= Lc) pa = Lc - 1;
+          prev_val(pa);
+          v = prev_val(p);
+        }
+      }
+      ring[p & (kR - 1)] = v;
+    }
+  };
+  // publish chunk c's results (output staging slot c % kQ) to global memory
+  auto publish = [&](int c) {
+    const double *ob =
+        reinterpret_cast<const double *>(sm + SwfSmem::kOut) + ((c % kQ) * 32 + j) * kRow;
+    const int p0 = c * kT - lag * j;
+    if (r16 && full(c)) {
+      double *g0 = out + rowp(c);
+#pragma unroll
+      for (int u = 0; u < kT / 2; ++u) {
+        const double2 v = reinterpret_cast<const double2 *>(ob)[u];
+        // backward rows descend: memory pair u holds positions T-1-2u, T-2-2u
+        const double lo = FWD ? v.x : ob[kT - 1 - 2 * u];
+        const double hi = FWD ? v.y : ob[kT - 2 - 2 * u];
+        asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(g0 + 2 * u), "d"(lo),
+                     "d"(hi)
+                     : "memory");
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < kT; ++t) {
+        const int p = p0 + t;
+        if (p >= 0 && p < G.plim)
+          g_pub(out + (FWD ? G.lbase + p : (long long)n - 1 - G.lbase - p), ob[t]);
+      }
+    }
+  };
+
+  // prologue: records 0..kNB-1, right-hand sides 0..kQ-2, chunk 0 ready
+  if (j == 0) {
+    const int first = nch < kNB ? nch : kNB;
+    for (int c = 0; c < first; ++c) {
+      s_mbar_arrive_tx(rec_bar + c, cb);
+      s_bulk(buf + (size_t)c * cb, src + (size_t)c * cb, cb, rec_bar + c);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kQ - 1; ++c) rhs_issue(c);
+  ring_fill(0);
+  ring_fill(1);
+  prev_load(2);
+  asm volatile("cp.async.wait_group %0;" ::"n"(kQ - 2) : "memory");  // rhs(0) landed
+  s_mbar_arrive_rel(ready + 0);
+  for (int c = 0; c < nch; ++c) {
+    // chunk c+1 ready (its right-hand sides and previous-line values)
+    if (c + 1 < nch) {
+      if (c + 1 >= 2) {
+        prev_store(c + 1);
+        prev_load(c + 2);
+      }
+      asm volatile("cp.async.wait_group %0;" ::"n"(kQ - 3) : "memory");  // rhs(c+1)
+      s_mbar_arrive_rel(ready + (c + 1) % kQ);
+    }
+    // chunk c computed: publish it, refill its record buffer and its rhs slot
+    s_mbar_wait(done + c % kQ, (uint32_t)((c / kQ) & 1));
+    publish(c);
     if (j == 0 && c + kNB < nch) {
       const int b = c % kNB;
-      s_mbar_arrive_tx(bars + b, cb);
-      s_bulk(buf + (size_t)b * cb, src + (size_t)(c + kNB) * cb, cb, bars + b);
+      s_mbar_arrive_tx(rec_bar + b, cb);
+      s_bulk(buf + (size_t)b * cb, src + (size_t)(c + kNB) * cb, cb, rec_bar + b);
     }
+    rhs_issue(c + kQ - 1);  // slot (c - 1) % kQ: chunk c-1 is long done
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-
 template <int NK, int KEYS, bool FWD>
-__global__ void __launch_bounds__(32 * kSwfMaxW, 1)
-    swf_kernel(SweepArgs a, SPhase P, int W) {
+__global__ void __launch_bounds__(64, 1) swf_kernel(SweepArgs a, SPhase P) {
   __shared__ int s_tick;
   int *tick = a.tick;
   {  // stopped solve: skip, but count this CTA out (ticket reset)
@@ -566,40 +591,38 @@ __global__ void __launch_bounds__(32 * kSwfMaxW, 1)
   }
   extern __shared__ __align__(128) unsigned char sm[];
   const int w = threadIdx.x >> 5, j = threadIdx.x & 31;
-  unsigned char *wb = sm + (size_t)w * P.wbytes;
-  const int nct = (P.ngroups + W - 1) / W;
   for (;;) {
-    if (threadIdx.x == 0) s_tick = atomicAdd(tick, 1);
-    // fresh ring and barriers per ticket (no copy is pending here)
-    double *ring = reinterpret_cast<double *>(wb + SwfSmem::kRing);
-#pragma unroll
-    for (int u = 0; u < kR / 32; ++u) ring[j + 32 * u] = sent_val();
-    if (j == 0) {
-      uint64_t *bars = reinterpret_cast<uint64_t *>(wb + SwfSmem::kBars);
-      for (int b = 0; b < kNB; ++b) s_mbar_init(bars + b, 1);
-      uint64_t *full = reinterpret_cast<uint64_t *>(wb + SwfSmem::kFull);
-      for (int b = 0; b < kNF; ++b) s_mbar_init(full + b, 1);
-      *reinterpret_cast<int *>(wb + SwfSmem::kProg) = -1;
+    if (threadIdx.x == 0) {
+      s_tick = atomicAdd(tick, 1);
+      // fresh barriers per group (no copy is pending here)
+      uint64_t *rb = reinterpret_cast<uint64_t *>(sm + SwfSmem::kRec);
+      for (int b = 0; b < kNB; ++b) s_mbar_init(rb + b, 1);
+      uint64_t *ready = reinterpret_cast<uint64_t *>(sm + SwfSmem::kReady);
+      uint64_t *done = reinterpret_cast<uint64_t *>(sm + SwfSmem::kDone);
+      for (int b = 0; b < kQ; ++b) {
+        s_mbar_init(ready + b, 32);
+        s_mbar_init(done + b, 32);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    const int t = s_tick;
-    if (t >= nct) break;
-    const int g = t * W + w;
-    if (g < P.ngroups) {
-      if (swf_dbg_on && j == 0 && g < 4096) {
-        unsigned wid, smid;
-        asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        swf_dbg[(FWD ? 0 : 2 * 4096) + 2 * g] = gtimer();
-        if (g < 64) swf_dbgw[FWD ? 0 : 1][g] = (int)(smid * 1000 + wid);
-      }
-      swf_group<NK, KEYS, FWD>(a, P, g, w, W, wb, sm);
-      if (swf_dbg_on && j == 0 && g < 4096)
-        swf_dbg[(FWD ? 0 : 2 * 4096) + 2 * g + 1] = gtimer();
+    const int g = s_tick;
+    if (g >= P.ngroups) break;
+    if (swf_dbg_on && j == 0 && w == 0 && g < 4096) {
+      unsigned wid, smid;
+      asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      swf_dbg[(FWD ? 0 : 2 * 4096) + 2 * g] = gtimer();
+      if (g < 64) swf_dbgw[FWD ? 0 : 1][g] = (int)(smid * 1000 + wid);
     }
+    if (w == 0)
+      swf_compute<NK, KEYS, FWD>(a, P, g, sm);
+    else
+      swf_helper<FWD>(a, P, g, sm);
     __syncthreads();
+    if (swf_dbg_on && j == 0 && w == 0 && g < 4096)
+      swf_dbg[(FWD ? 0 : 2 * 4096) + 2 * g + 1] = gtimer();
   }
   // last CTA out resets the ticket for the next launch / graph replay
   if (threadIdx.x == 0) {
@@ -811,7 +834,7 @@ static void launch_pat(const SweepArgs &a, const SPhase &P, int W, int grid, siz
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  fn<<<grid, 32 * W, smem, st>>>(a, P, W);
+  fn<<<grid, 64, smem, st>>>(a, P);
 }
 
 static void launch_phase(const SweepArgs &a, const SPhase &P, int W, int grid, size_t smem,
@@ -868,25 +891,16 @@ bool build_ssweep(SSweep &w, int n, bool cx, const int *rp, const int *ci, const
     free_ssweep(t);
     return false;
   }
-  const char *ew = getenv("MPK_SSWEEP_W");
-  int W = ew ? atoi(ew) : kSwfMaxW;
-  if (W < 1) W = 1;
-  if (W > kSwfMaxW) W = kSwfMaxW;
-  const int maxg = std::max(t.f.ngroups, t.b.ngroups);
-  if (W > maxg) W = maxg;
+  // one group per CTA: a compute warp and a helper warp
   const int chunkmax = std::max(t.f.chunkb, t.b.chunkb);
   const int wbytes = (SwfSmem::kBuf + kNB * chunkmax + 127) / 128 * 128;
   t.f.wbytes = t.b.wbytes = wbytes;
-  t.W = W;
-  t.smem = (size_t)W * wbytes;
+  t.W = 1;
+  t.smem = (size_t)wbytes;
   if (t.smem > 220 * 1024) {
     free_ssweep(t);
     return false;
   }
-  const char *er = getenv("MPK_SWF_RPF");
-  t.f.rpf = t.b.rpf = er ? atoi(er) : 4;
-  const char *ep = getenv("MPK_SWF_PF");
-  t.f.pf = t.b.pf = ep ? atoi(ep) : 8;
   t.cost = cf + cbk;
   t.on = 1;
   w = t;
@@ -911,7 +925,7 @@ void launch_ssweep(const SweepArgs &a, const SSweep &w, cudaStream_t st) {
     ++tl_launches;
     SPhase Q = *P;
     if (only_g0) Q.ngroups = only_g0;  // diagnostics: timing of the first groups alone
-    int grid = (Q.ngroups + w.W - 1) / w.W;
+    int grid = Q.ngroups;
     if (grid > 148) grid = 148;
     launch_phase(a, Q, w.W, grid, w.smem, st);
   }

@@ -47,7 +47,7 @@ if len(sys.argv) > 2 and sys.argv[1] == "child":
         cb = (ctypes.c_longlong * (2 * 2 * 512 * 6))()
         L.mpk_swf_debugc(cb)
         c = np.array(cb[:], dtype=np.int64).reshape(2, 2, 512, 6)
-        names = ["rec_wait", "rhs_wait", "acquire", "steps", "publish"]
+        names = ["ready_wait", "rec_wait", "steps", "x", "arrive"]
         for ph in range(2):
             for g in range(2):
                 x = c[ph, g]
