@@ -1006,10 +1006,10 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
       if (getenv("MPK_VERBOSE"))
         fprintf(stderr,
                 "[mpk] shuffle-wavefront plan n=%lld: fwd Lc=%d lag=%d groups=%d S=%d pat=%d, "
-                "bwd Lc=%d lag=%d groups=%d S=%d pat=%d, W=%d smem=%zu; apply %.4f ms vs "
+                "bwd Lc=%d lag=%d groups=%d S=%d pat=%d, cluster=%d smem=%zu; apply %.4f ms vs "
                 "%.4f ms (other plan) -> %s\n",
                 (long long)n, ss.f.Lc, ss.f.lag, ss.f.ngroups, ss.f.S, ss.f.pat, ss.b.Lc,
-                ss.b.lag, ss.b.ngroups, ss.b.S, ss.b.pat, ss.W, ss.smem, ts, tb,
+                ss.b.lag, ss.b.ngroups, ss.b.S, ss.b.pat, ss.f.cl, ss.smem, ts, tb,
                 A.smat.ss.on ? "shuffle-wavefront" : "other");
     }
     CKR(cudaGetLastError());
@@ -1679,7 +1679,7 @@ int mpk_sweep_info(mpk_matrix *m, int64_t *info, int ninfo) {
     v[8] = S.ss.b.S;
     v[9] = S.ss.W;
     v[10] = S.ss.f.chunkb;
-    v[11] = S.ss.b.chunkb;
+    v[11] = S.ss.f.cl;
   }
   for (int i = 0; i < ninfo && i < 12; ++i) info[i] = v[i];
   return MPK_OK;

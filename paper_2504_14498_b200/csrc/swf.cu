@@ -104,6 +104,48 @@ __device__ __forceinline__ double s_ldv(const double *p) {
 __device__ __forceinline__ void s_stv(double *p, double v) {
   asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(s_u32(p)), "d"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t s_mapa(const void *p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(s_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void c_st_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void c_st_u32(uint32_t addr, int v) {
+  asm volatile("st.relaxed.cluster.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ void c_arrive_rel(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
+               : "memory");
+}
+__device__ __forceinline__ void s_mbar_wait_cl(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "SWF_WAITC%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra SWF_WAITC%=;\n}\n" ::"r"(s_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ int s_ld_acq_i(const int *p) {
+  int v;
+  // relaxed (an acquire at cluster scope costs a GPU-scope MEMBAR): the
+  // consumer stores its progress after its ring reads have been used
+  asm volatile("ld.relaxed.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(s_u32(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
 __device__ __forceinline__ void s_mbar_arrive_rel(uint64_t *b) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(b))
                : "memory");
@@ -186,15 +228,19 @@ __device__ __noinline__ void swf_rerun_mark() { asm volatile("" ::: "memory"); }
 // Shared memory of one CTA (= one group: a compute warp and a helper warp):
 // record mbarriers | ready / done mbarriers | previous-line ring | rhs
 // staging | output staging | record buffers (TMA)
-constexpr int kQ = 4;             // rhs / output staging depth (chunks)
+constexpr int kQ = 4;             // output staging depth / ready-done barriers (chunks)
+constexpr int kQR = 6;            // rhs staging depth (chunks): requested kQR-1 ahead
+constexpr int kNU = 16;           // upstream-chunk mbarriers (DSMEM hand-off)
 constexpr int kRow = kT + 2;      // doubles per lane row (16-byte aligned)
 struct SwfSmem {
   static constexpr int kRec = 0;                   // kNB mbarriers
   static constexpr int kReady = 64;                // kQ mbarriers
   static constexpr int kDone = kReady + kQ * 8;    // kQ mbarriers
-  static constexpr int kRing = 128;
+  static constexpr int kUp = kDone + kQ * 8;       // kNU mbarriers (cluster hand-off)
+  static constexpr int kProg = kUp + kNU * 8;      // downstream progress (int)
+  static constexpr int kRing = (kProg + 8 + 127) / 128 * 128;
   static constexpr int kRhs = kRing + kR * 8;
-  static constexpr int kOut = kRhs + kQ * 32 * kRow * 8;
+  static constexpr int kOut = kRhs + kQR * 32 * kRow * 8;
   static constexpr int kBuf = (kOut + kQ * 32 * kRow * 8 + 127) / 128 * 128;
 };
 
@@ -257,17 +303,27 @@ struct SwfGeo {
 // ---------------------------------------------------------------------
 template <int NK, int KEYS, bool FWD>
 __device__ __forceinline__ void swf_compute(const SweepArgs &a, const SPhase &P, int g,
-                                            unsigned char *sm) {
+                                            int rank, unsigned char *sm) {
   constexpr int STEPB = swf_stepb(NK, FWD);
   const SwfGeo G(a, P, g);
-  const int j = G.j, lag = G.lag, nch = G.nch;
+  const int j = G.j, lag = G.lag, nch = G.nch, Lc = G.Lc;
+  // thread-block cluster hand-off (P.cl > 1): the previous group runs in
+  // the CTA of cluster rank - 1 and stores its last line into this CTA's
+  // ring (distributed shared memory), one mbarrier arrival per chunk; this
+  // CTA's lane 31 feeds rank + 1 the same way.  Rank 0's previous line
+  // comes from global memory (helper warp).
+  const bool dsm_in = P.cl > 1 && rank > 0 && G.has_prev;
+  uint64_t *up = reinterpret_cast<uint64_t *>(sm + SwfSmem::kUp);
+  const int cshift = (32 * lag + kT - 1) / kT;  // upstream chunk covering a chunk's needs
+  constexpr int HD = swf_depth<NK, KEYS>();
+  uint32_t r_prog = 0;
+  if (dsm_in) r_prog = s_mapa(sm + SwfSmem::kProg, (uint32_t)rank - 1);
   uint64_t *rec_bar = reinterpret_cast<uint64_t *>(sm + SwfSmem::kRec);
   uint64_t *ready = reinterpret_cast<uint64_t *>(sm + SwfSmem::kReady);
   uint64_t *done = reinterpret_cast<uint64_t *>(sm + SwfSmem::kDone);
   const double *ring = reinterpret_cast<const double *>(sm + SwfSmem::kRing);
   unsigned char *buf = sm + SwfSmem::kBuf;
   const uint32_t cb = (uint32_t)P.chunkb;
-  constexpr int H = swf_depth<NK, KEYS>();
   double o[4] = {0.0, 0.0, 0.0, 0.0}, q[4] = {0.0, 0.0, 0.0, 0.0};
   double lv[NK], dv = 1.0, dr = 1.0;
   auto load_step = [&](const unsigned char *rec, int t) {
@@ -290,19 +346,25 @@ __device__ __forceinline__ void swf_compute(const SweepArgs &a, const SPhase &P,
     const int sq = c % kQ;
     if (dbc && c < 512) dbp[c * 6] = clock64();
     s_mbar_wait(ready + sq, (uint32_t)((c / kQ) & 1));  // rhs(c) staged, ring(c) filled
+    if (dsm_in) {  // the upstream chunk whose results cover this chunk
+      const int cp = c + cshift < nch ? c + cshift : nch - 1;
+      s_mbar_wait_cl(up + (cp % kNU), (uint32_t)((cp / kNU) & 1));
+    }
     if (dbc && c < 512) dbp[c * 6 + 1] = clock64();
     if (c == 0) {
       // the window's previous-line entries before step 0 (pre-roll)
       double pre[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int d = H; d >= 1; --d) pre[(4 - d) & 3] = ring[(lag - d) & (kR - 1)];
+      for (int d = HD; d >= 1; --d)
+        pre[(4 - d) & 3] = (G.has_prev && lag - d >= 0) ? ring[(lag - d + 31 * lag) & (kR - 1)] : 0.0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) q[u] = j == 0 ? pre[u] : 0.0;
     }
-    s_mbar_wait(rec_bar + (c % kNB), (uint32_t)((c / kNB) & 1));
+    // (the records' TMA completion was observed by the helper before ready)
     if (dbc && c < 512) dbp[c * 6 + 2] = clock64();
     const unsigned char *rec = buf + (size_t)(c % kNB) * cb;
-    const double *rh = reinterpret_cast<const double *>(sm + SwfSmem::kRhs) + (sq * 32 + j) * kRow;
+    const double *rh =
+        reinterpret_cast<const double *>(sm + SwfSmem::kRhs) + ((c % kQR) * 32 + j) * kRow;
     double *ob = reinterpret_cast<double *>(sm + SwfSmem::kOut) + (sq * 32 + j) * kRow;
     const int pc0 = c * kT + lag;  // previous line's position of step 0 (lane 0's view)
     // One chunk of T steps.  EXACT = false: the backward division uses the
@@ -328,7 +390,8 @@ __device__ __forceinline__ void swf_compute(const SweepArgs &a, const SPhase &P,
           rr1 = v.y;
         }
         // lane 31 sends the previous line's value of this step to lane 0
-        const double av = ring[(pc0 + t) & (kR - 1)];
+        const double av =
+            (G.has_prev && (unsigned)(pc0 + t) < (unsigned)Lc) ? ring[(pc0 + t + 31 * lag) & (kR - 1)] : 0.0;
         double acc = (t & 1) ? rr1 : rr0;
 #pragma unroll
         for (int e = 0; e < NK; ++e) {
@@ -391,6 +454,8 @@ __device__ __forceinline__ void swf_compute(const SweepArgs &a, const SPhase &P,
       if (!isfinite(nfin)) atomicOr(a.err, 1);
     }
     if (dbc && c < 512) dbp[c * 6 + 3] = clock64();
+    if (dsm_in && j == 31) c_st_u32(r_prog, c);  // ring positions of chunk c consumed
+    if (dbc && c < 512) dbp[c * 6 + 4] = clock64();
     s_mbar_arrive_rel(done + sq);  // (count 32) outputs staged, buffers free
     if (dbc && c < 512) dbp[c * 6 + 5] = clock64();
   }
@@ -402,8 +467,18 @@ __device__ __forceinline__ void swf_compute(const SweepArgs &a, const SPhase &P,
 // ---------------------------------------------------------------------
 template <bool FWD>
 __device__ __forceinline__ void swf_helper(const SweepArgs &a, const SPhase &P, int g,
-                                           unsigned char *sm) {
+                                           int rank, unsigned char *sm) {
   const SwfGeo G(a, P, g);
+  // previous line from the upstream CTA of the cluster (no polling here);
+  // the group's last line sent to the downstream CTA of the cluster
+  const bool dsm_in = P.cl > 1 && rank > 0 && G.has_prev;
+  const bool dsm_out = P.cl > 1 && rank + 1 < P.cl && g + 1 < P.ngroups;
+  uint32_t r_ring = 0, r_up = 0;
+  if (dsm_out) {
+    r_ring = s_mapa(sm + SwfSmem::kRing, (uint32_t)rank + 1);
+    r_up = s_mapa(sm + SwfSmem::kUp, (uint32_t)rank + 1);
+  }
+  const int *prog = reinterpret_cast<const int *>(sm + SwfSmem::kProg);
   const int j = G.j, lag = G.lag, nch = G.nch, n = G.n, Lc = G.Lc;
   uint64_t *rec_bar = reinterpret_cast<uint64_t *>(sm + SwfSmem::kRec);
   uint64_t *ready = reinterpret_cast<uint64_t *>(sm + SwfSmem::kReady);
@@ -429,7 +504,7 @@ __device__ __forceinline__ void swf_helper(const SweepArgs &a, const SPhase &P, 
   // chunk c's right-hand sides into staging slot c % kQ in POSITION order
   auto rhs_issue = [&](int c) {
     if (c < nch) {
-      double *d0 = reinterpret_cast<double *>(sm + SwfSmem::kRhs) + ((c % kQ) * 32 + j) * kRow;
+      double *d0 = reinterpret_cast<double *>(sm + SwfSmem::kRhs) + ((c % kQR) * 32 + j) * kRow;
       const int p0 = c * kT - lag * j;
       if (FWD && r16 && full(c)) {
         const double *g0 = rin + rowp(c);
@@ -464,11 +539,11 @@ __device__ __forceinline__ void swf_helper(const SweepArgs &a, const SPhase &P, 
   auto ring_fill = [&](int c) {
     if (j < kT) {
       const int p = c * kT + lag + j;
-      ring[p & (kR - 1)] = prev_val(p);
+      ring[(p + 31 * lag) & (kR - 1)] = prev_val(p);
     }
     if (c == 0 && j >= kT && j < kT + HMAX) {
       const int p = lag - (j - kT) - 1;
-      ring[p & (kR - 1)] = prev_val(p);
+      ring[(p + 31 * lag) & (kR - 1)] = prev_val(p);
     }
   };
   // steady state: lanes 0..T-1 LOAD chunk c's positions one iteration
@@ -502,7 +577,7 @@ __device__ __forceinline__ void swf_helper(const SweepArgs &a, const SPhase &P, 
           v = prev_val(p);
         }
       }
-      ring[p & (kR - 1)] = v;
+      ring[(p + 31 * lag) & (kR - 1)] = v;
     }
   };
   // publish chunk c's results (output staging slot c % kQ) to global memory
@@ -541,45 +616,86 @@ __device__ __forceinline__ void swf_helper(const SweepArgs &a, const SPhase &P, 
     }
   }
 #pragma unroll
-  for (int c = 0; c < kQ - 1; ++c) rhs_issue(c);
-  ring_fill(0);
-  ring_fill(1);
-  prev_load(2);
-  asm volatile("cp.async.wait_group %0;" ::"n"(kQ - 2) : "memory");  // rhs(0) landed
+  for (int c = 0; c < kQR - 1; ++c) rhs_issue(c);
+  if (!dsm_in) {
+    ring_fill(0);
+    ring_fill(1);
+    prev_load(2);
+  }
+  asm volatile("cp.async.wait_group %0;" ::"n"(kQR - 2) : "memory");  // rhs(0) landed
+  s_mbar_wait(rec_bar, 0u);                                            // records(0)
   s_mbar_arrive_rel(ready + 0);
+  constexpr int HD = 4;  // pre-roll bound of the throttle (window depth <= 4)
   for (int c = 0; c < nch; ++c) {
-    // chunk c+1 ready (its right-hand sides and previous-line values)
+    // chunk c+1 ready: its right-hand sides, previous-line values, records
     if (c + 1 < nch) {
-      if (c + 1 >= 2) {
+      if (c + 1 >= 2 && !dsm_in) {
         prev_store(c + 1);
         prev_load(c + 2);
       }
-      asm volatile("cp.async.wait_group %0;" ::"n"(kQ - 3) : "memory");  // rhs(c+1)
+      asm volatile("cp.async.wait_group %0;" ::"n"(kQR - 3) : "memory");  // rhs(c+1)
+      s_mbar_wait(rec_bar + (c + 1) % kNB, (uint32_t)(((c + 1) / kNB) & 1));
+      // the output staging slot of chunk c+1 is the one chunk c+1-kQ sent
+      // to the downstream CTA: that bulk copy (issued kQ-1 iterations ago;
+      // the kQ-2 younger ones may still be in flight) must have read it
+      if (dsm_out && j == 31)
+        asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kQ - 2) : "memory");
       s_mbar_arrive_rel(ready + (c + 1) % kQ);
     }
-    // chunk c computed: publish it, refill its record buffer and its rhs slot
+    // chunk c computed
     s_mbar_wait(done + c % kQ, (uint32_t)((c / kQ) & 1));
+    if (dsm_out && j == 31) {
+      // the group's last line (output staging row 31) into the downstream
+      // CTA's ring slots rslot(p0) .. +T-1 = c*T mod kR .. (contiguous), one
+      // bulk copy completing the peer's mbarrier phase c, once the slots it
+      // overwrites have been consumed there
+      const int p0 = c * kT - lag * 31;
+      const int pmax = p0 + kT - 1;
+      for (;;) {
+        const int pr = s_ld_acq_i(prog);
+        const int consumed = pr < 0 ? lag - HD - 1 : pr * kT + kT - 1 + lag;
+        if (pmax <= consumed + kR) break;
+        __nanosleep(64);
+      }
+      const double *ob =
+          reinterpret_cast<const double *>(sm + SwfSmem::kOut) + ((c % kQ) * 32 + 31) * kRow;
+      const uint32_t bar = r_up + (uint32_t)((c % kNU) * 8);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      // relaxed: the data travels by the bulk copy, whose completion the
+      // phase waits for (a release here costs a GPU-scope MEMBAR)
+      asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"((uint32_t)(kT * 8))
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              r_ring + (uint32_t)(((c * kT) & (kR - 1)) * 8)),
+          "r"(s_u32(ob)), "r"((uint32_t)(kT * 8)), "r"(bar)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
     publish(c);
     if (j == 0 && c + kNB < nch) {
       const int b = c % kNB;
       s_mbar_arrive_tx(rec_bar + b, cb);
       s_bulk(buf + (size_t)b * cb, src + (size_t)(c + kNB) * cb, cb, rec_bar + b);
     }
-    rhs_issue(c + kQ - 1);  // slot (c - 1) % kQ: chunk c-1 is long done
+    rhs_issue(c + kQR - 1);  // slot (c - 1) % kQR: chunk c-1 is long done
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (dsm_out && j == 31) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <int NK, int KEYS, bool FWD>
 __global__ void __launch_bounds__(64, 1) swf_kernel(SweepArgs a, SPhase P) {
   __shared__ int s_tick;
   int *tick = a.tick;
+  const bool clustered = P.cl > 1;
   {  // stopped solve: skip, but count this CTA out (ticket reset)
     int d = 0;
     if (threadIdx.x == 0 && a.done) d = *(volatile const int *)a.done;
     d = __syncthreads_or(d);
     if (d) {
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0 && !clustered) {
         __threadfence();
         if (atomicAdd(&tick[1], 1) == (int)gridDim.x - 1) {
           atomicExch(&tick[0], 0);
@@ -591,9 +707,9 @@ __global__ void __launch_bounds__(64, 1) swf_kernel(SweepArgs a, SPhase P) {
   }
   extern __shared__ __align__(128) unsigned char sm[];
   const int w = threadIdx.x >> 5, j = threadIdx.x & 31;
-  for (;;) {
+  const int rank = clustered ? (int)cluster_rank() : 0;
+  auto init = [&]() {
     if (threadIdx.x == 0) {
-      s_tick = atomicAdd(tick, 1);
       // fresh barriers per group (no copy is pending here)
       uint64_t *rb = reinterpret_cast<uint64_t *>(sm + SwfSmem::kRec);
       for (int b = 0; b < kNB; ++b) s_mbar_init(rb + b, 1);
@@ -603,12 +719,14 @@ __global__ void __launch_bounds__(64, 1) swf_kernel(SweepArgs a, SPhase P) {
         s_mbar_init(ready + b, 32);
         s_mbar_init(done + b, 32);
       }
+      uint64_t *up = reinterpret_cast<uint64_t *>(sm + SwfSmem::kUp);
+      for (int b = 0; b < kNU; ++b) s_mbar_init(up + b, 1);
+      *reinterpret_cast<int *>(sm + SwfSmem::kProg) = -1;
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    __syncthreads();
-    const int g = s_tick;
-    if (g >= P.ngroups) break;
+  };
+  auto run = [&](int g) {
     if (swf_dbg_on && j == 0 && w == 0 && g < 4096) {
       unsigned wid, smid;
       asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
@@ -617,12 +735,31 @@ __global__ void __launch_bounds__(64, 1) swf_kernel(SweepArgs a, SPhase P) {
       if (g < 64) swf_dbgw[FWD ? 0 : 1][g] = (int)(smid * 1000 + wid);
     }
     if (w == 0)
-      swf_compute<NK, KEYS, FWD>(a, P, g, sm);
+      swf_compute<NK, KEYS, FWD>(a, P, g, rank, sm);
     else
-      swf_helper<FWD>(a, P, g, sm);
+      swf_helper<FWD>(a, P, g, rank, sm);
     __syncthreads();
     if (swf_dbg_on && j == 0 && w == 0 && g < 4096)
       swf_dbg[(FWD ? 0 : 2 * 4096) + 2 * g + 1] = gtimer();
+  };
+  if (clustered) {
+    // static mapping: group = CTA index (all clusters co-resident, checked
+    // at plan build); peers' shared memory is live between the two syncs
+    init();
+    __syncthreads();
+    cluster_sync();
+    const int g = blockIdx.x;
+    if (g < P.ngroups) run(g);
+    cluster_sync();
+    return;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) s_tick = atomicAdd(tick, 1);
+    init();
+    __syncthreads();
+    const int g = s_tick;
+    if (g >= P.ngroups) break;
+    run(g);
   }
   // last CTA out resets the ticket for the next launch / graph replay
   if (threadIdx.x == 0) {
@@ -832,9 +969,67 @@ static void launch_pat(const SweepArgs &a, const SPhase &P, int W, int grid, siz
   static size_t attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = smem;
   }
-  fn<<<grid, 64, smem, st>>>(a, P);
+  if (P.cl > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(64);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)P.cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, fn, a, P);
+  } else {
+    fn<<<grid, 64, smem, st>>>(a, P);
+  }
+}
+
+// thread-block clusters of `cl` CTAs that can be resident at once
+template <int PAT, bool FWD>
+static int max_clusters_pat(int cl, int grid, size_t smem) {
+  constexpr Pattern pt = kPat[PAT];
+  constexpr int KEYS =
+      pt.keys[0] | (pt.keys[1] << 3) | (pt.keys[2] << 6) | (pt.keys[3] << 9);
+  auto *fn = swf_kernel<pt.nk, KEYS, FWD>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(64);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int num = 0;
+  const cudaError_t e = cudaOccupancyMaxActiveClusters(&num, fn, &cfg);
+  if (getenv("MPK_VERBOSE"))
+    fprintf(stderr, "[mpk] swf cluster query cl=%d grid=%d smem=%zu: %s, %d clusters\n", cl,
+            grid, smem, cudaGetErrorString(e), num);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return num;
+}
+static int max_clusters(const SPhase &P, int cl, int grid, size_t smem) {
+  const bool f = P.fwd != 0;
+  switch (P.pat) {
+    case 0: return f ? max_clusters_pat<0, true>(cl, grid, smem) : max_clusters_pat<0, false>(cl, grid, smem);
+    case 1: return f ? max_clusters_pat<1, true>(cl, grid, smem) : max_clusters_pat<1, false>(cl, grid, smem);
+    case 2: return f ? max_clusters_pat<2, true>(cl, grid, smem) : max_clusters_pat<2, false>(cl, grid, smem);
+    default: return f ? max_clusters_pat<3, true>(cl, grid, smem) : max_clusters_pat<3, false>(cl, grid, smem);
+  }
 }
 
 static void launch_phase(const SweepArgs &a, const SPhase &P, int W, int grid, size_t smem,
@@ -901,6 +1096,23 @@ bool build_ssweep(SSweep &w, int n, bool cx, const int *rp, const int *ci, const
     free_ssweep(t);
     return false;
   }
+  // cluster hand-off between consecutive groups when every cluster of the
+  // grid can be resident at once (static group -> CTA mapping)
+  {
+    const char *ec = getenv("MPK_SWF_CL");
+    const int want = ec ? atoi(ec) : 16;
+    for (SPhase *Q : {&t.f, &t.b}) {
+      Q->cl = 1;
+      for (int cl = want; cl >= 2; cl /= 2) {
+        const int grid = (Q->ngroups + cl - 1) / cl * cl;
+        if (grid > 148) continue;
+        if (max_clusters(*Q, cl, grid, t.smem) >= grid / cl) {
+          Q->cl = cl;
+          break;
+        }
+      }
+    }
+  }
   t.cost = cf + cbk;
   t.on = 1;
   w = t;
@@ -926,7 +1138,10 @@ void launch_ssweep(const SweepArgs &a, const SSweep &w, cudaStream_t st) {
     SPhase Q = *P;
     if (only_g0) Q.ngroups = only_g0;  // diagnostics: timing of the first groups alone
     int grid = Q.ngroups;
-    if (grid > 148) grid = 148;
+    if (Q.cl > 1)
+      grid = (Q.ngroups + Q.cl - 1) / Q.cl * Q.cl;
+    else if (grid > 148)
+      grid = 148;
     launch_phase(a, Q, w.W, grid, w.smem, st);
   }
 }

@@ -84,6 +84,7 @@ struct SPhase {
   int rhs16 = 0;          // 16-byte right-hand-side copies possible
   int rpf = 0;            // L2 prefetch distance of the right-hand sides (chunks, 0: off)
   int pf = 0;             // L2 prefetch distance of the records (chunks, 0: off)
+  int cl = 1;             // thread-block cluster size (1: ticketed CTAs)
   unsigned char *rec = nullptr;
   int *esrc = nullptr;    // value slot ((g*S+s)*nk+e)*32+j -> lu index / -1
   int *dsrc = nullptr;    // divisor slot (g*S+s)*32+j -> lu index / -1
