@@ -166,7 +166,9 @@ int mpk_mc_elementwise(mpk_ctx *ctx, int op, int k, int64_t n,
                        const double *b_re, const double *b_im, double *o_re,
                        double *o_im);
 /* Host-side MC scalar arithmetic (MCFloat/MCComplex operators,
- * multicomponent.py:184-231): same op codes, one element, no GPU. */
+ * multicomponent.py:184-231): same op codes, one element, no GPU.  Host-only
+ * codes 13 two_sum(a0, b0) and 14 two_prod(a0, b0) write (s, e) to o_re[0..1]
+ * (the two_sum / two_prod exports, _mccore.py:19-51). */
 int mpk_mc_host(int op, int k, const double *a_re, const double *a_im,
                 const double *b_re, const double *b_im, double *o_re,
                 double *o_im);

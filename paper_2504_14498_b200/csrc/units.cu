@@ -247,6 +247,18 @@ int unit_mc(int op, int k, const double *a_re, const double *a_im,
 int host_mc(int op, int k, const double *a_re, const double *a_im,
             const double *b_re, const double *b_im, double *o_re,
             double *o_im) {
+  // host-only error-free transformations (two_sum / two_prod exports,
+  // _mccore.py:19-51): o = (s, e)
+  if (op == 13 || op == 14) {
+    double s, e;
+    if (op == 13)
+      two_sum(a_re[0], b_re[0], s, e);
+    else
+      two_prod(a_re[0], b_re[0], s, e);
+    o_re[0] = s;
+    o_re[1] = e;
+    return 0;
+  }
   switch (k) {
     case 1: {
       // k = 1 degenerates to native binary64 (multicomponent.py:31-66)
@@ -268,6 +280,19 @@ int host_mc(int op, int k, const double *a_re, const double *a_im,
           sqrt_mc<1>(x, q);
           o = q[0];
           break;
+        }
+        case 5:
+        case 6: {  // complex mul / Smith division in plain binary64
+          const double ar[1] = {a_re[0]}, ai[1] = {a_im ? a_im[0] : 0.0};
+          const double br[1] = {b_re[0]}, bi[1] = {b_im ? b_im[0] : 0.0};
+          double orr[1], oi[1];
+          if (op == 5)
+            cmul<1>(ar, ai, br, bi, orr, oi);
+          else
+            cdiv<1>(ar, ai, br, bi, orr, oi);
+          o_re[0] = orr[0];
+          if (o_im) o_im[0] = oi[0];
+          return 0;
         }
         default: return 3;
       }

@@ -22,7 +22,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .multicomponent import Precision, _mc_add
+from .multicomponent import Precision, add_limbs
 from .sparse import CsrMatrix
 
 __all__ = ["MatrixMarketError", "CooMatrix", "parse_matrix_market",
@@ -179,8 +179,8 @@ def coo_to_csr(coo: CooMatrix, precision: Precision) -> CsrMatrix:
             if k == 1:
                 sr, si = (sr[0] + vr[q],), (si[0] + vi[q],)
             else:
-                sr = _mc_add(sr, (float(vr[q]),) + pad)
-                si = _mc_add(si, (float(vi[q]),) + pad)
+                sr = add_limbs(sr, (float(vr[q]),) + pad)
+                si = add_limbs(si, (float(vi[q]),) + pad)
         out_re[t], out_im[t] = sr, si
     row_ptr = np.zeros(n + 1, np.int64)
     np.add.at(row_ptr, r[first] + 1, 1)

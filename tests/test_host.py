@@ -26,6 +26,47 @@ def test_library_exports_every_header_symbol():
         assert hasattr(L, name), name
 
 
+def test_error_free_transformations_match_reference():
+    """two_sum / two_prod exports over the whole exponent range, incl. the
+    overflowing and underflowing cases (mc_scalar.npz, reference _mccore.py:19-51)."""
+    import paper_2504_14498_b200 as mpk
+
+    g = golden("mc_scalar.npz")
+    ts = np.array([mpk.two_sum(a, b) for a, b in g["eft_in"]])
+    tp = np.array([mpk.two_prod(a, b) for a, b in g["eft_in"]])
+    assert np.array_equal(ts, g["two_sum"], equal_nan=True)
+    assert np.array_equal(tp, g["two_prod"], equal_nan=True)
+    finite = np.isfinite(g["two_prod"]).all(axis=1)
+    assert bits_equal(tp[finite], g["two_prod"][finite])
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_mc_scalar_strings_and_complex_match_reference(k):
+    """MCFloat.to_string (exact and 7 digits), from_string, and complex
+    mul / div / sqrt, against the reference's outputs (mc_scalar.npz)."""
+    import paper_2504_14498_b200 as mpk
+
+    g = golden("mc_scalar.npz")
+    P = mpk.Precision.from_k(k)
+    vals = [mpk.MCFloat(tuple(v)) for v in g[f"k{k}_vals"]]
+    assert [v.to_string() for v in vals] == list(g[f"k{k}_str"])
+    assert [v.to_string(7) for v in vals] == list(g[f"k{k}_str7"])
+    for v, s in zip(vals, g[f"k{k}_str"]):  # exact strings round-trip bitwise
+        assert bits_equal(mpk.MCFloat.from_string(str(s), P).components, v.components)
+    parsed = [mpk.MCFloat.from_string(str(t), P).components for t in g[f"k{k}_parse_in"]]
+    assert bits_equal(np.array(parsed), g[f"k{k}_parse"])
+    zs = [mpk.MCComplex(vals[i], vals[i + 1]) for i in range(0, 58, 2)]
+    for name, res in (("cmul", [zs[i] * zs[i + 1] for i in range(len(zs) - 1)]),
+                      ("cdiv", [zs[i] / zs[i + 1] for i in range(len(zs) - 1)]),
+                      ("csqrt", [z.sqrt() for z in zs])):
+        got = np.array([(z.re.components, z.im.components) for z in res])
+        assert bits_equal(got, g[f"k{k}_{name}"]), name
+    with pytest.raises(ValueError):
+        mpk.MCFloat.from_string("not a number", P)
+    with pytest.raises(ValueError):
+        (-abs(vals[0]) - 1.0).sqrt()
+
+
 def test_library_is_sm100a():
     so = ROOT / "paper_2504_14498_b200" / "_lib" / "libmpkb200.so"
     import subprocess
