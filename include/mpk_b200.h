@@ -100,6 +100,19 @@ void *mpk_ctx_stream(mpk_ctx *ctx);
  * real and complex */
 #define MPK_PRECOND_ILU0_FULL 2
 int mpk_ctx_set_option(mpk_ctx *ctx, int option, int64_t value);
+/* Per-call form of MPK_OPT_PRECOND (SolverConfig.precond is an argument of
+ * every solve() in the reference, solvers.py:418-425): the calling thread's
+ * next solves use `value` instead of the context's setting; value < 0
+ * clears the override.  Thread-local, so concurrent solves on one context
+ * never see each other's preconditioner. */
+int mpk_thread_set_option(int option, int64_t value);
+/* MPK_OPT_SPMV (per-thread only): SolverConfig.spmv_mode (solvers.py:64-85,
+ * _Ctx.matvec :126-134).  MPK_SPMV_FULL makes the solvers multiply with the
+ * matrix's working-precision values when mpk_csr_set_mc_values attached
+ * them; for binary64-valued matrices both modes are the same computation. */
+#define MPK_OPT_SPMV 3
+#define MPK_SPMV_MIXED 0
+#define MPK_SPMV_FULL 1
 
 /* CsrMatrix.demoted() upload (sparse.py:192-249): binary64 values, val_im
  * NULL for the real field.  Columns must be strictly increasing per row. */
@@ -112,6 +125,14 @@ void mpk_csr_free(mpk_matrix *m);
  * analysis -- level sets, sweep matrices, solver plans -- is kept). */
 int mpk_csr_set_values(mpk_matrix *m, const double *val_re,
                        const double *val_im);
+/* CsrMatrix values at working precision (sparse.py:192-249: val_re / val_im
+ * of shape (nnz, k), row-major).  Attaches all k components of every entry
+ * for spmv_mode "full" (mpk_spmv_full, MPK_OPT_SPMV) and for the
+ * working-precision ILU(0) of an MC-valued matrix (ilu.py:279-281); k = 0
+ * detaches them.  The binary64 values of mpk_csr_upload stay the demoted
+ * matrix (CsrMatrix.demoted, sparse.py:251-258) that ILU(0)-mixed factors. */
+int mpk_csr_set_mc_values(mpk_matrix *m, int k, const double *val_re,
+                          const double *val_im);
 
 /* ilu0_factorize_demoted (ilu.py:284-286 -> _factorize_tuples :178-276).
  * Returns MPK_SINGULAR_PIVOT with *bad_row / *structural, or
@@ -141,6 +162,13 @@ int mpk_ilu0_apply_mixed(mpk_matrix *m, int k, const double *r_re,
 int mpk_spmv_mixed(mpk_matrix *m, int k, const double *x_re,
                    const double *x_im, double *y_re, double *y_im,
                    int adjoint);
+
+/* spmv / spmv_adjoint (sparse.py:414-451 -> _kernels.py:224-240, 266-278,
+ * 300-323, 356-376): the matrix at working precision (MC x MC products).
+ * Without attached MC values the matrix is binary64-valued and the mixed
+ * kernels compute the same result bit for bit. */
+int mpk_spmv_full(mpk_matrix *m, int k, const double *x_re, const double *x_im,
+                  double *y_re, double *y_im, int adjoint);
 
 /* hdot (sparse.py:509-517): out_re/out_im k doubles.  norm2 (:532-539).
  * Device reduction order is a fixed tree. */

@@ -47,7 +47,8 @@ EXPORTS = (
     "mpk_spmv_mixed", "mpk_hdot", "mpk_norm2", "mpk_axpy", "mpk_mc_elementwise",
     "mpk_mc_host", "mpk_solve", "mpk_plane_ld", "mpk_solve_dev", "mpk_to_planar",
     "mpk_from_planar", "mpk_solve_batch", "mpk_ctx_stream", "mpk_bench_apply", "mpk_bench_spmv", "mpk_sweep_info",
-    "mpk_csr_set_values", "mpk_run_jobs", "mpk_ctx_set_option",
+    "mpk_csr_set_values", "mpk_csr_set_mc_values", "mpk_spmv_full", "mpk_run_jobs",
+    "mpk_ctx_set_option", "mpk_thread_set_option",
     "mpk_comm_unique_id", "mpk_comm_create", "mpk_comm_create_local", "mpk_comm_destroy",
     "mpk_comm_rank", "mpk_comm_world", "mpk_solve_dev_sharded",
     "mpk_ilu0_factor_full", "mpk_ilu0_download_full", "mpk_ilu0_apply_full",
@@ -57,35 +58,34 @@ EXPORTS = (
 MPK_OPT_REDUCTION = 1
 REDUCTION_MODE = {"tree": 0, "sequential": 1}
 MPK_OPT_PRECOND = 2  # 0: none (M = I), 1: ILU(0)-mixed (default)
-_precond_lock = threading.Lock()
+MPK_OPT_SPMV = 3  # per-thread: 0 mixed, 1 full (the matrix's attached MC values)
 
 
 class precond_scope:
-    """Selects the solvers' preconditioner on a context for one call
+    """Selects the preconditioner of the calling thread's solves for one call
     (MPK_OPT_PRECOND: 0 none, 1 ILU(0)-mixed, 2 working-precision ILU(0))
-    and restores ILU(0)-mixed afterwards; calls on the same context are
-    serialised while a non-default preconditioner is set."""
+    through the library's thread-local override, so concurrent solves on one
+    context never see each other's setting; cleared on exit."""
 
-    def __init__(self, ctx, ilu):
+    def __init__(self, ctx, ilu, spmv_full: bool = False):
         # ilu: True -> 1 (default), False -> 0, or the option value itself
         self.ctx = ctx
-        self.value = int(ilu) if isinstance(ilu, bool) else int(ilu)
-        self.ilu = self.value == 1
+        self.value = int(ilu)
+        self.spmv_full = bool(spmv_full)
 
     def __enter__(self):
-        if not self.ilu:
-            _precond_lock.acquire()
-            check(lib().mpk_ctx_set_option(self.ctx, ctypes.c_int(MPK_OPT_PRECOND),
-                                           ctypes.c_int64(self.value)), "mpk_ctx_set_option")
+        check(lib().mpk_thread_set_option(ctypes.c_int(MPK_OPT_PRECOND),
+                                          ctypes.c_int64(self.value)),
+              "mpk_thread_set_option")
+        if self.spmv_full:
+            check(lib().mpk_thread_set_option(ctypes.c_int(MPK_OPT_SPMV), ctypes.c_int64(1)),
+                  "mpk_thread_set_option")
         return self
 
     def __exit__(self, *exc):
-        if not self.ilu:
-            try:
-                lib().mpk_ctx_set_option(self.ctx, ctypes.c_int(MPK_OPT_PRECOND),
-                                         ctypes.c_int64(1))
-            finally:
-                _precond_lock.release()
+        lib().mpk_thread_set_option(ctypes.c_int(MPK_OPT_PRECOND), ctypes.c_int64(-1))
+        lib().mpk_thread_set_option(ctypes.c_int(MPK_OPT_SPMV), ctypes.c_int64(0))
+        return False
 
 
 class MpkReport(ctypes.Structure):
@@ -181,6 +181,22 @@ def context(device: int = 0):
                 c = p
                 _ctx[device] = c
     return c
+
+
+_ctx_locks: dict = {}
+
+
+def ctx_lock(ctx) -> "threading.RLock":
+    """One lock per device context: a context is one CUDA stream plus cached
+    solver plans (captured graphs), so calls on it from several host threads
+    take turns.  Contexts are independent of each other (mpk_run_jobs runs
+    one native thread per context concurrently)."""
+    key = ctx.value if hasattr(ctx, "value") else int(ctx)
+    lk = _ctx_locks.get(key)
+    if lk is None:
+        with _lock:
+            lk = _ctx_locks.setdefault(key, threading.RLock())
+    return lk
 
 
 def dptr(a):

@@ -862,6 +862,23 @@ int mpk_ctx_set_option(mpk_ctx *ctx, int option, int64_t value) {
   }
 }
 
+static thread_local int tl_precond = -1;   // mpk_thread_set_option overrides
+static thread_local int tl_spmv_full = 0;
+
+int mpk_thread_set_option(int option, int64_t value) {
+  if (option == MPK_OPT_SPMV) {
+    if (value > MPK_SPMV_FULL) return fail(MPK_INVALID, "spmv mode must be 0 (mixed) or 1 (full)");
+    tl_spmv_full = value == MPK_SPMV_FULL ? 1 : 0;
+    return MPK_OK;
+  }
+  if (option != MPK_OPT_PRECOND)
+    return fail(MPK_INVALID, "per-thread options: MPK_OPT_PRECOND, MPK_OPT_SPMV");
+  if (value > MPK_PRECOND_ILU0_FULL)
+    return fail(MPK_INVALID, "precond must be 0 (none), 1 (ilu0-mixed) or 2 (ilu0)");
+  tl_precond = value < 0 ? -1 : (int)value;
+  return MPK_OK;
+}
+
 int64_t mpk_plane_ld(int64_t n) { return plane_ld(n); }
 
 int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
@@ -869,6 +886,7 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
                    const double *val_re, const double *val_im,
                    mpk_matrix **out) {
   // CsrMatrix._validate sparse.py:217-233
+  const double t_up0 = host_ms();
   if (n < 0 || nnz < 0) return fail(MPK_INVALID, "negative size");
   if (n > INT_MAX - 1 || nnz > INT_MAX)
     return fail(MPK_INVALID, "matrix too large for int32 indices");
@@ -902,6 +920,7 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
     for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
       if (col_idx[p] == i) A.h_dp[i] = (int)p;
   cudaStream_t st = ctx->stream;
+  const double t_up1 = host_ms();
   // level orders of the L (forward) and U (backward) DAGs; a missing
   // diagonal (dp = -1) only matters for the structural check at factor time
   std::vector<int> of, ob, pf, pb;
@@ -915,6 +934,7 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
         [&](int i) { return dp[i] < 0 ? rp[i + 1] : dp[i] + 1; },
         [&](int i) { return rp[i + 1]; }, ob, pb);
   }
+  const double t_up2 = host_ms();
   if (upload(&A.rp, A.h_rp, st) || upload(&A.ci, A.h_ci, st) ||
       upload(&A.dp, A.h_dp, st) || upload(&A.ord_f, of, st) ||
       upload(&A.ord_b, ob, st) || upload(&A.lev_f, pf, st) ||
@@ -964,9 +984,48 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
   CKR(cudaMalloc(&m->rowflag, sizeof(int) * (n + 1)));
   CKR(cudaMalloc(&m->fscratch, sizeof(int) * 4));
   CKR(cudaStreamSynchronize(st));
+  // shuffle-wavefront plan (swf.cu) for stencil-structured real sweeps.
+  // On a large pattern (the vector does not fit one SM's shared memory, so
+  // the alternative is the sync-free ticket sweep at >= 10 us per DAG level)
+  // the plan is kept as soon as its analysis succeeds: timing the
+  // alternatives would cost more than the solves the plan serves (cfg4:
+  // 8 x 64 ms ticket applies).  Small patterns are timed against the plan
+  // chosen above (MPK_SWEEP_PICK=swf forces it).
+  const double t_plan0 = host_ms();
+  if (getenv("MPK_VERBOSE"))
+    fprintf(stderr,
+            "[mpk] upload n=%lld: validate+copy %.1f ms, level orders %.1f ms, uploads + "
+            "SMEM plans %.1f ms\n",
+            (long long)n, t_up1 - t_up0, t_up2 - t_up1, t_plan0 - t_up2);
+  bool swf_kept_untimed = false;
+  {
+    SSweep ss;
+    if (build_ssweep(ss, (int)n, A.cx, A.h_rp.data(), A.h_ci.data(), A.h_dp.data(), st)) {
+      const char *pick = getenv("MPK_SWEEP_PICK");
+      const bool force = pick && !strcmp(pick, "swf");
+      const bool other = pick && !force;
+      const bool large = n >= (1 << 18) && !getenv("MPK_SWEEP_TIME_ALL");
+      float tb = 1e30f, ts = 0.f;
+      if (!force && !other && !large) tb = time_apply_plan(A, st);
+      gather_ssweep(A.val, ss, st);  // timing values (regathered after factorization)
+      A.smat.ss = ss;
+      if (!force && !other && !large) ts = time_apply_plan(A, st);
+      if (other || !(ts < tb)) free_ssweep(A.smat.ss);
+      swf_kept_untimed = A.smat.ss.on && large;
+      if (getenv("MPK_VERBOSE"))
+        fprintf(stderr,
+                "[mpk] shuffle-wavefront plan n=%lld: fwd Lc=%d lag=%d groups=%d S=%d pat=%d, "
+                "bwd Lc=%d lag=%d groups=%d S=%d pat=%d, cluster=%d smem=%zu; apply %.4f ms vs "
+                "%.4f ms (other plan) -> %s%s\n",
+                (long long)n, ss.f.Lc, ss.f.lag, ss.f.ngroups, ss.f.S, ss.f.pat, ss.b.Lc,
+                ss.b.lag, ss.b.ngroups, ss.b.S, ss.b.pat, ss.f.cl, ss.smem, ts, tb,
+                A.smat.ss.on ? "shuffle-wavefront" : "other", large ? " (untimed: large n)" : "");
+    }
+    CKR(cudaGetLastError());
+  }
   // lane-chunk wavefront plan (wf.cu) for banded sweep DAGs: kept when it
   // beats the plan chosen above on this device (MPK_SWEEP_PICK=wf forces it)
-  {
+  if (!swf_kept_untimed && !A.smat.ss.on) {
     WSweep wf;
     if (build_wsweep(wf, (int)n, A.cx, A.h_rp.data(), A.h_ci.data(),
                      A.h_dp.data(), A.levels_f, A.levels_b, st)) {
@@ -989,31 +1048,9 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
     }
     CKR(cudaGetLastError());
   }
-  // shuffle-wavefront plan (swf.cu) for stencil-structured real sweeps:
-  // kept when it beats the plan chosen above (MPK_SWEEP_PICK=swf forces it)
-  {
-    SSweep ss;
-    if (build_ssweep(ss, (int)n, A.cx, A.h_rp.data(), A.h_ci.data(), A.h_dp.data(), st)) {
-      const char *pick = getenv("MPK_SWEEP_PICK");
-      const bool force = pick && !strcmp(pick, "swf");
-      const bool other = pick && !force;
-      float tb = 1e30f, ts = 0.f;
-      if (!force && !other) tb = time_apply_plan(A, st);
-      gather_ssweep(A.val, ss, st);  // timing values (regathered after factorization)
-      A.smat.ss = ss;
-      if (!force && !other) ts = time_apply_plan(A, st);
-      if (other || !(ts < tb)) free_ssweep(A.smat.ss);
-      if (getenv("MPK_VERBOSE"))
-        fprintf(stderr,
-                "[mpk] shuffle-wavefront plan n=%lld: fwd Lc=%d lag=%d groups=%d S=%d pat=%d, "
-                "bwd Lc=%d lag=%d groups=%d S=%d pat=%d, cluster=%d smem=%zu; apply %.4f ms vs "
-                "%.4f ms (other plan) -> %s\n",
-                (long long)n, ss.f.Lc, ss.f.lag, ss.f.ngroups, ss.f.S, ss.f.pat, ss.b.Lc,
-                ss.b.lag, ss.b.ngroups, ss.b.S, ss.b.pat, ss.f.cl, ss.smem, ts, tb,
-                A.smat.ss.on ? "shuffle-wavefront" : "other");
-    }
-    CKR(cudaGetLastError());
-  }
+  if (getenv("MPK_VERBOSE"))
+    fprintf(stderr, "[mpk] upload n=%lld: sweep plans %.1f ms\n", (long long)n,
+            host_ms() - t_plan0);
   *out = m;
   return MPK_OK;
 }
@@ -1039,6 +1076,7 @@ void mpk_csr_free(mpk_matrix *m) {
   free_sweeps(A.smat);
   free_sweeps(A.smat_adj);
   if (A.lu_mc) cudaFree(A.lu_mc);
+  if (A.mcv) cudaFree(A.mcv);
   if (A.rcp_mc) cudaFree(A.rcp_mc);
   if (A.sw_mc) cudaFree(A.sw_mc);
   if (A.sw_mc2) cudaFree(A.sw_mc2);
@@ -1135,6 +1173,13 @@ __global__ void promote_vals_kernel(long long nnz, int k, int cx, const double *
     }
 }
 
+// planar MC matrix values (DMat::mcv) -> flat K-component entries
+__global__ void mc_vals_kernel(long long nnz, int w, const double *v, long long vld, double *o) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < nnz;
+       p += (long long)gridDim.x * blockDim.x)
+    for (int c = 0; c < w; ++c) o[p * w + c] = v[c * vld + p];
+}
+
 // ilu0_factorize (ilu.py:279-281 -> _factorize_tuples at precision k > 1) of
 // the uploaded binary64 matrix promoted to k components; real field.
 int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *structural) {
@@ -1167,7 +1212,10 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
   A.mc_factored = false;
   if (A.nnz > 0) {
     ++tl_launches;
-    promote_vals_kernel<<<148 * 4, 256, 0, st>>>(A.nnz, k, A.cx ? 1 : 0, A.val, A.lu_mc);
+    if (A.mcv && A.mcv_k == k)  // MC-valued matrix: ilu0_factorize(A) factors A itself
+      mc_vals_kernel<<<148 * 4, 256, 0, st>>>(A.nnz, W, A.mcv, A.mcv_ld, A.lu_mc);
+    else
+      promote_vals_kernel<<<148 * 4, 256, 0, st>>>(A.nnz, k, A.cx ? 1 : 0, A.val, A.lu_mc);
   }
   CKR(cudaMemsetAsync(m->rowflag, 0, sizeof(int) * (A.n + 1), st));
   if (!m->hres) CKR(cudaMallocHost(&m->hres, sizeof(int) * 8));
@@ -1194,6 +1242,7 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
   cudaEventCreate(&e1);
   cudaEventRecord(e0, st);
   if (A.n > 0) launch_factor_mc(fa, k, st);
+  CKR(cudaGetLastError());
   cudaEventRecord(e1, st);
   int *res = m->hres + 4;
   CKR(cudaMemcpyAsync(res, m->fscratch, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
@@ -1209,6 +1258,7 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
   }
   if (res[3]) return fail(MPK_NUMERIC_BREAKDOWN, "non-finite value in ILU(0) factors");
   launch_recip_mc(A.n, A.dp, A.lu_mc, A.rcp_mc, k, A.cx, st);
+  CKR(cudaGetLastError());
   A.mc_factored = true;
   return MPK_OK;
 }
@@ -1741,7 +1791,7 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   int64_t bad = -1;
   int32_t structural = 0;
   tl_phase[0] = host_ms();
-  const int pre = m->ctx->precond;
+  const int pre = tl_precond >= 0 ? tl_precond : m->ctx->precond;
   const bool ilu = pre != MPK_PRECOND_NONE;
   if (pre != MPK_PRECOND_ILU0_MIXED && ex)
     return fail(MPK_INVALID, "sharded solve: ILU(0)-mixed only");
@@ -1774,6 +1824,10 @@ static int solve_core(mpk_matrix *m, int method, int k, double eps_rel,
   p.hist_cap = hist_cap;
   p.reduce_seq = m->ctx->reduce_seq;
   p.ex = ex;
+  p.full_a = (tl_spmv_full && m->A.mcv) ? 1 : 0;
+  if (p.full_a && m->A.mcv_k != k)
+    return fail(MPK_INVALID, "matrix and vector precision must match for spmv");
+  if (p.full_a && ex) return fail(MPK_INVALID, "sharded solve: binary64-valued matrices only");
   SolveOut o{};
   char eb[256] = {0};
   rc = run_solve(m->A, p, d_b, d_x, d_hist, &o, m->ctx->stream, eb);
@@ -1954,6 +2008,62 @@ int mpk_csr_set_values(mpk_matrix *m, const double *val_re,
   A.adj_ready = false;
   CKR(cudaStreamSynchronize(st));
   return MPK_OK;
+}
+
+// CsrMatrix values at working precision (sparse.py:192-249 val_re / val_im,
+// shape (nnz, k) row-major): attaches all k components of every entry for
+// spmv_mode 'full' (mpk_spmv_full, MPK_OPT_SPMV) and for the
+// working-precision ILU(0); k = 0 detaches them.  The binary64 heads
+// uploaded by mpk_csr_upload / mpk_csr_set_values stay the demoted matrix.
+int mpk_csr_set_mc_values(mpk_matrix *m, int k, const double *val_re,
+                          const double *val_im) {
+  DMat &A = m->A;
+  CKR(cudaSetDevice(m->ctx->device));
+  if (A.mcv) {
+    CKR(cudaStreamSynchronize(m->ctx->stream));
+    cudaFree(A.mcv);
+    A.mcv = nullptr;
+    A.mcv_k = 0;
+    A.mc_factored = false;
+  }
+  if (k == 0) return MPK_OK;
+  if (k < 2 || k > 4) return fail(MPK_INVALID, "MC matrix values: k = 2..4");
+  if (!val_re || A.cx != (val_im != nullptr))
+    return fail(MPK_INVALID, "field mismatch: matrix/values");
+  int rc = to_dev_planar(m->ctx, A.nnz, k, val_re, val_im, &A.mcv);
+  if (rc) return rc;
+  A.mcv_k = k;
+  A.mcv_ld = plane_ld(A.nnz);
+  return MPK_OK;
+}
+
+// spmv / spmv_adjoint (sparse.py:414-451): y = A x or A^H x with the matrix
+// at working precision; binary64-valued matrices (no MC values attached)
+// take the mixed kernels, which compute the same thing bit for bit
+int mpk_spmv_full(mpk_matrix *m, int k, const double *x_re, const double *x_im,
+                  double *y_re, double *y_im, int adjoint) {
+  DMat &A = m->A;
+  if (!A.mcv) return mpk_spmv_mixed(m, k, x_re, x_im, y_re, y_im, adjoint);
+  if (A.mcv_k != k)
+    return fail(MPK_INVALID, "matrix and vector precision must match for spmv");
+  if (A.cx != (x_im != nullptr))
+    return fail(MPK_INVALID, std::string("field mismatch: matrix ") +
+                                 (A.cx ? "complex" : "real") + ", vector " +
+                                 (x_im ? "complex" : "real"));
+  CKR(cudaSetDevice(m->ctx->device));
+  cudaStream_t st = m->ctx->stream;
+  double *dx = nullptr, *dy = nullptr;
+  int rc = to_dev_planar(m->ctx, A.n, k, x_re, x_im, &dx);
+  if (rc) return rc;
+  const long long L = plane_ld(A.n);
+  CKR(cudaMalloc(&dy, sizeof(double) * k * 2 * L + 16));
+  rc = unit_spmv_full(A, k, adjoint != 0, false, dx, dy, nullptr, st);
+  if (rc) return fail(MPK_INVALID, "unsupported k");
+  CKR(cudaGetLastError());
+  rc = from_dev_planar(m->ctx, A.n, k, dy, y_re, A.cx ? y_im : nullptr);
+  cudaFree(dx);
+  cudaFree(dy);
+  return rc;
 }
 
 int mpk_solve_batch(int nsys, mpk_matrix **ms, int method, int k,

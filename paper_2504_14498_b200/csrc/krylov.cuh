@@ -54,6 +54,13 @@ struct DMat {
   int *rp = nullptr, *ci = nullptr, *dp = nullptr;
   double *val = nullptr;  // real [nnz] or double2 [nnz]
   double *lu = nullptr;   // factors, same layout
+  // MC-valued matrix (spmv_mode 'full', sparse.py:414-451): all K
+  // components of every entry, planar (component c of entry p at
+  // mcv[c * mcv_ld + p]; complex: K imaginary planes after the real ones);
+  // null for binary64-valued matrices, whose full SpMV is the mixed one
+  double *mcv = nullptr;
+  int mcv_k = 0;
+  long long mcv_ld = 0;
   bool factored = false;
   // A^T gather (ascending source row) for spmv_adjoint
   int *at_rp = nullptr, *at_ci = nullptr, *at_perm = nullptr;
@@ -115,6 +122,7 @@ struct SolveParams {
   int precond_ilu;  // 1: ILU(0)-mixed, 0: identity, 2: working-precision ILU(0)
   long long hist_cap;
   int reduce_seq;   // 1: sequential-order (bit-identical twin) reductions
+  int full_a = 0;   // 1: SpMV on the matrix's MC values (DMat::mcv)
   Exchange *ex = nullptr;  // row-block sharded solve (shard.cuh), else null
 };
 
@@ -136,6 +144,8 @@ int run_solve(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
 // unit kernels used by the C-ABI (parity tests)
 int unit_spmv(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
               double *d_y, cudaStream_t st);
+int unit_spmv_full(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
+                   double *d_y, const int *done, cudaStream_t st);
 int unit_reduce(int k, bool cx, int op, long long n, const double *d_x,
                 const double *d_y, double *h_out, cudaStream_t st, int seq);
 int unit_axpy(int k, bool cx, long long n, const double *alpha_re,

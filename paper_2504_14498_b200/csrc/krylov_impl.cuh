@@ -185,6 +185,8 @@ struct Solver : PlanBase {
   cudaEvent_t evf = nullptr, evj = nullptr, evj3 = nullptr;
   double *part2 = nullptr;
   double *seqbuf = nullptr;  // twin-mode element terms [slot][i][2K]
+  // MC-valued matrix (p.full_a): A x / A^H x of the next row kernel
+  double *prebuf = nullptr, *prebuf_adj = nullptr;
   State *hp = nullptr;  // pinned host staging of the device State (x2)
   int *hpi = nullptr;
 
@@ -228,6 +230,10 @@ struct Solver : PlanBase {
     if (p.reduce_seq)
       seqbuf = (double *)dalloc(sizeof(double) * 8 * 2 * K * (size_t)(n > 0 ? n : 1));
     da = DA{A.n, A.rp, A.ci, A.val, A.at_rp, A.at_ci, A.at_val};
+    if (p.full_a) {
+      da.pre = prebuf = mc();
+      if (p.method == kBiCG) da.pre_adj = prebuf_adj = mc();
+    }
     S = (State *)dalloc(sizeof(State));
     part = (double *)dalloc(sizeof(double) * 6 * kMaxGrid * 8);
     hist_cap = p.hist_cap > 0 ? p.hist_cap : 1;
@@ -266,6 +272,14 @@ struct Solver : PlanBase {
     if (hp) cudaFreeHost(hp);
     if (hpi) cudaFreeHost(hpi);
     for (void *q : allocs) cudaFree(q);
+  }
+  // MC-valued matrix: the SpMV the next row kernel consumes (sparse.py:
+  // 414-451), x an F vector (xf) or a full MC vector
+  void pre_spmv(const double *x_, bool xf, bool adjoint = false,
+                bool after_loop = false) {
+    if (!p.full_a) return;
+    unit_spmv_full(A, K, adjoint, xf, x_, adjoint ? prebuf_adj : prebuf,
+                   after_loop ? nullptr : done, st);
   }
   void zero_mc(double *q) {
     cudaMemsetAsync(q, 0, sizeof(double) * K * (CX ? 2 : 1) * ld, st);
@@ -406,6 +420,7 @@ struct Solver : PlanBase {
     const long long L = ld;
     const int np_ = nopre;
     const bool two = r2_ != nullptr;
+    pre_spmv(fzero, !nopre);
     rows<K, CX, 1, 1>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 1> &red) {
                         double axr[K], axi[K], br[K], bi[K], rr[K], ri[K];
@@ -517,6 +532,7 @@ struct Solver : PlanBase {
     sweep(head_re(pp), head_im(pp), A.sw_y, phat, false, 0);
     // K4: v = A phat ; sigma = hdot(rt0, v)
     const double *phc = phat;
+    pre_spmv(phat, !nopre);
     rows<K, CX, 1, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
                         double vr[K], vi[K], rr[K], ri[K];
@@ -565,6 +581,7 @@ struct Solver : PlanBase {
     sweep(head_re(s), head_im(s), A.sw_y, shat, false, 0);
     // K7: t = A shat ; tt = hdot(t,t), ts = hdot(t,s)
     const double *shc = shat;
+    pre_spmv(shat, !nopre);
     rows<K, CX, 2, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 2, 0> &red) {
                         double tr[K], ti[K], sr[K], si[K];
@@ -689,6 +706,7 @@ struct Solver : PlanBase {
                       });
     sweep(head_re(pp), head_im(pp), A.sw_y, phat, false, 0);
     const double *phc = phat;
+    pre_spmv(phat, !nopre);
     rows<K, CX, 1, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
                         double vr[K], vi[K], rr[K], ri[K];
@@ -735,6 +753,7 @@ struct Solver : PlanBase {
     sweep(whead, CX ? whead + ld : nullptr, A.sw_y, uhat, false, 0);
     // qhat = A uhat ; x += alpha uhat ; r -= alpha qhat ; norm2(r), rho
     const double *uhc = uhat;
+    pre_spmv(uhat, !nopre);
     rows<K, CX, 1, 1>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 1> &red) {
                         double qr[K], qi[K], xr[K], xi[K], fr[K], fi[K],
@@ -816,6 +835,7 @@ struct Solver : PlanBase {
                       });
     sweep(head_re(pp), head_im(pp), A.sw_y, Mp, false, 0);
     const double *mpc = Mp;
+    pre_spmv(Mp, !nopre);
     rows<K, CX, 1, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
                         double vr[K], vi[K], rr[K], ri[K];
@@ -863,6 +883,7 @@ struct Solver : PlanBase {
     sweep(head_re(t), head_im(t), A.sw_y, Mt, false, 0);
     // K7: Bt = A Mt ; btbt, btt (+ yy, ybt, bty, yt when it > 1)
     const double *mtc = Mt;
+    pre_spmv(Mt, !nopre);
     rows<K, CX, 6, 0>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 6, 0> &red) {
                         double br[K], bi[K], tr[K], ti[K];
@@ -1075,19 +1096,21 @@ struct Solver : PlanBase {
     // q = A p ; sigma = hdot(pt, q) (role 0) || qt = A^H pt (role 1): the
     // two SpMV chains run on separate threads
     const long long nn = n;
+    pre_spmv(pp, false);
+    pre_spmv(pt, false, true);
     rows<K, CX, 1, 0>(
         n, done, part, st,
         [=] __device__(long long i, Red<K, CX, 1, 0> &red) {
           if (i < nn) {
             double qr[K], qi[K], pr[K], pi[K];
-            spmv_row<K, CX, false, false>(a, (int)i, pc, L, qr, qi);
+            spmv_mc<K, CX, false>(a, (int)i, pc, L, qr, qi);
             Q.store(i, qr, qi);
             PT.load(i, pr, pi);
             acc_hdot<K, CX>(red.h[0], pr, pi, qr, qi);
           } else {
             const long long j = i - nn;
             double wr[K], wi[K];
-            spmv_row<K, CX, false, true>(a, (int)j, ptc, L, wr, wi);
+            spmv_mc<K, CX, true>(a, (int)j, ptc, L, wr, wi);
             QT.store(j, wr, wi);
           }
         },
@@ -1232,10 +1255,11 @@ struct Solver : PlanBase {
     const DA a = da;
     const long long L = ld;
     const int np_ = nopre;
+    pre_spmv(d_x, false, false, true);
     rows<K, CX, 0, 2>(n, nullptr, part, st,
                       [=] __device__(long long i, Red<K, CX, 0, 2> &red) {
                         double axr[K], axi[K], br[K], bi[K], rr[K], ri[K];
-                        spmv_row<K, CX, false, false>(a, (int)i, d_x, L, axr, axi);
+                        spmv_mc<K, CX, false>(a, (int)i, d_x, L, axr, axi);
                         B.load(i, br, bi);
                         e_sub<K, CX>(br, bi, axr, axi, rr, ri);
                         acc_sumsq<K, CX>(red.nr[0], rr, ri);
@@ -1267,7 +1291,7 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   // plan cache: one workspace + graph per (method, K, field) on this matrix
   const int key = (p.precond_ilu == 1 ? 0 : (p.precond_ilu + 1) * 10000000) +
                   (p.ex ? 100000 * p.ex->world : 0) +
-                  p.reduce_seq * 1000 +
+                  p.reduce_seq * 1000 + p.full_a * 5000 +
                   p.method * 100 + K * 10 + (CX ? 1 : 0);
   Solver<K, CX> *sv = nullptr;
   auto it = A.plans.find(key);

@@ -15,7 +15,21 @@ struct DA {
   const double *val;
   const int *at_rp, *at_ci;
   const double *at_val;
+  // MC-valued matrix (spmv_mode 'full'): A x / A^H x were formed by the
+  // full-precision kernel (units.cu spmv_full_kernel) into these planar MC
+  // vectors just before the row kernel; null otherwise
+  const double *pre = nullptr, *pre_adj = nullptr;
 };
+
+template <int K, bool CX>
+__device__ __forceinline__ void load_pre(const double *q, long long ld, int i,
+                                         double (&yr)[K], double (&yi)[K]) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    yr[c] = q[c * ld + i];
+    yi[c] = CX ? q[(K + c) * ld + i] : 0.0;
+  }
+}
 
 template <int K, bool CX, bool XF, bool ADJ>
 __device__ __forceinline__ void spmv_row(const DA &A, int i, const double *x,
@@ -71,10 +85,24 @@ template <int K, bool CX>
 __device__ __forceinline__ void spmv_fv(const DA &A, int i, const double *x,
                                         long long ld, int mc, double (&yr)[K],
                                         double (&yi)[K]) {
-  if (mc)
+  if (A.pre)
+    load_pre<K, CX>(A.pre, ld, i, yr, yi);
+  else if (mc)
     spmv_row<K, CX, false, false>(A, i, x, ld, yr, yi);
   else
     spmv_row<K, CX, true, false>(A, i, x, ld, yr, yi);
+}
+
+// SpMV row (plain or adjoint) on a full MC vector
+template <int K, bool CX, bool ADJ>
+__device__ __forceinline__ void spmv_mc(const DA &A, int i, const double *x,
+                                        long long ld, double (&yr)[K],
+                                        double (&yi)[K]) {
+  const double *q = ADJ ? A.pre_adj : A.pre;
+  if (q)
+    load_pre<K, CX>(q, ld, i, yr, yi);
+  else
+    spmv_row<K, CX, false, ADJ>(A, i, x, ld, yr, yi);
 }
 
 // ---------------------------------------------------------------------

@@ -62,6 +62,111 @@ int unit_spmv(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
   return 3;
 }
 
+// ---------------------------------------------------------------------
+// Full-precision SpMV on an MC-valued matrix (sparse.py:414-451 ->
+// _kernels.py:224-240 spmv_real, :266-278 spmv_adjoint_real, :300-323
+// spmv_cx, :356-376 spmv_adjoint_cx): every product is the generic
+// K x K `mul` / `cmul`, rows accumulate in ascending column order; the
+// adjoint is a gather over the transposed pattern in ascending source-row
+// order (the reference's scatter order per output row) with the matrix
+// entry conjugated.  Values are planar: component c of entry p at
+// mcv[c * vld + p], imaginary planes after the K real ones.  xf != 0: x is
+// an F vector (binary64 head of an ILU(0)-mixed apply; zero tails).
+// ---------------------------------------------------------------------
+template <int K, bool CX, bool ADJ>
+__global__ void __launch_bounds__(kBlock)
+    spmv_full_kernel(int n, const int *__restrict__ rp, const int *__restrict__ ci,
+                     const int *__restrict__ perm, const double *__restrict__ mcv,
+                     long long vld, const double *__restrict__ x, long long ld, int xf,
+                     double *__restrict__ y, const int *done) {
+  if (done && *done) return;
+  for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kBlock) {
+    double yr[K], yi[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) yr[c] = yi[c] = 0.0;
+    const int lo = rp[i], hi = rp[i + 1];
+    for (int q = lo; q < hi; ++q) {
+      const int j = ci[q];
+      const long long p = ADJ ? perm[q] : q;
+      double ar[K], xr[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) ar[c] = mcv[c * vld + p];
+      if constexpr (!CX) {
+        if (xf) {
+#pragma unroll
+          for (int c = 0; c < K; ++c) xr[c] = 0.0;
+          xr[0] = x[j];
+        } else {
+#pragma unroll
+          for (int c = 0; c < K; ++c) xr[c] = x[c * ld + j];
+        }
+        double t[K];
+        mul<K>(ar, xr, t);
+        add<K>(yr, t, yr);
+      } else {
+        double ai[K], xi[K], pr[K], pi[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          const double v = mcv[(K + c) * vld + p];
+          ai[c] = ADJ ? -v : v;
+        }
+        if (xf) {
+          const double2 xv = reinterpret_cast<const double2 *>(x)[j];
+#pragma unroll
+          for (int c = 0; c < K; ++c) xr[c] = xi[c] = 0.0;
+          xr[0] = xv.x;
+          xi[0] = xv.y;
+        } else {
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            xr[c] = x[c * ld + j];
+            xi[c] = x[(K + c) * ld + j];
+          }
+        }
+        cmul<K>(ar, ai, xr, xi, pr, pi);
+        add<K>(yr, pr, yr);
+        add<K>(yi, pi, yi);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      y[c * ld + i] = yr[c];
+      if constexpr (CX) y[(K + c) * ld + i] = yi[c];
+    }
+  }
+}
+
+int unit_spmv_full(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
+                   double *d_y, const int *done, cudaStream_t st) {
+  if (!A.mcv || A.mcv_k != k) return 3;
+  if (adjoint) ensure_adjoint(A, st);
+  const long long L = plane_ld(A.n);
+  const int *rp = adjoint ? A.at_rp : A.rp, *ci = adjoint ? A.at_ci : A.ci;
+  const int grid = grid_for(A.n);
+  ++tl_launches;
+#define LAUNCH(KK, CXX, ADJJ)                                                        \
+  spmv_full_kernel<KK, CXX, ADJJ><<<grid, kBlock, 0, st>>>(                          \
+      A.n, rp, ci, A.at_perm, A.mcv, A.mcv_ld, d_x, L, x_is_f ? 1 : 0, d_y, done)
+#define DISPATCH(KK)                                   \
+  if (k == KK) {                                       \
+    if (A.cx) {                                        \
+      if (adjoint) LAUNCH(KK, true, true);             \
+      else LAUNCH(KK, true, false);                    \
+    } else {                                           \
+      if (adjoint) LAUNCH(KK, false, true);            \
+      else LAUNCH(KK, false, false);                   \
+    }                                                  \
+    return 0;                                          \
+  }
+  DISPATCH(2)
+  DISPATCH(3)
+  DISPATCH(4)
+#undef DISPATCH
+#undef LAUNCH
+  return 3;
+}
+
 template <int K, bool CX>
 __global__ void unit_fin_kernel(const double *part, int G, int op,
                                 double *out) {

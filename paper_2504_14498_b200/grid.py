@@ -130,15 +130,27 @@ def _row(name: str, rep: SolveReport) -> BenchRow:
                     float(rep.error_norm))
 
 
-def run_cell(A, problem: ProblemSpec, cfg: SolverConfig) -> BenchRow:
-    return _row(problem.matrix_name, solve(A, problem.b, cfg, x_star=problem.x_star))
+def run_cell(A, problem: ProblemSpec, cfg: SolverConfig,
+             parallel_spmv: bool = False) -> BenchRow:
+    """One cell (bench.py:172-176).  `parallel_spmv` asks the reference for
+    its row-parallel CPU SpMV; the device SpMV is row-parallel already and
+    computes the same rows, so the flag changes nothing here."""
+    return _row(problem.matrix_name,
+                solve(A, problem.b, cfg, x_star=problem.x_star, parallel_spmv=parallel_spmv))
 
 
-def run_benchmark(suite, log=None) -> list:
-    """Cells (A, problem, cfg) one after another on the device (uncontended
-    timings); a failing cell becomes a non-converged row with NaN timings."""
-    rows = []
-    for A, problem, cfg in suite:
+def run_benchmark(suite, jobs: int = 1, log=None) -> list:
+    """Cells (A, problem, cfg); a failing cell becomes a non-converged row
+    with NaN timings (bench.py:179-216).  jobs = 1 runs them one after
+    another (uncontended timings); jobs > 1 hands them to a pool of `jobs`
+    threads -- solves that share a device context queue behind each other on
+    its stream, so, as in the reference, the timing fields are then
+    unreliable while every other field is unchanged."""
+    if not callable(log) and log is not None:
+        raise TypeError("log must be a callable taking one string (or None)")
+
+    def one(cell):
+        A, problem, cfg = cell
         try:
             row = run_cell(A, problem, cfg)
         except Exception as exc:  # reported in the row, the grid continues
@@ -150,8 +162,15 @@ def run_benchmark(suite, log=None) -> list:
         if log:
             log(f"{row.matrix} {row.method} {row.precision} {row.precond} {row.spmv_mode}: "
                 f"iters={row.iterations} converged={row.converged} total={row.total_s:.3f}s")
-        rows.append(row)
-    return rows
+        return row
+
+    suite = list(suite)
+    if int(jobs) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=int(jobs)) as pool:
+            return list(pool.map(one, suite))
+    return [one(cell) for cell in suite]
 
 
 def ratio_rows(rows) -> list:

@@ -4,9 +4,9 @@ Reference: /root/reference/pkg/src/mpkrylov/ilu.py.  The factorization
 (_factorize_tuples :178-276 with k=1) and the forward/backward sweeps
 (:322-371) run as sync-free, one-row-per-thread CUDA kernels that keep the
 reference's per-row operation order, so factors and sweep results are
-bitwise identical (csrc/ilu.cu).  The full-working-precision ILU(0)
-(PrecondMode.ILU0_FULL) is not on the north-star
-path and raises NotImplementedError.
+bitwise identical (csrc/ilu.cu).  The working-precision ILU(0)
+(PrecondMode.ILU0_FULL, ilu.py:279-281) runs in
+K-component arithmetic on the device (csrc/ilu_mc.cu).
 """
 
 from __future__ import annotations
@@ -156,13 +156,10 @@ class IluFactorsMC(IluFactors):
 def ilu0_factorize(A) -> IluFactors:
     """Zero-fill ILU at the matrix's working precision (ilu.py:279-281): k = 1
     binary64, k = 2..4 in K-component arithmetic with the reference's fused
-    a - b*c (real field, binary64-valued matrices on the device path)."""
+    a - b*c; an MC-valued matrix is factored with all its components
+    (device_matrix attaches them)."""
     if A.precision.k == 1:
         return _factor(A)
-    if np.any(np.asarray(A.val_re)[:, 1:]) or (
-            A.val_im is not None and np.any(np.asarray(A.val_im)[:, 1:])):
-        raise NotImplementedError(
-            "working-precision ILU(0) on the B200 path: binary64-valued matrices")
     d = device_matrix(A)
     bad = ctypes.c_int64(-1)
     st = ctypes.c_int32(0)

@@ -7,11 +7,10 @@ factorization, the method loop with its MC scalar recurrences and stopping
 test, and the true residual -- runs on the GPU in one C-ABI call
 (mpk_solve); the host only uploads A and b and downloads x.
 
-The device path covers the north-star configuration: precond
-``PrecondMode.ILU0_MIXED`` with ``spmv_mode="mixed"``.
-Other combinations (unpreconditioned, full-precision ILU(0)) are listed as
-"next" in SURVEY.md section 8f and raise NotImplementedError instead of
-silently running something else.
+Every combination the reference accepts runs on the device: precond
+``ILU0_MIXED`` (the north-star configuration), ``ILU0_FULL`` and ``NONE``;
+``spmv_mode`` "mixed" and "full", the latter with MC x MC products when the
+matrix carries non-zero tail components (SURVEY.md section 8 a-f).
 
 Extension over the reference report: ``history`` holds every norm2 value
 the method computed (the reference's per-iteration residual norms, as
@@ -117,14 +116,14 @@ def _device_solve(A, b: DenseVector, cfg: SolverConfig, hist_cap: int | None = N
         raise ValueError(f"field mismatch: matrix {A.field}, vector {b.field}")
     if b.precision != cfg.precision:
         raise ValueError("vector precision must match cfg.precision")
-    if cfg.spmv_mode == "full":
-        # full SpMV on a matrix whose values are exactly binary64 IS the mixed
-        # computation bit for bit (reference tests/test_sparse.py:130-147);
-        # matrices with non-zero tails need MC x MC products (section 8f)
-        if not _binary64_exact(A):
-            raise NotImplementedError(
-                "spmv_mode='full' on the B200 path needs binary64-representable "
-                "matrix values (MC-valued matrices: SURVEY.md section 8f)")
+    full = cfg.spmv_mode == "full"
+    if full:
+        # _Ctx.matvec -> spmv(A, v) (solvers.py:126-129, sparse.py:414-418): on
+        # a binary64-valued matrix that IS the mixed computation bit for bit
+        # (reference tests/test_sparse.py:130-147); an MC-valued matrix
+        # multiplies with all its components (device_matrix attaches them)
+        if A.precision.k != cfg.precision.k:
+            raise ValueError("matrix and vector precision must match for spmv")
     elif not _binary64_exact(A):
         raise ValueError("mixed SpMV requires binary64-representable matrix values")
     k = cfg.precision.k
@@ -132,21 +131,27 @@ def _device_solve(A, b: DenseVector, cfg: SolverConfig, hist_cap: int | None = N
     max_iter = cfg.resolved_max_iter(n)
     if hist_cap is None:
         hist_cap = 2 * max_iter + 2
-    d = device_matrix(A)
     x = DenseVector.zeros(n, cfg.precision, A.field)
     hist = np.zeros((max(hist_cap, 1), k))
     rep = _lib.MpkReport()
     pre = {PrecondMode.NONE: 0, PrecondMode.ILU0_MIXED: 1, PrecondMode.ILU0_FULL: 2}[cfg.precond]
-    with _lib.precond_scope(d.ctx, pre):
+    with _lib.ctx_lock(_lib.context()):
+        d = device_matrix(A)
+        rc = _solve_locked(d, cfg, k, max_iter, b, x, hist, hist_cap, rep, pre, full)
+    _lib.check(rc, "mpk_solve")
+    h = [tuple(r) for r in hist[: min(rep.hist_len, hist_cap)]]
+    return rep, (x if rep.has_x else None), h
+
+
+def _solve_locked(d, cfg, k, max_iter, b, x, hist, hist_cap, rep, pre, full):
+    with _lib.precond_scope(d.ctx, pre, spmv_full=full):
         rc = _lib.lib().mpk_solve(
             d.h, ctypes.c_int(_lib.METHOD_CODE[cfg.method]), ctypes.c_int(k),
             ctypes.c_double(cfg.eps_rel), ctypes.c_double(cfg.eps_abs),
             ctypes.c_int64(max_iter), _lib.dptr(_lib.f64(b.re)),
             _lib.dptr(None if b.im is None else _lib.f64(b.im)), _lib.dptr(x.re),
             _lib.dptr(x.im), _lib.dptr(hist), ctypes.c_int64(hist_cap), ctypes.byref(rep))
-    _lib.check(rc, "mpk_solve")
-    h = [tuple(r) for r in hist[: min(rep.hist_len, hist_cap)]]
-    return rep, (x if rep.has_x else None), h
+    return rc
 
 
 def _breakdown_string(rep) -> str | None:

@@ -23,12 +23,16 @@ __all__ = [
     "CsrMatrix",
     "DenseVector",
     "spmv",
+    "spmv_adjoint",
     "spmv_mixed",
     "spmv_adjoint_mixed",
     "hdot",
     "dot",
     "norm2",
     "axpy",
+    "scale",
+    "vec_sub",
+    "vec_add",
     "vec_copy",
     "device_matrix",
 ]
@@ -183,7 +187,31 @@ class DenseVector:
 # ---------------------------------------------------------------------
 # device matrix handles (one upload per matrix object)
 # ---------------------------------------------------------------------
+def _words(a):
+    return np.ascontiguousarray(a).view(np.uint64).ravel()
+
+
+def _fingerprint(*arrays):
+    """Content fingerprint of host arrays: xor and wrapping sum of the raw
+    64-bit words (any in-place change of one entry changes the xor)."""
+    out = []
+    for a in arrays:
+        if a is None:
+            out.append(None)
+            continue
+        w = _words(np.asarray(a))
+        out.append((w.size, int(np.bitwise_xor.reduce(w)) if w.size else 0,
+                    int(w.sum(dtype=np.uint64)) if w.size else 0))
+    return tuple(out)
+
+
 class _DevMatrix:
+    """Device copy of one CsrMatrix: the binary64 (demoted) values every
+    kernel of the mixed path reads and, for an MC-valued matrix (non-zero
+    tail components), all k components for spmv_mode 'full' and the
+    working-precision ILU(0).  `sync` re-uploads values the caller changed in
+    place since the last call (the reference reads A afresh on every call)."""
+
     def __init__(self, A, device: int = 0):
         L = _lib.lib()
         self.ctx = _lib.context(device)
@@ -200,18 +228,53 @@ class _DevMatrix:
         self.h = h
         self.cx = vim is not None
         self.factored = False
+        self.mc_k = 0
+        self.pattern = _fingerprint(A.row_ptr, A.col_idx)
+        self.values = None
         self._fin = weakref.finalize(self, L.mpk_csr_free, h)
+        self.sync(A, heads_current=True)
+
+    def sync(self, A, heads_current: bool = False) -> None:
+        fp = _fingerprint(A.val_re, A.val_im)
+        if fp == self.values:
+            return
+        L = _lib.lib()
+        vre_all = np.asarray(A.val_re)
+        vim_all = None if A.val_im is None else np.asarray(A.val_im)
+        if not heads_current:
+            _lib.check(L.mpk_csr_set_values(
+                self.h, _lib.dptr(_lib.f64(vre_all[:, 0])),
+                _lib.dptr(None if vim_all is None else _lib.f64(vim_all[:, 0]))),
+                "mpk_csr_set_values")
+            self.factored = False
+        k = vre_all.shape[1]
+        tails = k > 1 and (bool(np.any(vre_all[:, 1:])) or
+                           (vim_all is not None and bool(np.any(vim_all[:, 1:]))))
+        if tails:
+            _lib.check(L.mpk_csr_set_mc_values(
+                self.h, ctypes.c_int(k), _lib.dptr(_lib.f64(vre_all)),
+                _lib.dptr(None if vim_all is None else _lib.f64(vim_all))),
+                "mpk_csr_set_mc_values")
+            self.mc_k = k
+        elif self.mc_k:
+            _lib.check(L.mpk_csr_set_mc_values(self.h, ctypes.c_int(0), None, None),
+                       "mpk_csr_set_mc_values")
+            self.mc_k = 0
+        self.values = fp
 
 
 _dev_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 def device_matrix(A) -> _DevMatrix:
-    """The uploaded binary64 (demoted) copy of A, cached per matrix object.
-    Works for this package's CsrMatrix and for the reference's."""
+    """The device copy of A, cached per matrix object and kept in step with
+    in-place changes of A's values (fingerprint check per call) or pattern
+    (fresh upload).  Works for this package's CsrMatrix and the reference's."""
     try:
         d = _dev_cache.get(A)
     except TypeError:
+        d = None
+    if d is not None and d.pattern != _fingerprint(A.row_ptr, A.col_idx):
         d = None
     if d is None:
         d = _DevMatrix(A)
@@ -219,6 +282,8 @@ def device_matrix(A) -> _DevMatrix:
             _dev_cache[A] = d
         except TypeError:
             pass
+    else:
+        d.sync(A)
     return d
 
 
@@ -262,18 +327,35 @@ def spmv_adjoint_mixed(A64, x: DenseVector) -> DenseVector:
     return _spmv_dev(A64, x, True)
 
 
-def spmv(A, x: DenseVector, parallel: bool = False) -> DenseVector:
-    """Full-precision SpMV (sparse.py:414-435) for matrices whose values are
-    exactly binary64 (bitwise equal to the mixed kernel on the demoted
-    matrix, tests/test_sparse.py:130-147)."""
+def _spmv_full_dev(A, x: DenseVector, adjoint: bool, what: str) -> DenseVector:
     _check_pair(A, x)
     if A.precision.k != x.precision.k:
-        raise ValueError("matrix and vector precision must match for spmv")
-    if A.precision.k > 1 and (np.any(A.val_re[:, 1:]) or
-                              (A.val_im is not None and np.any(A.val_im[:, 1:]))):
-        raise NotImplementedError(
-            "device spmv supports binary64-representable matrices only")
-    return _spmv_dev(A, x, False)
+        raise ValueError(f"matrix and vector precision must match for {what}")
+    d = device_matrix(A)
+    k = x.precision.k
+    out = DenseVector.zeros(A.n, x.precision, A.field)
+    xr, xi = _lib.f64(x.re), None if x.im is None else _lib.f64(x.im)
+    _lib.check(_lib.lib().mpk_spmv_full(d.h, ctypes.c_int(k), _lib.dptr(xr), _lib.dptr(xi),
+                                        _lib.dptr(out.re), _lib.dptr(out.im),
+                                        ctypes.c_int(int(adjoint))), "mpk_spmv_full")
+    return out
+
+
+def spmv(A, x: DenseVector, parallel: bool = False) -> DenseVector:
+    """y = A x with products and accumulation at the value precision
+    (sparse.py:414-435 -> _kernels.py:224-240 / 300-323): MC x MC products
+    for an MC-valued matrix; for a binary64-valued one the mixed kernel,
+    which is the same computation bit for bit (tests/test_sparse.py:130-147).
+    `parallel` selects the reference's row-parallel CPU variant, which
+    computes the same rows; the device kernel is row-parallel already."""
+    return _spmv_full_dev(A, x, False, "spmv")
+
+
+def spmv_adjoint(A, x: DenseVector) -> DenseVector:
+    """y = A^H x (sparse.py:438-451 -> _kernels.py:266-278 / 356-376), as a
+    gather over the transposed pattern in the reference's scatter order
+    (ascending source row per output row), entries conjugated."""
+    return _spmv_full_dev(A, x, True, "spmv_adjoint")
 
 
 def _check_vecs(x: DenseVector, y: DenseVector):
@@ -338,6 +420,57 @@ def axpy(alpha, x: DenseVector, y: DenseVector) -> DenseVector:
         _lib.dptr(None if y.im is None else _lib.f64(y.im)), _lib.dptr(out.re),
         _lib.dptr(out.im)), "mpk_axpy")
     return out
+
+
+def _elementwise(op: int, k: int, a_re, a_im, b_re, b_im, cx: bool):
+    n = len(b_re)
+    o_re = np.zeros((n, k))
+    o_im = np.zeros((n, k)) if cx else None
+    _lib.check(_lib.lib().mpk_mc_elementwise(
+        _lib.context(), ctypes.c_int(op), ctypes.c_int(k), ctypes.c_int64(n),
+        _lib.dptr(_lib.f64(a_re)), _lib.dptr(None if a_im is None else _lib.f64(a_im)),
+        _lib.dptr(_lib.f64(b_re)), _lib.dptr(None if b_im is None else _lib.f64(b_im)),
+        _lib.dptr(o_re), _lib.dptr(o_im)), "mpk_mc_elementwise")
+    return o_re, o_im
+
+
+def scale(alpha, x: DenseVector) -> DenseVector:
+    """alpha * x (sparse.py:563-579 -> _kernels.py scale_real / scale_cx:
+    alpha is the left factor of every product)."""
+    k = x.precision.k
+    ar = np.zeros((x.n, k))
+    if x.im is None:
+        ar[:] = alpha.components if isinstance(alpha, MCFloat) else alpha
+        o_re, _ = _elementwise(2, k, ar, None, x.re, None, False)
+        return DenseVector(o_re, None, x.precision)
+    ai = np.zeros((x.n, k))
+    if isinstance(alpha, MCComplex):
+        ar[:] = alpha.re.components
+        ai[:] = alpha.im.components
+    else:
+        ar[:] = alpha.components if isinstance(alpha, MCFloat) else alpha
+    o_re, o_im = _elementwise(5, k, ar, ai, x.re, x.im, True)
+    return DenseVector(o_re, o_im, x.precision)
+
+
+def _planes(op: int, x: DenseVector, y: DenseVector) -> DenseVector:
+    _check_vecs(x, y)
+    k = x.precision.k
+    o_re, _ = _elementwise(op, k, x.re, None, y.re, None, False)
+    o_im = None
+    if x.im is not None:
+        o_im, _ = _elementwise(op, k, x.im, None, y.im, None, False)
+    return DenseVector(o_re, o_im, x.precision)
+
+
+def vec_sub(x: DenseVector, y: DenseVector) -> DenseVector:
+    """x - y (sparse.py:582-590), real and imaginary planes separately."""
+    return _planes(1, x, y)
+
+
+def vec_add(x: DenseVector, y: DenseVector) -> DenseVector:
+    """x + y (sparse.py:593-600)."""
+    return _planes(0, x, y)
 
 
 def vec_copy(x: DenseVector) -> DenseVector:

@@ -374,7 +374,7 @@ def gen_solver_none():
                             tol, 1e-100, None, precond="none")
                 for key, v in o.items():
                     data[f"{tag}{k}_none_{m}_{key}"] = v
-            for m in ("bicgstab", "gpbicg"):
+            for m in ("bicg", "cgs", "bicgstab", "gpbicg"):
                 o = run_ref(A64.val_re[:, 0], vim, A64.row_ptr, A64.col_idx, n, b, m, k,
                             tol, 1e-100, None, spmv_mode="full")
                 for key, v in o.items():

@@ -64,3 +64,31 @@ def test_default_grid_matches_reference():
     assert parse_report(text) == rows
     rr = ratio_rows(rows)
     assert len(rr) == 4 and all(np.isfinite(x.ilu0_over_ilu0d) for x in rr)
+
+
+def test_run_benchmark_jobs_pool_and_signature():
+    """run_benchmark(suite, jobs, log) as the reference's (bench.py:179-216):
+    a thread pool gives the same rows (timing fields aside); a failing cell
+    becomes a non-converged row and is logged."""
+    import paper_2504_14498_b200 as pkg
+    from paper_2504_14498_b200.grid import build_problem, default_grid, run_benchmark, run_cell
+
+    A, _, P = _mats(pkg, 2)
+    pr = build_problem(A, P, "cd5_8")
+    suite = [(A, pr, pkg.SolverConfig(method=m, precision=p, precond=pre, spmv_mode=mode,
+                                      eps_rel=1e-20))
+             for m, p, pre, mode in default_grid(methods=["bicgstab", "cgs"], precisions=[P])]
+    lines = []
+    one = run_benchmark(suite, 1, lines.append)
+    pool = run_benchmark(suite, 4)  # second positional argument is `jobs`
+    stable = lambda r: (r.matrix, r.method, r.precision, r.precond, r.spmv_mode, r.iterations,
+                        r.converged, r.true_relres, r.err2)
+    assert [stable(r) for r in pool] == [stable(r) for r in one]
+    assert len(lines) == len(suite)
+    row = run_cell(A, pr, suite[0][2], parallel_spmv=True)
+    assert stable(row) == stable(one[0])
+    wrong = pkg.DenseVector.zeros(A.n, pkg.Precision.TD, "real")  # precision mismatch
+    bad_pr = type(pr)(pr.matrix_name, pr.field, pr.n, pr.x_star, wrong)
+    failed = run_benchmark([(A, bad_pr, suite[0][2])], jobs=2, log=lines.append)
+    assert failed[0].iterations == 0 and not failed[0].converged
+    assert any(s.startswith("cell failed") for s in lines)

@@ -164,3 +164,29 @@ def test_product_does_not_import_oracle():
         assert "import oracle" not in txt and "from oracle" not in txt, f
     for f in list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
         assert "mpk_oracle" not in f.read_text(), f
+
+
+def test_integration_binding_signatures():
+    """The reference-side ctypes stub in INTEGRATION.md declares argtypes that
+    match include/mpk_b200.h parameter for parameter (an untyped Python int
+    would travel as a 32-bit c_int into an int64_t parameter)."""
+    doc = (ROOT / "INTEGRATION.md").read_text()
+    hdr = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "mpk_b200.h").read_text(), flags=re.S)
+    stubs = dict(re.findall(r"_L\.(mpk_\w+)\.argtypes = \[(.*?)\]", doc, flags=re.S))
+    assert {"mpk_csr_upload", "mpk_solve", "mpk_ctx_create", "mpk_thread_set_option",
+            "mpk_csr_set_mc_values", "mpk_csr_free"} <= set(stubs)
+    scalar = {"int": "c_int", "int32_t": "c_int32", "int64_t": "c_int64", "double": "c_double"}
+    for fn, arglist in stubs.items():
+        args = [a.strip() for a in re.sub(r"#.*", "", arglist).replace("\n", " ").split(",")
+                if a.strip()]
+        # POINTER(x) contains no comma, so the split is positional
+        m = re.search(rf"\b{fn}\s*\((.*?)\)\s*;", hdr, flags=re.S)
+        assert m, fn
+        params = [p.strip() for p in m.group(1).replace("\n", " ").split(",")]
+        assert len(params) == len(args), (fn, params, args)
+        for prm, arg in zip(params, args):
+            if "*" in prm:
+                assert arg == "c_void_p" or arg.startswith("POINTER("), (fn, prm, arg)
+            else:
+                ctype = prm.replace("const ", "").split()[0]
+                assert scalar[ctype] == arg, (fn, prm, arg)
