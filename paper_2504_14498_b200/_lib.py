@@ -200,9 +200,12 @@ def ctx_lock(ctx) -> "threading.RLock":
 
 
 def dptr(a):
+    """Pointer argument for an array (or None).  The returned object holds a
+    reference to `a` (numpy's data_as), so a temporary such as the
+    contiguous copy `f64(v[:, 0])` stays alive until the call returns."""
     if a is None:
         return None
-    return ctypes.c_void_p(a.ctypes.data)
+    return a.ctypes.data_as(ctypes.c_void_p)
 
 
 def f64(a):

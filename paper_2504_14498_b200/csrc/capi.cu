@@ -1213,9 +1213,9 @@ int mpk_ilu0_factor_full(mpk_matrix *m, int k, int64_t *bad_row, int32_t *struct
   if (A.nnz > 0) {
     ++tl_launches;
     if (A.mcv && A.mcv_k == k)  // MC-valued matrix: ilu0_factorize(A) factors A itself
-      mc_vals_kernel<<<148 * 4, 256, 0, st>>>(A.nnz, W, A.mcv, A.mcv_ld, A.lu_mc);
+      mc_vals_kernel<<<sm_count() * 4, 256, 0, st>>>(A.nnz, W, A.mcv, A.mcv_ld, A.lu_mc);
     else
-      promote_vals_kernel<<<148 * 4, 256, 0, st>>>(A.nnz, k, A.cx ? 1 : 0, A.val, A.lu_mc);
+      promote_vals_kernel<<<sm_count() * 4, 256, 0, st>>>(A.nnz, k, A.cx ? 1 : 0, A.val, A.lu_mc);
   }
   CKR(cudaMemsetAsync(m->rowflag, 0, sizeof(int) * (A.n + 1), st));
   if (!m->hres) CKR(cudaMallocHost(&m->hres, sizeof(int) * 8));
@@ -1348,6 +1348,21 @@ int mpk_ilu0_download(mpk_matrix *m, double *lu_re, double *lu_im) {
   return MPK_OK;
 }
 
+// The sync-free sweeps signal "value ready" by overwriting a signalling-NaN
+// sentinel (common.cuh kSentBits; the wavefront plans test its high word).
+// No binary64 operation produces a signalling NaN, so inside a solve every
+// sweep input (an MC arithmetic result) is safe; a caller-supplied vector
+// could carry the pattern through a row without entries (a pure copy) and
+// stall its consumers.  The apply entry points therefore quiet such values
+// (-> the quiet NaN the hardware would make of them) before the sweep: the
+// apply then ends with NumericBreakdownError like any non-finite input.
+__global__ void quiet_sentinels_kernel(double *v, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (__double2hiint(v[i]) == (int)(kSentBits >> 32))
+      v[i] = __longlong_as_double((long long)kQNaNBits);
+}
+
 // apply on a device planar-MC input; output F vector in `fz`
 static int apply_dev(mpk_matrix *m, int k, const double *in_mc, double *fz,
                      int adjoint) {
@@ -1357,6 +1372,11 @@ static int apply_dev(mpk_matrix *m, int k, const double *in_mc, double *fz,
   const long long L = plane_ld(A.n);
   CKR(cudaMemsetAsync(A.err, 0, sizeof(int), st));
   launch_sweep_reset(A.sw_y, fz, A.n, A.cx, nullptr, st);
+  if (A.n > 0) {  // head planes only: the sweeps read the demoted input
+    double *head = const_cast<double *>(in_mc);
+    quiet_sentinels_kernel<<<grid_for(A.n), kBlock, 0, st>>>(head, A.n);
+    if (A.cx) quiet_sentinels_kernel<<<grid_for(A.n), kBlock, 0, st>>>(head + (long long)k * L, A.n);
+  }
   SweepArgs a{};
   a.n = A.n;
   a.rp = A.rp;

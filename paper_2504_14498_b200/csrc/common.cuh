@@ -33,6 +33,17 @@ inline thread_local long long tl_launches = 0;
 inline thread_local double *tl_seq = nullptr;
 // host-side phase marks of the current solve (MPK_PHASE_TIMES diagnostics)
 inline thread_local double tl_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+// SM count of the current device (B200: 148), queried once
+inline int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    return v;
+  }();
+  return n;
+}
 inline double host_ms() {
   return std::chrono::duration<double, std::milli>(
              std::chrono::steady_clock::now().time_since_epoch())

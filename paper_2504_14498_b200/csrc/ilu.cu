@@ -1197,6 +1197,10 @@ __global__ void __launch_bounds__(1024, 1)
         else
           qr = ddiv(ar, vals[x]);
       }
+      // a value carrying the sentinel pattern (only a copied input can) is
+      // published as a quiet NaN, so no consumer waits on it forever
+      qr = unsent(qr);
+      if constexpr (CX) qi = unsent(qi);
       // push to every peer first, then the own copy
       const uint32_t la = vbase + (uint32_t)d.row * ESZ;
       for (int kk = 1; kk < C; ++kk) {
@@ -1425,7 +1429,7 @@ int sweep_grid(int n) {
   long long warps = (2LL * n + 31) / 32;
   long long blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks < 1) blocks = 1;
-  if (blocks > 148 * 6) blocks = 148 * 6;
+  if (blocks > sm_count() * 6) blocks = sm_count() * 6;
   return (int)blocks;
 }
 
@@ -1626,7 +1630,7 @@ void launch_factor(const FactorArgs &a, bool cx, cudaStream_t st) {
   long long warps = (a.n + 31) / 32;
   long long blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks < 1) blocks = 1;
-  if (blocks > 148 * 6) blocks = 148 * 6;
+  if (blocks > sm_count() * 6) blocks = sm_count() * 6;
   if (cx)
     factor_kernel<true><<<(int)blocks, kBlock, 0, st>>>(b);
   else

@@ -495,7 +495,7 @@ static int mc_grid_cap() {
   static const int cap = [] {
     const char *e = getenv("MPK_MC_BLOCKS");
     const int v = e ? atoi(e) : 0;
-    return v > 0 ? v : 148;
+    return v > 0 ? v : sm_count();
   }();
   return cap;
 }
@@ -520,7 +520,7 @@ void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k,
                      cudaStream_t st) {
   if (n <= 0) return;
   ++tl_launches;
-  const int g = (n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8;
+  const int g = (n + 255) / 256 < sm_count() * 8 ? (n + 255) / 256 : sm_count() * 8;
   if (k == 2 && !cx) recip_mc_kernel<2, false><<<g, 256, 0, st>>>(n, dp, lu, rcp);
   if (k == 3 && !cx) recip_mc_kernel<3, false><<<g, 256, 0, st>>>(n, dp, lu, rcp);
   if (k == 4 && !cx) recip_mc_kernel<4, false><<<g, 256, 0, st>>>(n, dp, lu, rcp);
@@ -531,7 +531,7 @@ void launch_recip_mc(int n, const int *dp, const double *lu, double *rcp, int k,
 
 void launch_sweep_mc(const SweepMcArgs &a, int k, cudaStream_t st) {
   const int nb = (a.n + 255) / 256 > 0 ? (a.n + 255) / 256 : 1;
-  const int g = nb < 148 * 8 ? nb : 148 * 8;
+  const int g = nb < sm_count() * 8 ? nb : sm_count() * 8;
   tl_launches += 2;
   reset_mc_kernel<<<g, 256, 0, st>>>(a.y, a.z, a.n, a.ld, (a.cx ? 2 : 1) * k, a.done);
   long long warps = (2LL * a.n + 31) / 32;

@@ -132,14 +132,27 @@ struct Red {
   }
 };
 
-// at least kRowsMinBlocks blocks per SM: caps registers so more warps stay
-// resident (the row kernels are latency-bound chains of MC operations, and
-// concurrent solves compete for warp slots)
+// Blocks per SM the row kernels are compiled for (the register cap).  The
+// reduction tree is fixed at kMaxGrid = 4 x 148 block partials, so a kernel
+// that fits 4 blocks per SM (<= 64 registers) runs its 592 blocks in ONE
+// wave; at 3 per SM (the 68-register DD SpMV / update kernels of cfg4) the
+// grid took 1.33 waves with a third of the SMs' warp slots idle in the
+// second (ncu r02: achieved occupancy 30 %, 44 % of cycles without an
+// eligible warp).  Real DD kernels fit 64 registers without spilling; the
+// complex / TD / QD kernels keep 3 blocks per SM (80 registers; concurrent
+// solves of cfg2 / cfg5 compete for warp slots).
+#ifndef MPK_ROWS_MIN_BLOCKS_DD
+#define MPK_ROWS_MIN_BLOCKS_DD 4
+#endif
 #ifndef MPK_ROWS_MIN_BLOCKS
 #define MPK_ROWS_MIN_BLOCKS 3
 #endif
+template <int K, bool CX>
+constexpr int rows_min_blocks() {
+  return (K == 2 && !CX) ? MPK_ROWS_MIN_BLOCKS_DD : MPK_ROWS_MIN_BLOCKS;
+}
 template <int K, bool CX, int NH, int NN, class F>
-__global__ void __launch_bounds__(kBlock, MPK_ROWS_MIN_BLOCKS)
+__global__ void __launch_bounds__(kBlock, rows_min_blocks<K, CX>())
     rows_kernel(long long n_total, long long n, const int *done, double *part,
                 double *seq, F f, long long i0) {
   // n_total = roles * n: element i of role r is index r * n + i; only role 0

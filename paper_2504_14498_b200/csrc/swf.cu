@@ -1105,7 +1105,7 @@ bool build_ssweep(SSweep &w, int n, bool cx, const int *rp, const int *ci, const
       Q->cl = 1;
       for (int cl = want; cl >= 2; cl /= 2) {
         const int grid = (Q->ngroups + cl - 1) / cl * cl;
-        if (grid > 148) continue;
+        if (grid > sm_count()) continue;
         if (max_clusters(*Q, cl, grid, t.smem) >= grid / cl) {
           Q->cl = cl;
           break;
@@ -1126,7 +1126,7 @@ void gather_ssweep(const double *lu, const SSweep &w, cudaStream_t st) {
     if (tot <= 0) continue;
     ++tl_launches;
     long long g = (tot + 255) / 256;
-    if (g > 148 * 16) g = 148 * 16;
+    if (g > sm_count() * 16) g = sm_count() * 16;
     swf_gather_kernel<<<(unsigned)g, 256, 0, st>>>(lu, *P);
   }
 }
@@ -1140,8 +1140,8 @@ void launch_ssweep(const SweepArgs &a, const SSweep &w, cudaStream_t st) {
     int grid = Q.ngroups;
     if (Q.cl > 1)
       grid = (Q.ngroups + Q.cl - 1) / Q.cl * Q.cl;
-    else if (grid > 148)
-      grid = 148;
+    else if (grid > sm_count())
+      grid = sm_count();
     launch_phase(a, Q, w.W, grid, w.smem, st);
   }
 }

@@ -830,7 +830,7 @@ void gather_wsweep(const double *lu, const WSweep &w, bool cx,
     if (tot <= 0) continue;
     ++tl_launches;
     long long g = (tot + 255) / 256;
-    if (g > 148 * 16) g = 148 * 16;
+    if (g > sm_count() * 16) g = sm_count() * 16;
     wf_gather_kernel<<<(unsigned)g, 256, 0, st>>>(lu, *P, cx ? 1 : 0);
   }
 }
@@ -842,7 +842,7 @@ void launch_wsweep(const SweepArgs &a, const WSweep &w, bool cx,
   const int bufsz = std::max(w.f.chunkb, w.b.chunkb);
   const int gtot = w.f.ngroups + w.b.ngroups;
   int grid = gtot;
-  if (grid > 148) grid = 148;
+  if (grid > sm_count()) grid = sm_count();
   if (cx) {
     static bool attr = false;
     if (!attr) {

@@ -242,19 +242,21 @@ class _DevMatrix:
         vre_all = np.asarray(A.val_re)
         vim_all = None if A.val_im is None else np.asarray(A.val_im)
         if not heads_current:
-            _lib.check(L.mpk_csr_set_values(
-                self.h, _lib.dptr(_lib.f64(vre_all[:, 0])),
-                _lib.dptr(None if vim_all is None else _lib.f64(vim_all[:, 0]))),
-                "mpk_csr_set_values")
+            # the head columns are strided views: keep their contiguous copies
+            # alive in locals for the duration of the call
+            hre = _lib.f64(vre_all[:, 0])
+            him = None if vim_all is None else _lib.f64(vim_all[:, 0])
+            _lib.check(L.mpk_csr_set_values(self.h, _lib.dptr(hre), _lib.dptr(him)),
+                       "mpk_csr_set_values")
             self.factored = False
         k = vre_all.shape[1]
         tails = k > 1 and (bool(np.any(vre_all[:, 1:])) or
                            (vim_all is not None and bool(np.any(vim_all[:, 1:]))))
         if tails:
-            _lib.check(L.mpk_csr_set_mc_values(
-                self.h, ctypes.c_int(k), _lib.dptr(_lib.f64(vre_all)),
-                _lib.dptr(None if vim_all is None else _lib.f64(vim_all))),
-                "mpk_csr_set_mc_values")
+            fre = _lib.f64(vre_all)
+            fim = None if vim_all is None else _lib.f64(vim_all)
+            _lib.check(L.mpk_csr_set_mc_values(self.h, ctypes.c_int(k), _lib.dptr(fre),
+                                               _lib.dptr(fim)), "mpk_csr_set_mc_values")
             self.mc_k = k
         elif self.mc_k:
             _lib.check(L.mpk_csr_set_mc_values(self.h, ctypes.c_int(0), None, None),
@@ -426,10 +428,10 @@ def _elementwise(op: int, k: int, a_re, a_im, b_re, b_im, cx: bool):
     n = len(b_re)
     o_re = np.zeros((n, k))
     o_im = np.zeros((n, k)) if cx else None
+    ins = [None if a is None else _lib.f64(a) for a in (a_re, a_im, b_re, b_im)]  # kept alive
     _lib.check(_lib.lib().mpk_mc_elementwise(
         _lib.context(), ctypes.c_int(op), ctypes.c_int(k), ctypes.c_int64(n),
-        _lib.dptr(_lib.f64(a_re)), _lib.dptr(None if a_im is None else _lib.f64(a_im)),
-        _lib.dptr(_lib.f64(b_re)), _lib.dptr(None if b_im is None else _lib.f64(b_im)),
+        _lib.dptr(ins[0]), _lib.dptr(ins[1]), _lib.dptr(ins[2]), _lib.dptr(ins[3]),
         _lib.dptr(o_re), _lib.dptr(o_im)), "mpk_mc_elementwise")
     return o_re, o_im
 

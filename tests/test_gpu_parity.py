@@ -392,6 +392,36 @@ def test_device_sweep_paths_bitwise(pkg, monkeypatch, path, mat):
             assert bits_equal(z.im, zi), (path, mat, adj)
 
 
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("path", list(SWEEP_PATHS))
+@pytest.mark.parametrize("mat", ["cfg1", "cfg2"])
+def test_device_sweeps_do_not_wait_on_a_sentinel_valued_input(pkg, monkeypatch, path, mat):
+    """The sync-free sweeps mark "not ready" with a signalling-NaN pattern.  A
+    caller's vector that carries this very pattern through rows without
+    entries (pure copies) must not stall any sweep implementation: the
+    apply ends with NumericBreakdownError, as the reference does for any
+    non-finite sweep value (ilu.py:322-343, 448-458)."""
+    from paper_2504_14498_b200 import problems
+
+    for k_, v_ in SWEEP_PATHS[path].items():
+        monkeypatch.setenv(k_, v_)
+    p = getattr(problems, mat)()
+    A = _csr(pkg, p.row_ptr, p.col_idx, p.val_re, p.val_im)
+    F = pkg.ilu0_factorize_demoted(A)
+    sent = np.array([0x7FF40000DEADBEEF], dtype=np.uint64).view(np.float64)[0]
+    r = np.ones((p.n, 2))
+    r[:, 1] = 0.0
+    r[0, 0] = sent   # row 0 has no L entries: y_0 = r_0
+    r[p.n - 1, 0] = sent
+    rv = pkg.DenseVector(r, None, pkg.Precision.DD)
+    for apply in (pkg.ilu0_apply_mixed, pkg.ilu0_apply_adjoint_mixed):
+        with pytest.raises(pkg.NumericBreakdownError):
+            apply(F, rv)
+    ok = pkg.ilu0_apply_mixed(F, pkg.DenseVector(np.ones((p.n, 2)) * [1.0, 0.0], None,
+                                                 pkg.Precision.DD))
+    assert np.all(np.isfinite(ok.re))  # the matrix state is intact afterwards
+
+
 WF_MATS = {
     "cd5_64": lambda pr: pr.convdiff5(64, 10.0)[:3] + (None,),
     "cd9_200": lambda pr: pr.convdiff9(200, 5.0)[:3] + (None,),

@@ -14,12 +14,16 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
 
 
 def short(name):
-    m = re.match(r"void (?:mpk::)?(?:\(anonymous namespace\)::|<unnamed>::)?(\w+)", name)
-    base = m.group(1) if m else name[:50]
+    name = re.sub(r"\((?:int|bool)\)", "", name)
+    m = re.match(r"(?:void )?(?:mpk::)?(?:\(anonymous namespace\)::|<?unnamed>::)?(\w+)(<[\d, ]+>)?", name)
+    base = (m.group(1) + (m.group(2) or "")) if m else name[:50]
+    r = re.match(r"(?:void )?(?:mpk::)?rows_kernel<(\d), (\d), (\d), (\d)", name)
+    if r:
+        base = f"rows_kernel<K={r.group(1)},cx={r.group(2)},NH={r.group(3)},NN={r.group(4)}>"
     s = re.search(r"Solver<(\d), (\d)>::(\w+)\([^)]*\)::\[lambda[^\]]*\(instance (\d+)\)\]", name)
     if s:
-        base += f" {s.group(3)}#{s.group(4)} K={s.group(1)}{' cx' if s.group(2) == '1' else ''}"
-    t = re.search(r"sweep\w*_kernel<\(bool\)(\d), \(bool\)(\d)", name)
+        base += f" {s.group(3)}#{s.group(4)}"
+    t = re.search(r"sweep\w*_kernel<(\d), (\d)>", name)
     if t:
         base += f" cx={t.group(1)} adj={t.group(2)}"
     return base
