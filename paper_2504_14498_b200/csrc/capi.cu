@@ -935,6 +935,21 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
         [&](int i) { return rp[i + 1]; }, ob, pb);
   }
   const double t_up2 = host_ms();
+  // deep L DAG (grid stencils: thousands of levels): factorization tickets
+  // in level order, each level padded to whole warps (ilu.cu launch_factor)
+  if (A.levels_f >= 1024) {
+    std::vector<int> op;
+    op.reserve(of.size() + 32 * (size_t)A.levels_f);
+    for (int l = 0; l < A.levels_f; ++l) {
+      for (int q = pf[l]; q < pf[l + 1]; ++q) op.push_back(of[q]);
+      while (op.size() % 32) op.push_back(-1);
+    }
+    A.nt_fp = (int)op.size();
+    if (upload(&A.ord_fp, op, st)) {
+      delete m;
+      return fail(MPK_CUDA_ERROR, "allocation failed");
+    }
+  }
   if (upload(&A.rp, A.h_rp, st) || upload(&A.ci, A.h_ci, st) ||
       upload(&A.dp, A.h_dp, st) || upload(&A.ord_f, of, st) ||
       upload(&A.ord_b, ob, st) || upload(&A.lev_f, pf, st) ||
@@ -1051,6 +1066,46 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
   if (getenv("MPK_VERBOSE"))
     fprintf(stderr, "[mpk] upload n=%lld: sweep plans %.1f ms\n", (long long)n,
             host_ms() - t_plan0);
+  // Sweep-pipelined SpMV plan (units.cu pspmv_kernel): for a large real
+  // stencil pattern on the shuffle-wavefront plan, the 32-row chunks of A
+  // sorted by the backward-DAG level at which all their columns' z values
+  // exist (counting sort over the levels).
+  if (A.smat.ss.on && !A.cx && n >= (1 << 18) && ssweep_bwd_ctas(A.smat.ss) > 0 &&
+      env_int("MPK_PIPE", 1) != 0) {
+    const double t_p0 = host_ms();
+    const int *rp = A.h_rp.data(), *ci = A.h_ci.data();
+    int maxlen = 0;
+    for (int64_t i = 0; i < n; ++i) maxlen = std::max(maxlen, rp[i + 1] - rp[i]);
+    if (maxlen <= kPipeRow) {
+      std::vector<int> levb(n);
+      for (int l = 0; l < A.levels_b; ++l)
+        for (int q = pb[l]; q < pb[l + 1]; ++q) levb[ob[q]] = l;
+      const int nch = (int)((n + 31) / 32);
+      std::vector<int> ready(nch, 0), cnt(A.levels_b + 1, 0), order(nch);
+      for (int c = 0; c < nch; ++c) {
+        const int64_t i1 = std::min<int64_t>(n, (int64_t)c * 32 + 32);
+        int r = 0;
+        for (int q = rp[(int64_t)c * 32]; q < rp[i1]; ++q) r = std::max(r, levb[ci[q]]);
+        ready[c] = r;
+        ++cnt[r + 1];
+      }
+      for (int l = 0; l < A.levels_b; ++l) cnt[l + 1] += cnt[l];
+      for (int c = 0; c < nch; ++c) order[cnt[ready[c]]++] = c;
+      A.pipe_nchunks = nch;
+      if (upload(&A.pipe_order, order, st) ||
+          cudaMalloc(&A.pipe_state, sizeof(int) * 4) != cudaSuccess ||
+          cudaMalloc(&A.pipe_flag, sizeof(int) * nch) != cudaSuccess) {
+        delete m;
+        return fail(MPK_CUDA_ERROR, "allocation failed");
+      }
+      CKR(cudaMemsetAsync(A.pipe_state, 0, sizeof(int) * 4, st));
+      CKR(cudaMemsetAsync(A.pipe_flag, 0, sizeof(int) * nch, st));
+      CKR(cudaStreamSynchronize(st));
+    }
+    if (getenv("MPK_VERBOSE"))
+      fprintf(stderr, "[mpk] upload n=%lld: pipelined-SpMV plan %.1f ms (%d chunks)\n",
+              (long long)n, host_ms() - t_p0, A.pipe_nchunks);
+  }
   *out = m;
   return MPK_OK;
 }
@@ -1066,7 +1121,8 @@ void mpk_csr_free(mpk_matrix *m) {
                   A.ut_val, A.lt_val, A.sw_y,    A.sw_y2,  A.tick,
                   A.ord_f,  A.ord_b,  A.ord_fa,  A.ord_ba,
                   A.lev_f,  A.lev_b,  A.lev_fa,  A.lev_ba,
-                  A.err,    m->rowflag, m->fscratch};
+                  A.err,    m->rowflag, m->fscratch, A.ord_fp,
+                  A.pipe_order, A.pipe_state, A.pipe_flag};
   if (m->hres) cudaFreeHost(m->hres);
   for (auto &B : m->io) {
     void *q[] = {B.b, B.x, B.stage, B.hist};
@@ -1122,6 +1178,8 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   fa.ord = A.ord_f;
   fa.lev = A.lev_f;
   fa.nlev = A.levels_f;
+  fa.ordp = A.ord_fp;
+  fa.nt = A.nt_fp;
   fa.tick = m->fscratch;
   fa.bad_row = m->fscratch + 2;
   fa.nonfinite = m->fscratch + 3;

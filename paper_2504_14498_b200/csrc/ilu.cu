@@ -110,6 +110,22 @@ __device__ void factor_row(const FactorArgs &a, int i) {
 constexpr int kFactRow = 32;
 constexpr int kFactBatch = 8;
 
+// The wait for pivot row kc is an acquire load of its completion flag (its
+// factors were written before the producer's release store), and everything
+// that does not depend on the pivot row's VALUES -- its extent and the column
+// indices of its upper part, which belong to the static pattern -- is loaded
+// before the wait, so that one L2 round trip (the diagonal and the first
+// batch of upper values, independent loads) separates "row kc is done" from
+// the division: the per-level latency of a deep DAG (cfg4: 6142 levels).
+__device__ __forceinline__ int ld_acquire_i(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i(int *p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ void factor_row_local(const FactorArgs &a, int i) {
   const int lo = a.rp[i], hi = a.rp[i + 1], d = a.dp[i];
   const int len = hi - lo;
@@ -119,29 +135,94 @@ __device__ void factor_row_local(const FactorArgs &a, int i) {
     cols[q] = a.ci[lo + q];
     vals[q] = __ldcg(&a.lu[lo + q]);
   }
-  for (int t = 0; t < d - lo; ++t) {
-    const int kc = cols[t];
-    while (ld_volatile_i(&a.rowflag[kc]) == 0) __nanosleep(32);
-    __threadfence();
-    const int uk = a.dp[kc], kend = a.rp[kc + 1];
-    const double l = ddiv(vals[t], __ldcg(&a.lu[uk]));
-    vals[t] = l;
-    int q = t + 1;
-    for (int s0 = uk + 1; s0 < kend; s0 += kFactBatch) {
-      int cb[kFactBatch];
-      double ub[kFactBatch];
+  const int nl = d - lo;  // L entries
+  int uks[kFactRow], kends[kFactRow];
+  for (int t = 0; t < nl; ++t) {
+    uks[t] = a.dp[cols[t]];
+    kends[t] = a.rp[cols[t] + 1];
+  }
+  // Short rows over short pivot rows (grid stencils): wait for ALL pivot
+  // rows first (one round of independent relaxed flag loads per poll, one
+  // acquire fence), fetch every diagonal and upper part in one round of
+  // independent loads, then eliminate from registers / local memory in the
+  // reference's order.  After the last pivot row is published the row needs
+  // one poll, one fence and one load round trip instead of one of each per
+  // L entry: the per-level latency of a deep DAG.
+  constexpr int kFew = 8;
+  bool few = nl <= kFew;
+  for (int t = 0; t < nl && few; ++t) few = kends[t] - uks[t] - 1 <= kFactBatch;
+  if (few) {
+    int cbf[kFew][kFactBatch];
+    for (int t = 0; t < nl; ++t)
 #pragma unroll
       for (int b = 0; b < kFactBatch; ++b) {
-        const int s = s0 + b;
-        cb[b] = s < kend ? __ldcg(&a.ci[s]) : INT_MAX;
-        ub[b] = s < kend ? __ldcg(&a.lu[s]) : 0.0;
+        const int s = uks[t] + 1 + b;
+        cbf[t][b] = s < kends[t] ? a.ci[s] : INT_MAX;
       }
+    for (;;) {
+      int all = 1;
+      for (int t = 0; t < nl; ++t) all &= ld_volatile_i(&a.rowflag[cols[t]]);
+      if (all) break;
+      __nanosleep(20);
+    }
+    __threadfence();  // acquire: the flags were read relaxed
+    double ukk[kFew], ubf[kFew][kFactBatch];
+    for (int t = 0; t < nl; ++t) {
+      ukk[t] = __ldcg(&a.lu[uks[t]]);
+#pragma unroll
+      for (int b = 0; b < kFactBatch; ++b) {
+        const int s = uks[t] + 1 + b;
+        ubf[t][b] = s < kends[t] ? __ldcg(&a.lu[s]) : 0.0;
+      }
+    }
+    for (int t = 0; t < nl; ++t) {
+      const double l = ddiv(vals[t], ukk[t]);
+      vals[t] = l;
+      int q = t + 1;
+#pragma unroll
+      for (int b = 0; b < kFactBatch; ++b) {
+        const int col = cbf[t][b];
+        if (col == INT_MAX) break;
+        while (q < len && cols[q] < col) ++q;
+        if (q < len && cols[q] == col) vals[q] = dsub(vals[q], dmul(l, ubf[t][b]));
+      }
+    }
+  }
+  for (int t = 0; t < nl && !few; ++t) {
+    const int kc = cols[t];
+    const int uk = uks[t], kend = kends[t];
+    int cb[kFactBatch];
+#pragma unroll
+    for (int b = 0; b < kFactBatch; ++b) {
+      const int s = uk + 1 + b;
+      cb[b] = s < kend ? a.ci[s] : INT_MAX;
+    }
+    while (ld_acquire_i(&a.rowflag[kc]) == 0) __nanosleep(20);
+    const double ukk = __ldcg(&a.lu[uk]);
+    double ub[kFactBatch];
+#pragma unroll
+    for (int b = 0; b < kFactBatch; ++b) {
+      const int s = uk + 1 + b;
+      ub[b] = s < kend ? __ldcg(&a.lu[s]) : 0.0;
+    }
+    const double l = ddiv(vals[t], ukk);
+    vals[t] = l;
+    int q = t + 1;
+    for (int s0 = uk + 1;;) {
 #pragma unroll
       for (int b = 0; b < kFactBatch; ++b) {
         const int col = cb[b];
         if (col == INT_MAX) break;
         while (q < len && cols[q] < col) ++q;
         if (q < len && cols[q] == col) vals[q] = dsub(vals[q], dmul(l, ub[b]));
+      }
+      s0 += kFactBatch;
+      if (s0 >= kend) break;
+#pragma unroll
+      for (int b = 0; b < kFactBatch; ++b) {
+        const int s = s0 + b;
+        cb[b] = s < kend ? a.ci[s] : INT_MAX;
+        ub[b] = s < kend ? __ldcg(&a.lu[s]) : 0.0;
       }
     }
   }
@@ -152,19 +233,19 @@ __device__ void factor_row_local(const FactorArgs &a, int i) {
   }
   if (vals[d - lo] == 0.0) atomicMin(a.bad_row, i);
   if (!fin) atomicOr(a.nonfinite, 1);
-  __threadfence();
-  atomicExch(&a.rowflag[i], 1);
+  st_release_i(&a.rowflag[i], 1);
 }
 
 template <bool CX>
 __global__ void __launch_bounds__(kBlock) factor_kernel(FactorArgs a) {
   const int lane = threadIdx.x & 31;
+  const int nt = a.ord ? a.nt : a.n;
   for (;;) {
     const int base = grab_ticket(a.tick);
-    if (base >= a.n) break;
+    if (base >= nt) break;
     const int t = base + lane;
-    if (t < a.n) {
-      const int row = a.ord ? a.ord[t] : t;
+    const int row = t < nt ? (a.ord ? a.ord[t] : t) : -1;
+    if (row >= 0) {
       if (!CX && a.rp[row + 1] - a.rp[row] <= kFactRow)
         factor_row_local(a, row);
       else
@@ -1625,12 +1706,28 @@ void launch_factor(const FactorArgs &a, bool cx, cudaStream_t st) {
       factor_smem_kernel<false><<<1, kSmemThreads, 0, st>>>(a);
     return;
   }
-  FactorArgs b = a;  // multi-CTA sync-free kernel: natural row order
-  b.ord = nullptr;
-  long long warps = (a.n + 31) / 32;
+  // Multi-CTA sync-free kernel.  Ticket t -> row: natural order (t), or the
+  // level order of the L DAG (a.ord).  In natural order the 32 rows of a warp
+  // are usually chained (a grid stencil's row i needs row i-1), so the lanes
+  // of one warp wait on each other and every DAG level costs a divergent
+  // spin hand-off (cfg4: 6142 levels x 16 us).  In level order a warp's rows
+  // are independent and only wait on rows of lower levels, held by other
+  // (resident, lower-ticket) warps -- every level is padded to a multiple of
+  // 32 tickets (FactorArgs::ordp), else the warp straddling a level boundary
+  // would chain its lanes again.  Deep DAGs take the level order; shallow
+  // ones (random patterns: tens of levels, rows of a level scattered over
+  // the matrix) keep the natural order and its coalesced row reads.
+  // MPK_FACTOR_ORDER = natural | level overrides.
+  FactorArgs b = a;
+  bool level = a.ordp != nullptr;
+  if (const char *e = getenv("MPK_FACTOR_ORDER")) level = a.ordp != nullptr && e[0] == 'l';
+  b.ord = level ? a.ordp : nullptr;
+  long long warps = ((level ? a.nt : a.n) + 31) / 32;
   long long blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks < 1) blocks = 1;
-  if (blocks > sm_count() * 6) blocks = sm_count() * 6;
+  int per_sm = level ? 1 : 6;  // level order: fewer pollers, shorter hand-off (measured)
+  if (const char *e = getenv("MPK_FACTOR_BLOCKS")) per_sm = atoi(e) > 0 ? atoi(e) : per_sm;
+  if (blocks > (long long)sm_count() * per_sm) blocks = (long long)sm_count() * per_sm;
   if (cx)
     factor_kernel<true><<<(int)blocks, kBlock, 0, st>>>(b);
   else

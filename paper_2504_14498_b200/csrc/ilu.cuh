@@ -41,7 +41,16 @@ struct SweepArgs {
   int *tick;       // [0] ticket, [1] exit counter
   int *err;        // set to 1 on a non-finite z (NumericBreakdownError)
   const int *done; // solver done flag (skip when set), may be null
+  // sweep-pipelined SpMV (units.cu pspmv_kernel): every CTA of the backward
+  // phase counts itself in here once it is running (null: unused)
+  int *started = nullptr;
 };
+
+// Host-side hook of the pipelined SpMV: when set, a sweep plan that runs its
+// two phases as two launches records this event between them (the consumer
+// kernel is released when the forward phase is done, next to the backward
+// launch).  Null: no event.  Only the shuffle-wavefront plan honours it.
+inline thread_local cudaEvent_t tl_sweep_mid = nullptr;
 
 // Level-ordered copy of one sweep phase ("sweep matrix"): position r in
 // level order holds row row[r] whose entries are col/val[ptr[r]..ptr[r+1])
@@ -165,6 +174,7 @@ bool build_ssweep(SSweep &w, int n, bool cx, const int *rp, const int *ci, const
 void gather_ssweep(const double *lu, const SSweep &w, cudaStream_t st);
 void launch_ssweep(const SweepArgs &a, const SSweep &w, cudaStream_t st);
 void free_ssweep(SSweep &w);
+int ssweep_bwd_ctas(const SSweep &w);
 void launch_rsweep(const SweepArgs &a, const RSweep &p, bool cx, bool adjoint,
                    cudaStream_t st);
 void gather_rsweep(const double *lu, const RSweep &p, bool cx, cudaStream_t st);
@@ -191,6 +201,11 @@ struct FactorArgs {
   const int *ord;  // level order of the L DAG (single-CTA path)
   const int *lev;  // level pointers into ord
   int nlev;
+  // ticket order of the multi-CTA kernel for deep DAGs: the level order with
+  // every level padded (-1) to a multiple of 32 tickets, so that the 32 rows
+  // a warp claims always belong to ONE level and never wait on each other
+  const int *ordp = nullptr;
+  int nt = 0;      // padded ticket count
   int *tick;       // [0] ticket, [1] exit counter
   int *bad_row;    // atomicMin of zero-pivot rows (init INT_MAX)
   int *nonfinite;  // set if any factor is non-finite

@@ -78,6 +78,17 @@ struct DMat {
   int *ord_f = nullptr, *ord_b = nullptr, *ord_fa = nullptr, *ord_ba = nullptr;
   int *lev_f = nullptr, *lev_b = nullptr, *lev_fa = nullptr, *lev_ba = nullptr;
   int levels_f = 0, levels_b = 0, levels_fa = 0, levels_ba = 0;
+  // sweep-pipelined SpMV (units.cu pspmv_kernel; large stencil patterns
+  // whose sweeps run on the shuffle-wavefront plan): 32-row chunks sorted by
+  // the backward-DAG level at which their inputs are complete, claim /
+  // started counters and per-chunk done flags
+  int *pipe_order = nullptr;
+  int pipe_nchunks = 0;
+  int *pipe_state = nullptr;  // [0] claimed chunks, [1] backward CTAs running
+  int *pipe_flag = nullptr;   // [pipe_nchunks]
+  // factorization ticket order of deep DAGs (FactorArgs::ordp), else null
+  int *ord_fp = nullptr;
+  int nt_fp = 0;
   // level-ordered sweep matrices (single-CTA path, small n)
   SweepMats smat, smat_adj;
   bool smat_built = false, smat_adj_built = false;
@@ -144,6 +155,14 @@ int run_solve(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
 // unit kernels used by the C-ABI (parity tests)
 int unit_spmv(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
               double *d_y, cudaStream_t st);
+constexpr int kPipeRow = 12;  // longest row a pipeline plan accepts
+// y (planar MC, K planes of ld) = A z for the chunks whose inputs the running
+// backward sweep has already produced (z: F vector, sentinel until written);
+// see units.cu.  Launches nothing and returns false when the matrix has no
+// pipeline plan.
+void launch_pipe_reset(DMat &A, cudaStream_t st);
+bool launch_pspmv(DMat &A, int k, const double *z, double *y, const int *done,
+                  cudaStream_t st);
 int unit_spmv_full(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
                    double *d_y, const int *done, cudaStream_t st);
 int unit_reduce(int k, bool cx, int op, long long n, const double *d_x,

@@ -187,6 +187,12 @@ struct Solver : PlanBase {
   double *seqbuf = nullptr;  // twin-mode element terms [slot][i][2K]
   // MC-valued matrix (p.full_a): A x / A^H x of the next row kernel
   double *prebuf = nullptr, *prebuf_adj = nullptr;
+  // sweep-pipelined SpMV (units.cu pspmv_kernel): the SpMV of a sweep's
+  // output runs beside the sweep's backward phase on the SMs it leaves idle
+  bool pipe_on = false;
+  DA dap;  // da + the pipeline's result buffer and chunk flags
+  cudaEvent_t evp_mid = nullptr, evp_join = nullptr;
+  int *cur_started = nullptr;
   State *hp = nullptr;  // pinned host staging of the device State (x2)
   int *hpi = nullptr;
 
@@ -234,6 +240,19 @@ struct Solver : PlanBase {
       da.pre = prebuf = mc();
       if (p.method == kBiCG) da.pre_adj = prebuf_adj = mc();
     }
+    dap = da;
+    {
+      const char *e = getenv("MPK_PIPE");
+      pipe_on = A.pipe_order && !CX && p.precond_ilu == 1 && !p.ex && !p.full_a &&
+                p.method != kBiCG && A.smat.ss.on && ssweep_bwd_ctas(A.smat.ss) > 0 &&
+                !(e && e[0] == '0');
+    }
+    if (pipe_on) {
+      dap.pre = prebuf = mc();
+      dap.pflag = A.pipe_flag;
+      cudaEventCreateWithFlags(&evp_mid, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&evp_join, cudaEventDisableTiming);
+    }
     S = (State *)dalloc(sizeof(State));
     part = (double *)dalloc(sizeof(double) * 6 * kMaxGrid * 8);
     hist_cap = p.hist_cap > 0 ? p.hist_cap : 1;
@@ -269,6 +288,8 @@ struct Solver : PlanBase {
     if (st2) cudaStreamDestroy(st2);
     if (st3) cudaStreamDestroy(st3);
     if (evj3) cudaEventDestroy(evj3);
+    if (evp_mid) cudaEventDestroy(evp_mid);
+    if (evp_join) cudaEventDestroy(evp_join);
     if (hp) cudaFreeHost(hp);
     if (hpi) cudaFreeHost(hpi);
     for (void *q : allocs) cudaFree(q);
@@ -325,6 +346,26 @@ struct Solver : PlanBase {
       launch_sweep_reset(y, z, n, CX, after_loop ? nullptr : done, st);
     }
     sweep_on(st, in_re, in_im, y, z, adjoint, which, after_loop);
+  }
+  // ILU(0)-mixed apply whose output z the next row kernel multiplies by A:
+  // with a pipeline plan, A z is formed chunk by chunk beside the backward
+  // phase (st3, released between the two phases of the sweep) into
+  // `prebuf`; the row kernel then loads the flagged chunks (DA::pflag).
+  void sweep_spmv(const double *in_re, const double *in_im, double *y, double *z) {
+    if (!pipe_on) {
+      sweep(in_re, in_im, y, z, false, 0);
+      return;
+    }
+    launch_pipe_reset(A, st);
+    tl_sweep_mid = evp_mid;
+    cur_started = A.pipe_state + 1;
+    sweep(in_re, in_im, y, z, false, 0);
+    cur_started = nullptr;
+    tl_sweep_mid = nullptr;
+    cudaStreamWaitEvent(st3, evp_mid, 0);
+    launch_pspmv(A, K, z, prebuf, done, st3);
+    cudaEventRecord(evp_join, st3);
+    cudaStreamWaitEvent(st, evp_join, 0);
   }
   // z = U^-1 L^-1 in at working precision (real; planar K-component)
   void mc_sweep(const double *in, double *z, int which, bool after_loop,
@@ -398,6 +439,7 @@ struct Solver : PlanBase {
     a.tick = A.tick + 2 * which;
     a.err = A.err;
     a.done = after_loop ? nullptr : done;
+    a.started = cur_started;
     do_sweep(A, a, adjoint, s_);
   }
   const double *head_re(const double *v) const { return v; }
@@ -460,7 +502,7 @@ struct Solver : PlanBase {
     const FVt PH = fvv(phat), SH = fvv(shat), Y = fvv(A.sw_y);
     State *Sd = S;
     double *H = hist;
-    const DA a = da;
+    const DA a = pipe_on ? dap : da;
     const long long L = ld;
     const int np_ = nopre;
     // F5+F1: [end of the previous iteration, deferred: rho_old = rho,
@@ -529,7 +571,7 @@ struct Solver : PlanBase {
                         Y.set_sent(i);
                         PH.set_sent(i);
                       });
-    sweep(head_re(pp), head_im(pp), A.sw_y, phat, false, 0);
+    sweep_spmv(head_re(pp), head_im(pp), A.sw_y, phat);
     // K4: v = A phat ; sigma = hdot(rt0, v)
     const double *phc = phat;
     pre_spmv(phat, !nopre);
@@ -578,7 +620,7 @@ struct Solver : PlanBase {
             if (check_nrm<K>(S_, H, ss) && S_->converged) S_->half_exit = 1;
           }
         });
-    sweep(head_re(s), head_im(s), A.sw_y, shat, false, 0);
+    sweep_spmv(head_re(s), head_im(s), A.sw_y, shat);
     // K7: t = A shat ; tt = hdot(t,t), ts = hdot(t,s)
     const double *shc = shat;
     pre_spmv(shat, !nopre);
@@ -665,7 +707,7 @@ struct Solver : PlanBase {
     const FVt PH = fvv(phat), UH = fvv(uhat), Y = fvv(A.sw_y);
     State *Sd = S;
     double *H = hist;
-    const DA a = da;
+    const DA a = pipe_on ? dap : da;
     const long long L = ld;
     const int np_ = nopre;
     double *WH = whead;
@@ -704,7 +746,7 @@ struct Solver : PlanBase {
                         Y.set_sent(i);
                         PH.set_sent(i);
                       });
-    sweep(head_re(pp), head_im(pp), A.sw_y, phat, false, 0);
+    sweep_spmv(head_re(pp), head_im(pp), A.sw_y, phat);
     const double *phc = phat;
     pre_spmv(phat, !nopre);
     rows<K, CX, 1, 0>(n, done, part, st,
@@ -750,7 +792,7 @@ struct Solver : PlanBase {
                         Y.set_sent(i);
                         UH.set_sent(i);
                       });
-    sweep(whead, CX ? whead + ld : nullptr, A.sw_y, uhat, false, 0);
+    sweep_spmv(whead, CX ? whead + ld : nullptr, A.sw_y, uhat);
     // qhat = A uhat ; x += alpha uhat ; r -= alpha qhat ; norm2(r), rho
     const double *uhc = uhat;
     pre_spmv(uhat, !nopre);
@@ -805,7 +847,7 @@ struct Solver : PlanBase {
     const FVt MPv = fvv(Mp), MTv = fvv(Mt), Y = fvv(A.sw_y);
     State *Sd = S;
     double *H = hist;
-    const DA a = da;
+    const DA a = pipe_on ? dap : da;
     const long long L = ld;
     const int np_ = nopre;
     // K2: w = Bt + beta Bp (end of previous iteration), p = r + beta (p - u)
@@ -833,7 +875,7 @@ struct Solver : PlanBase {
                         Y.set_sent(i);
                         MPv.set_sent(i);
                       });
-    sweep(head_re(pp), head_im(pp), A.sw_y, Mp, false, 0);
+    sweep_spmv(head_re(pp), head_im(pp), A.sw_y, Mp);
     const double *mpc = Mp;
     pre_spmv(Mp, !nopre);
     rows<K, CX, 1, 0>(n, done, part, st,
@@ -880,7 +922,7 @@ struct Solver : PlanBase {
                         Y.set_sent(i);
                         MTv.set_sent(i);
                       });
-    sweep(head_re(t), head_im(t), A.sw_y, Mt, false, 0);
+    sweep_spmv(head_re(t), head_im(t), A.sw_y, Mt);
     // K7: Bt = A Mt ; btbt, btt (+ yy, ybt, bty, yt when it > 1)
     const double *mtc = Mt;
     pre_spmv(Mt, !nopre);

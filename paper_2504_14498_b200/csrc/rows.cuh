@@ -19,6 +19,10 @@ struct DA {
   // full-precision kernel (units.cu spmv_full_kernel) into these planar MC
   // vectors just before the row kernel; null otherwise
   const double *pre = nullptr, *pre_adj = nullptr;
+  // sweep-pipelined SpMV: `pre` holds A x only for the 32-row chunks whose
+  // flag is set (rows the pipeline kernel finished while the sweep ran);
+  // null: every row of `pre` is valid
+  const int *pflag = nullptr;
 };
 
 template <int K, bool CX>
@@ -85,7 +89,7 @@ template <int K, bool CX>
 __device__ __forceinline__ void spmv_fv(const DA &A, int i, const double *x,
                                         long long ld, int mc, double (&yr)[K],
                                         double (&yi)[K]) {
-  if (A.pre)
+  if (A.pre && (!A.pflag || A.pflag[i >> 5]))
     load_pre<K, CX>(A.pre, ld, i, yr, yi);
   else if (mc)
     spmv_row<K, CX, false, false>(A, i, x, ld, yr, yi);

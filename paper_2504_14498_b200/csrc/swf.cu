@@ -705,6 +705,7 @@ __global__ void __launch_bounds__(64, 1) swf_kernel(SweepArgs a, SPhase P) {
       return;
     }
   }
+  if (!FWD && a.started && threadIdx.x == 0) atomicAdd(a.started, 1);
   extern __shared__ __align__(128) unsigned char sm[];
   const int w = threadIdx.x >> 5, j = threadIdx.x & 31;
   const int rank = clustered ? (int)cluster_rank() : 0;
@@ -1143,7 +1144,14 @@ void launch_ssweep(const SweepArgs &a, const SSweep &w, cudaStream_t st) {
     else if (grid > sm_count())
       grid = sm_count();
     launch_phase(a, Q, w.W, grid, w.smem, st);
+    if (P == &w.f && tl_sweep_mid) cudaEventRecord(tl_sweep_mid, st);
   }
+}
+
+// CTAs of the backward phase (all resident at once in cluster mode)
+int ssweep_bwd_ctas(const SSweep &w) {
+  if (!w.on || w.b.cl <= 1) return 0;
+  return (w.b.ngroups + w.b.cl - 1) / w.b.cl * w.b.cl;
 }
 
 }  // namespace mpk

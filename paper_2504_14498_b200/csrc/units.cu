@@ -167,6 +167,155 @@ int unit_spmv_full(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
   return 3;
 }
 
+// ---------------------------------------------------------------------
+// Sweep-pipelined SpMV.  In BiCGSTAB / CGS / GPBiCG every SpMV multiplies
+// the output z of an ILU(0)-mixed apply (solvers.py:303-304, 311-312).  On
+// a large stencil pattern the apply is the shuffle-wavefront sweep
+// (swf.cu), a latency-bound kernel on 64 of the 148 SMs; this kernel runs
+// beside its backward phase on the other SMs and forms y_i = sum_j a_ij z_j
+// for each 32-row chunk as soon as the sweep has published the chunk's
+// inputs (z is sentinel-filled before the sweep, so "published" is visible
+// in the value itself).  Per row the operations and their order are those
+// of spmv_row (ascending columns, exact product + MC add), so y is the SpMV
+// bit for bit; the fused row kernel that follows loads y for the chunks
+// flagged here and computes the rest itself.
+//  * Chunks are claimed in the order their inputs become complete (host:
+//    max backward-DAG level over the rows' columns), through one counter.
+//  * No deadlock: a block first waits -- for a bounded time -- until every
+//    CTA of the backward phase is running (they count themselves in), and
+//    exits without claiming anything otherwise; once the sweep is resident
+//    it completes on its own, so every wait on z ends.  The 88 KB of
+//    dynamic shared memory only keep these blocks off the SMs of the sweep
+//    CTAs (which own 142 KB each), whose single compute warp must not
+//    share issue slots.
+// ---------------------------------------------------------------------
+struct PipeArgs {
+  int n, nchunks, need_started;
+  const int *rp, *ci;
+  const double *val;
+  const double *z;
+  double *y;
+  long long ld;
+  const int *order;
+  int *state, *flag;
+  const int *done;
+};
+constexpr int kPipeThreads = 512;
+constexpr size_t kPipeSmem = 88 * 1024;  // see above
+
+__global__ void pipe_delay_kernel() { __nanosleep(4000); }
+
+template <int K>
+__global__ void __launch_bounds__(kPipeThreads, 2) pspmv_kernel(PipeArgs a) {
+  if (a.done && *(volatile const int *)a.done) return;
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    int go = 0;
+    for (int t = 0; t < 1500 && !go; ++t) {  // <= ~0.3 ms
+      go = *(volatile int *)(a.state + 1) >= a.need_started;
+      if (!go) __nanosleep(200);
+    }
+    s_go = go;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const int lane = threadIdx.x & 31;
+  const int sent_hi = (int)(kSentBits >> 32);
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(a.state, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= a.nchunks) break;
+    const int chunk = a.order[c];
+    const int i = chunk * 32 + lane;
+    if (i < a.n) {
+      const int lo = a.rp[i], len = a.rp[i + 1] - lo;
+      int cj[kPipeRow];
+      double xv[kPipeRow];
+#pragma unroll
+      for (int q = 0; q < kPipeRow; ++q) cj[q] = q < len ? a.ci[lo + q] : 0;
+      for (;;) {
+        bool ready = true;
+#pragma unroll
+        for (int q = 0; q < kPipeRow; ++q) {
+          if (q < len) {
+            xv[q] = ld_relaxed(a.z + cj[q]);
+            ready = ready && (__double2hiint(xv[q]) != sent_hi);
+          }
+        }
+        if (ready) break;
+        __nanosleep(100);
+      }
+      double yr[K];
+#pragma unroll
+      for (int cc = 0; cc < K; ++cc) yr[cc] = 0.0;
+#pragma unroll
+      for (int q = 0; q < kPipeRow; ++q) {
+        if (q < len) {  // spmv_row<K, false, true, false>: ascending columns
+          double h, l;
+          mul_ff2(a.val[lo + q], xv[q], h, l);
+          add2<K>(yr, h, l, yr);
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < K; ++cc) a.y[cc * a.ld + i] = yr[cc];
+    }
+    __syncwarp();
+    if (lane == 0) a.flag[chunk] = 1;
+  }
+}
+
+__global__ void pipe_reset_kernel(int *state, int *flag, int nchunks) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < 4) state[t] = 0;
+  for (int c = t; c < nchunks; c += gridDim.x * blockDim.x) flag[c] = 0;
+}
+
+void launch_pipe_reset(DMat &A, cudaStream_t st) {
+  ++tl_launches;
+  pipe_reset_kernel<<<sm_count(), 256, 0, st>>>(A.pipe_state, A.pipe_flag, A.pipe_nchunks);
+}
+
+template <int K>
+static void launch_pspmv_k(const PipeArgs &a, int grid, cudaStream_t st) {
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(pspmv_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kPipeSmem);
+    once = true;
+  }
+  pspmv_kernel<K><<<grid, kPipeThreads, kPipeSmem, st>>>(a);
+}
+
+bool launch_pspmv(DMat &A, int k, const double *z, double *y, const int *done,
+                  cudaStream_t st) {
+  const int need = ssweep_bwd_ctas(A.smat.ss);
+  if (!A.pipe_order || A.cx || need <= 0 || need >= sm_count()) return false;
+  PipeArgs a{};
+  a.n = A.n;
+  a.nchunks = A.pipe_nchunks;
+  a.need_started = need;
+  a.rp = A.rp;
+  a.ci = A.ci;
+  a.val = A.val;
+  a.z = z;
+  a.y = y;
+  a.ld = plane_ld(A.n);
+  a.order = A.pipe_order;
+  a.state = A.pipe_state;
+  a.flag = A.pipe_flag;
+  a.done = done;
+  const int grid = (sm_count() - need) * 2;
+  tl_launches += 2;
+  pipe_delay_kernel<<<1, 1, 0, st>>>();
+  switch (k) {
+    case 2: launch_pspmv_k<2>(a, grid, st); break;
+    case 3: launch_pspmv_k<3>(a, grid, st); break;
+    default: launch_pspmv_k<4>(a, grid, st); break;
+  }
+  return true;
+}
+
 template <int K, bool CX>
 __global__ void unit_fin_kernel(const double *part, int G, int op,
                                 double *out) {

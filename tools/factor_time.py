@@ -6,7 +6,7 @@ from paper_2504_14498_b200 import _lib, problems
 L = _lib.lib(); ctx = _lib.context(0)
 L.mpk_ilu0_factor.restype = ctypes.c_int
 for name in sys.argv[1:] or ["cfg1", "cfg2", "cfg4"]:
-    p = problems.CONFIGS[name]()
+    p = (problems.CONFIGS[name](0) if name == "cfg5" else problems.CONFIGS[name]())
     h = ctypes.c_void_p()
     vim = None if p.val_im is None else _lib.f64(p.val_im)
     _lib.check(L.mpk_csr_upload(ctx, ctypes.c_int64(p.n), ctypes.c_int64(p.nnz), _lib.dptr(_lib.i64(p.row_ptr)),
