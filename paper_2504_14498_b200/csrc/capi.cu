@@ -1070,7 +1070,8 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
   // stencil pattern on the shuffle-wavefront plan, the 32-row chunks of A
   // sorted by the backward-DAG level at which all their columns' z values
   // exist (counting sort over the levels).
-  if (A.smat.ss.on && !A.cx && n >= (1 << 18) && ssweep_bwd_ctas(A.smat.ss) > 0 &&
+  if (A.smat.ss.on && !A.cx && n >= env_int("MPK_PIPE_MIN_N", 1 << 18) &&
+      ssweep_bwd_ctas(A.smat.ss) > 0 &&
       env_int("MPK_PIPE", 1) != 0) {
     const double t_p0 = host_ms();
     const int *rp = A.h_rp.data(), *ci = A.h_ci.data();
@@ -1081,18 +1082,24 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
       for (int l = 0; l < A.levels_b; ++l)
         for (int q = pb[l]; q < pb[l + 1]; ++q) levb[ob[q]] = l;
       const int nch = (int)((n + 31) / 32);
-      std::vector<int> ready(nch, 0), cnt(A.levels_b + 1, 0), order(nch);
+      std::vector<int> ready(nch, 0), cnt(A.levels_b + 1, 0), order(nch), last(nch, 0);
       for (int c = 0; c < nch; ++c) {
         const int64_t i1 = std::min<int64_t>(n, (int64_t)c * 32 + 32);
-        int r = 0;
-        for (int q = rp[(int64_t)c * 32]; q < rp[i1]; ++q) r = std::max(r, levb[ci[q]]);
+        int r = -1, lc = 0;
+        for (int q = rp[(int64_t)c * 32]; q < rp[i1]; ++q)
+          if (levb[ci[q]] > r) {
+            r = levb[ci[q]];
+            lc = ci[q];
+          }
+        if (r < 0) r = 0;
         ready[c] = r;
+        last[c] = lc;
         ++cnt[r + 1];
       }
       for (int l = 0; l < A.levels_b; ++l) cnt[l + 1] += cnt[l];
       for (int c = 0; c < nch; ++c) order[cnt[ready[c]]++] = c;
       A.pipe_nchunks = nch;
-      if (upload(&A.pipe_order, order, st) ||
+      if (upload(&A.pipe_order, order, st) || upload(&A.pipe_last, last, st) ||
           cudaMalloc(&A.pipe_state, sizeof(int) * 4) != cudaSuccess ||
           cudaMalloc(&A.pipe_flag, sizeof(int) * nch) != cudaSuccess) {
         delete m;
@@ -1122,7 +1129,7 @@ void mpk_csr_free(mpk_matrix *m) {
                   A.ord_f,  A.ord_b,  A.ord_fa,  A.ord_ba,
                   A.lev_f,  A.lev_b,  A.lev_fa,  A.lev_ba,
                   A.err,    m->rowflag, m->fscratch, A.ord_fp,
-                  A.pipe_order, A.pipe_state, A.pipe_flag};
+                  A.pipe_order, A.pipe_last, A.pipe_state, A.pipe_flag};
   if (m->hres) cudaFreeHost(m->hres);
   for (auto &B : m->io) {
     void *q[] = {B.b, B.x, B.stage, B.hist};

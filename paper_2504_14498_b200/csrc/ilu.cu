@@ -141,54 +141,7 @@ __device__ void factor_row_local(const FactorArgs &a, int i) {
     uks[t] = a.dp[cols[t]];
     kends[t] = a.rp[cols[t] + 1];
   }
-  // Short rows over short pivot rows (grid stencils): wait for ALL pivot
-  // rows first (one round of independent relaxed flag loads per poll, one
-  // acquire fence), fetch every diagonal and upper part in one round of
-  // independent loads, then eliminate from registers / local memory in the
-  // reference's order.  After the last pivot row is published the row needs
-  // one poll, one fence and one load round trip instead of one of each per
-  // L entry: the per-level latency of a deep DAG.
-  constexpr int kFew = 8;
-  bool few = nl <= kFew;
-  for (int t = 0; t < nl && few; ++t) few = kends[t] - uks[t] - 1 <= kFactBatch;
-  if (few) {
-    int cbf[kFew][kFactBatch];
-    for (int t = 0; t < nl; ++t)
-#pragma unroll
-      for (int b = 0; b < kFactBatch; ++b) {
-        const int s = uks[t] + 1 + b;
-        cbf[t][b] = s < kends[t] ? a.ci[s] : INT_MAX;
-      }
-    for (;;) {
-      int all = 1;
-      for (int t = 0; t < nl; ++t) all &= ld_volatile_i(&a.rowflag[cols[t]]);
-      if (all) break;
-      __nanosleep(20);
-    }
-    __threadfence();  // acquire: the flags were read relaxed
-    double ukk[kFew], ubf[kFew][kFactBatch];
-    for (int t = 0; t < nl; ++t) {
-      ukk[t] = __ldcg(&a.lu[uks[t]]);
-#pragma unroll
-      for (int b = 0; b < kFactBatch; ++b) {
-        const int s = uks[t] + 1 + b;
-        ubf[t][b] = s < kends[t] ? __ldcg(&a.lu[s]) : 0.0;
-      }
-    }
-    for (int t = 0; t < nl; ++t) {
-      const double l = ddiv(vals[t], ukk[t]);
-      vals[t] = l;
-      int q = t + 1;
-#pragma unroll
-      for (int b = 0; b < kFactBatch; ++b) {
-        const int col = cbf[t][b];
-        if (col == INT_MAX) break;
-        while (q < len && cols[q] < col) ++q;
-        if (q < len && cols[q] == col) vals[q] = dsub(vals[q], dmul(l, ubf[t][b]));
-      }
-    }
-  }
-  for (int t = 0; t < nl && !few; ++t) {
+  for (int t = 0; t < nl; ++t) {
     const int kc = cols[t];
     const int uk = uks[t], kend = kends[t];
     int cb[kFactBatch];

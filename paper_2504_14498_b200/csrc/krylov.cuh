@@ -83,6 +83,7 @@ struct DMat {
   // the backward-DAG level at which their inputs are complete, claim /
   // started counters and per-chunk done flags
   int *pipe_order = nullptr;
+  int *pipe_last = nullptr;   // per chunk: the column whose z value comes last
   int pipe_nchunks = 0;
   int *pipe_state = nullptr;  // [0] claimed chunks, [1] backward CTAs running
   int *pipe_flag = nullptr;   // [pipe_nchunks]

@@ -49,6 +49,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -822,13 +824,45 @@ constexpr Pattern kPat[] = {
 };
 constexpr int kNPat = 4;
 
+// Row ranges of the host analysis on a few threads (the passes below read the
+// pattern only; each thread reduces into its own slot).
+static int par_threads(int n) {
+  if (n < (1 << 16)) return 1;
+  const unsigned hw = std::thread::hardware_concurrency();
+  return (int)std::min<unsigned>(16u, hw ? hw : 1u);
+}
+template <class F>
+static void par_rows(int n, int T, F f) {
+  if (T <= 1) {
+    f(0, n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T);
+  const long long per = ((long long)n + T - 1) / T;
+  for (int t = 0; t < T; ++t) {
+    const int lo = (int)std::min<long long>(n, per * t), hi = (int)std::min<long long>(n, per * (t + 1));
+    th.emplace_back([=] { f(lo, hi, t); });
+  }
+  for (auto &x : th) x.join();
+}
+
 template <class Deps>
 static bool analyse_phase(SPhase &ph, int n, bool fwd, Deps deps, long long &cost) {
+  const int T = par_threads(n);
   long long D = 0;
-  for (int p = 0; p < n; ++p)
-    deps(p, [&](int pq, int) {
-      if (p - pq > D) D = p - pq;
+  {
+    std::vector<long long> dmax(T, 0);
+    par_rows(n, T, [&](int lo, int hi, int t) {
+      long long d = 0;
+      for (int p = lo; p < hi; ++p)
+        deps(p, [&](int pq, int) {
+          if (p - pq > d) d = p - pq;
+        });
+      dmax[t] = d;
     });
+    for (long long d : dmax) D = std::max(D, d);
+  }
   if (D < 2) return false;
   bool found = false;
   cost = LLONG_MAX;
@@ -839,25 +873,41 @@ static bool analyse_phase(SPhase &ph, int n, bool fwd, Deps deps, long long &cos
     // lag: a previous-line dependency at posq needs posq - pos + lag >= 1
     long long lag = 1;
     bool ok = true;
-    for (int p = 0; p < n && ok; ++p) {
-      const long long l = p / Lc, pos = p % Lc;
-      deps(p, [&](int pq, int) {
-        const long long lq = pq / Lc, posq = pq % Lc;
-        if (lq == l) return;
-        if (lq != l - 1) {
-          ok = false;
-          return;
+    {
+      std::vector<long long> lags(T, 1);
+      std::atomic<bool> okf{true};
+      par_rows(n, T, [&](int lo, int hi, int t) {
+        long long lg = 1;
+        bool okt = true;
+        for (int p = lo; p < hi && okt; ++p) {
+          const long long l = p / Lc, pos = p % Lc;
+          deps(p, [&](int pq, int) {
+            const long long lq = pq / Lc, posq = pq % Lc;
+            if (lq == l) return;
+            if (lq != l - 1) {
+              okt = false;
+              return;
+            }
+            if (posq - pos + 1 > lg) lg = posq - pos + 1;
+          });
+          if ((p & 4095) == 0 && !okf.load(std::memory_order_relaxed)) break;
         }
-        if (posq - pos + 1 > lag) lag = posq - pos + 1;
+        lags[t] = lg;
+        if (!okt) okf.store(false, std::memory_order_relaxed);
       });
+      ok = okf.load();
+      for (long long lg : lags) lag = std::max(lag, lg);
     }
     if (!ok || lag > 3) continue;
     // the entries of every row must follow one pattern's key list
     int pat = -1;
     for (int k = 0; k < kNPat && pat < 0; ++k) {
       const Pattern &P = kPat[k];
+      std::atomic<bool> goodf{true};
+      par_rows(n, T, [&](int lo_, int hi_, int) {
       bool good = true;
-      for (int p = 0; p < n && good; ++p) {
+      for (int p = lo_; p < hi_ && good; ++p) {
+        if ((p & 4095) == 0 && !goodf.load(std::memory_order_relaxed)) break;
         const long long l = p / Lc, pos = p % Lc;
         int e = 0;  // next key of the pattern to match
         bool used[4] = {false, false, false, false};
@@ -888,7 +938,9 @@ static bool analyse_phase(SPhase &ph, int n, bool fwd, Deps deps, long long &cos
           if (!inactive) good = false;
         }
       }
-      if (good) pat = k;
+      if (!good) goodf.store(false, std::memory_order_relaxed);
+      });
+      if (goodf.load()) pat = k;
     }
     if (pat < 0) continue;
     const long long ng = (nl + 31) / 32;
@@ -923,23 +975,25 @@ static bool build_phase(SPhase &ph, int n, Deps deps, Div div, cudaStream_t st) 
   ph.rhs16 = (ph.Lc % 2 == 0 && ph.lag % 2 == 0 && (fwd || n % 2 == 0)) ? 1 : 0;
   std::vector<int> esrc((size_t)ph.nslots, -1), dsrc((size_t)ph.ndslots, -1);
   const long long Lc = ph.Lc, lag = ph.lag;
-  for (int p = 0; p < n; ++p) {
-    const long long l = p / Lc, pos = p % Lc;
-    const long long g = l / 32, j = l % 32;
-    const long long s = pos + lag * j;
-    const long long gs = g * ph.S + s;
-    int e = 0;
-    deps(p, [&](int pq, int lu_idx) {
-      const long long lq = pq / Lc, posq = pq % Lc;
-      const long long dl = l - lq;
-      const long long ds = dl ? pos - posq + lag : pos - posq;
-      const int key = (int)(4 * dl + ds - 1);
-      while (P.keys[e] != key) ++e;  // analysed: always found
-      esrc[(size_t)((gs * NK + e) * 32 + j)] = lu_idx;
-      ++e;
-    });
-    if (!fwd) dsrc[(size_t)(gs * 32 + j)] = div(p);
-  }
+  par_rows(n, par_threads(n), [&](int lo_, int hi_, int) {  // rows own distinct slots
+    for (int p = lo_; p < hi_; ++p) {
+      const long long l = p / Lc, pos = p % Lc;
+      const long long g = l / 32, j = l % 32;
+      const long long s = pos + lag * j;
+      const long long gs = g * ph.S + s;
+      int e = 0;
+      deps(p, [&](int pq, int lu_idx) {
+        const long long lq = pq / Lc, posq = pq % Lc;
+        const long long dl = l - lq;
+        const long long ds = dl ? pos - posq + lag : pos - posq;
+        const int key = (int)(4 * dl + ds - 1);
+        while (P.keys[e] != key) ++e;  // analysed: always found
+        esrc[(size_t)((gs * NK + e) * 32 + j)] = lu_idx;
+        ++e;
+      });
+      if (!fwd) dsrc[(size_t)(gs * 32 + j)] = div(p);
+    }
+  });
   auto up = [&](void **d, const void *h, size_t bytes) {
     if (cudaMalloc(d, bytes < 16 ? 16 : bytes) != cudaSuccess) return false;
     return cudaMemcpyAsync(*d, h, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;

@@ -180,7 +180,9 @@ int unit_spmv_full(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,
 // bit for bit; the fused row kernel that follows loads y for the chunks
 // flagged here and computes the rest itself.
 //  * Chunks are claimed in the order their inputs become complete (host:
-//    max backward-DAG level over the rows' columns), through one counter.
+//    max backward-DAG level over the rows' columns), through one counter;
+//    a warp waits on ONE value (the chunk's last-produced column) with one
+//    lane, so the ~2700 waiting warps cost L2 one load each per poll.
 //  * No deadlock: a block first waits -- for a bounded time -- until every
 //    CTA of the backward phase is running (they count themselves in), and
 //    exits without claiming anything otherwise; once the sweep is resident
@@ -196,7 +198,7 @@ struct PipeArgs {
   const double *z;
   double *y;
   long long ld;
-  const int *order;
+  const int *order, *last;
   int *state, *flag;
   const int *done;
 };
@@ -227,6 +229,14 @@ __global__ void __launch_bounds__(kPipeThreads, 2) pspmv_kernel(PipeArgs a) {
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= a.nchunks) break;
     const int chunk = a.order[c];
+    // gate: one lane polls the value that the sweep produces last for this
+    // chunk (host: highest backward level among its columns); the lanes'
+    // own loads below re-check every value
+    if (lane == 0) {
+      const double *g = a.z + a.last[chunk];
+      while (__double2hiint(ld_relaxed(g)) == sent_hi) __nanosleep(300);
+    }
+    __syncwarp();
     const int i = chunk * 32 + lane;
     if (i < a.n) {
       const int lo = a.rp[i], len = a.rp[i + 1] - lo;
@@ -302,6 +312,7 @@ bool launch_pspmv(DMat &A, int k, const double *z, double *y, const int *done,
   a.y = y;
   a.ld = plane_ld(A.n);
   a.order = A.pipe_order;
+  a.last = A.pipe_last;
   a.state = A.pipe_state;
   a.flag = A.pipe_flag;
   a.done = done;

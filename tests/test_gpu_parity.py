@@ -712,3 +712,41 @@ def test_device_repeated_solves_same_matrix(pkg):
         assert all(r.converged and r.iterations == reps[0].iterations for r in reps)
         assert all(np.array_equal(np.asarray(r.history), np.asarray(reps[0].history))
                    for r in reps)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("method", ["bicgstab", "cgs", "gpbicg"])
+@pytest.mark.parametrize("k", [2, 3])
+def test_device_sweep_pipelined_spmv_is_bit_identical(pkg, monkeypatch, method, k):
+    """The sweep-pipelined SpMV (units.cu pspmv_kernel: A z formed chunk by
+    chunk beside the backward phase of the shuffle-wavefront sweep) computes
+    every row with spmv_row's operations in spmv_row's order, so a solve with
+    the pipeline is the solve without it bit for bit: history, x, iteration
+    count.  Enabled here on a 9-point grid of 40 000 rows (production
+    threshold: 2^18 rows) -- against the same solve with MPK_PIPE=0 and, for
+    the first iterations, against the oracle."""
+    import oracle.oracle as orc
+    from paper_2504_14498_b200 import problems
+
+    rp, ci, vre = problems.convdiff9(200, 5.0)[:3]
+    n = len(rp) - 1
+    P = getattr(pkg.Precision, PREC_OF[k])
+    b0 = pkg.spmv_mixed(_csr(pkg, rp, ci, vre, None),
+                        pkg.DenseVector.from_float64(np.ones(n), P))
+    cfg = pkg.SolverConfig(method=method, precision=P, precond=pkg.PrecondMode.ILU0_MIXED,
+                           spmv_mode="mixed", eps_rel=1e-300, eps_abs=1e-300, max_iter=12)
+    reps = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("MPK_SWEEP_PICK", "swf")
+        monkeypatch.setenv("MPK_PIPE", mode)
+        monkeypatch.setenv("MPK_PIPE_MIN_N", "1")
+        A = pkg.CsrMatrix.from_binary64(n, rp, ci, vre, None, P)  # fresh upload per mode
+        reps[mode] = [pkg.solve(A, b0, cfg) for _ in range(2)]  # second: graph replay
+    for off, on in zip(reps["0"], reps["1"]):
+        assert on.iterations == off.iterations == 12
+        assert bits_equal(np.asarray(on.history), np.asarray(off.history))
+        assert bits_equal(on.x.re, off.x.re)
+    if method == "bicgstab" and k == 2:
+        orep, _, _, ohist = orc.solve(n, rp, ci, vre, None, "bicgstab", 2, b0.re,
+                                      eps_rel=1e-300, eps_abs=1e-300, max_iter=12)
+        _hist_check(reps["1"][0].history, ohist, 2, n_iter=12)
