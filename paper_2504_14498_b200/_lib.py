@@ -14,7 +14,11 @@ import threading
 
 import numpy as np
 
-_SO = pathlib.Path(__file__).resolve().parent / "_lib" / "libmpkb200.so"
+import os
+
+# MPK_B200_LIB: another build of the same library (A/B measurements of kernel variants)
+_SO = pathlib.Path(os.environ.get("MPK_B200_LIB") or
+                   pathlib.Path(__file__).resolve().parent / "_lib" / "libmpkb200.so")
 _lib = None
 _lock = threading.Lock()
 _ctx = {}

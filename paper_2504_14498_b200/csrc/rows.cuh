@@ -45,30 +45,6 @@ __device__ __forceinline__ void spmv_row(const DA &A, int i, const double *x,
 #pragma unroll
   for (int c = 0; c < K; ++c) yr[c] = yi[c] = 0.0;
   const int lo = rp[i], hi = rp[i + 1];
-  if constexpr (!CX && XF) {
-    // binary64 A times an F vector: the entries are fetched four at a time
-    // (independent index / value / x loads ahead of the dependent MC
-    // accumulation, whose order -- ascending columns -- is unchanged)
-    constexpr int B = 4;
-    for (int p0 = lo; p0 < hi; p0 += B) {
-      double ab[B], xb[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const int p = p0 + b < hi ? p0 + b : hi - 1;
-        ab[b] = val[p];
-        xb[b] = x[ci[p]];
-      }
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        if (p0 + b < hi) {
-          double h, l;
-          mul_ff2(ab[b], xb[b], h, l);
-          add2<K>(yr, h, l, yr);
-        }
-      }
-    }
-    return;
-  }
   for (int p = lo; p < hi; ++p) {
     const int j = ci[p];
     if constexpr (!CX) {
@@ -175,9 +151,13 @@ struct Red {
 #ifndef MPK_ROWS_MIN_BLOCKS
 #define MPK_ROWS_MIN_BLOCKS 3
 #endif
+#ifndef MPK_ROWS_MIN_BLOCKS_QD
+#define MPK_ROWS_MIN_BLOCKS_QD MPK_ROWS_MIN_BLOCKS
+#endif
 template <int K, bool CX>
 constexpr int rows_min_blocks() {
-  return (K == 2 && !CX) ? MPK_ROWS_MIN_BLOCKS_DD : MPK_ROWS_MIN_BLOCKS;
+  return (K == 2 && !CX) ? MPK_ROWS_MIN_BLOCKS_DD
+                         : (K == 4 ? MPK_ROWS_MIN_BLOCKS_QD : MPK_ROWS_MIN_BLOCKS);
 }
 template <int K, bool CX, int NH, int NN, class F>
 __global__ void __launch_bounds__(kBlock, rows_min_blocks<K, CX>())
