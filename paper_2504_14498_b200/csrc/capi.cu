@@ -47,6 +47,8 @@ struct mpk_matrix {
   int *fscratch = nullptr;  // [0..1] ticket, [2] bad_row, [3] nonfinite
   float factor_ms = 0.f;
   IoBufs io[5];
+  double *fpub = nullptr;      // factorization publish-by-value copy (FactorArgs::pub)
+  int max_row = 0;             // longest row
   std::vector<double> h_vals;  // complex interleave staging
   int *hres = nullptr;         // pinned factor init/result words
 };
@@ -916,9 +918,11 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
   for (int64_t i = 0; i <= n; ++i) A.h_rp[i] = (int)row_ptr[i];
   for (int64_t p = 0; p < nnz; ++p) A.h_ci[p] = (int)col_idx[p];
   // CsrMatrix._find_diagonals sparse.py:235-243
-  for (int64_t i = 0; i < n; ++i)
+  for (int64_t i = 0; i < n; ++i) {
+    m->max_row = std::max<int>(m->max_row, (int)(row_ptr[i + 1] - row_ptr[i]));
     for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
       if (col_idx[p] == i) A.h_dp[i] = (int)p;
+  }
   cudaStream_t st = ctx->stream;
   const double t_up1 = host_ms();
   // level orders of the L (forward) and U (backward) DAGs; a missing
@@ -1131,6 +1135,7 @@ void mpk_csr_free(mpk_matrix *m) {
                   A.err,    m->rowflag, m->fscratch, A.ord_fp,
                   A.pipe_order, A.pipe_last, A.pipe_state, A.pipe_flag};
   if (m->hres) cudaFreeHost(m->hres);
+  if (m->fpub) cudaFree(m->fpub);
   for (auto &B : m->io) {
     void *q[] = {B.b, B.x, B.stage, B.hist};
     for (void *v : q)
@@ -1187,6 +1192,18 @@ int mpk_ilu0_factor(mpk_matrix *m, int64_t *bad_row, int32_t *structural) {
   fa.nlev = A.levels_f;
   fa.ordp = A.ord_fp;
   fa.nt = A.nt_fp;
+  // real rows that all fit the register-resident row routine, shallow DAG:
+  // results are published by value (ilu.cuh FactorArgs::pub).  Measured:
+  // cfg1 0.46 -> 0.34 ms, cfg2 0.27 -> 0.25 ms; on the deep level-ordered
+  // cfg4 DAG the ~38 k waiting rows polling five values each swamp L2
+  // (39 -> 96 ms), so deep DAGs keep the one-word flags.  MPK_FACTOR_PUB=0|1
+  // forces either protocol.
+  if (!A.cx && A.nnz > 0 && m->max_row <= 32 &&
+      env_int("MPK_FACTOR_PUB", A.ord_fp ? 0 : 1)) {
+    if (!m->fpub) CKR(cudaMalloc(&m->fpub, sizeof(double) * A.nnz));
+    launch_fill_sentinel(m->fpub, A.nnz, st);
+    fa.pub = m->fpub;
+  }
   fa.tick = m->fscratch;
   fa.bad_row = m->fscratch + 2;
   fa.nonfinite = m->fscratch + 3;

@@ -141,6 +141,8 @@ __device__ void factor_row_local(const FactorArgs &a, int i) {
     uks[t] = a.dp[cols[t]];
     kends[t] = a.rp[cols[t] + 1];
   }
+  const bool byval = a.pub != nullptr;
+  const int sent_hi = (int)(kSentBits >> 32);
   for (int t = 0; t < nl; ++t) {
     const int kc = cols[t];
     const int uk = uks[t], kend = kends[t];
@@ -150,13 +152,29 @@ __device__ void factor_row_local(const FactorArgs &a, int i) {
       const int s = uk + 1 + b;
       cb[b] = s < kend ? a.ci[s] : INT_MAX;
     }
-    while (ld_acquire_i(&a.rowflag[kc]) == 0) __nanosleep(20);
-    const double ukk = __ldcg(&a.lu[uk]);
-    double ub[kFactBatch];
+    double ukk, ub[kFactBatch];
+    if (byval) {
+      // the pivot row's diagonal and first batch arrive with the poll itself
+      for (;;) {
+        ukk = ld_relaxed(a.pub + uk);
+        bool ready = __double2hiint(ukk) != sent_hi;
 #pragma unroll
-    for (int b = 0; b < kFactBatch; ++b) {
-      const int s = uk + 1 + b;
-      ub[b] = s < kend ? __ldcg(&a.lu[s]) : 0.0;
+        for (int b = 0; b < kFactBatch; ++b) {
+          const int s = uk + 1 + b;
+          ub[b] = s < kend ? ld_relaxed(a.pub + s) : 0.0;
+          ready = ready && (__double2hiint(ub[b]) != sent_hi);
+        }
+        if (ready) break;
+        __nanosleep(20);
+      }
+    } else {
+      while (ld_acquire_i(&a.rowflag[kc]) == 0) __nanosleep(20);
+      ukk = __ldcg(&a.lu[uk]);
+#pragma unroll
+      for (int b = 0; b < kFactBatch; ++b) {
+        const int s = uk + 1 + b;
+        ub[b] = s < kend ? __ldcg(&a.lu[s]) : 0.0;
+      }
     }
     const double l = ddiv(vals[t], ukk);
     vals[t] = l;
@@ -175,18 +193,36 @@ __device__ void factor_row_local(const FactorArgs &a, int i) {
       for (int b = 0; b < kFactBatch; ++b) {
         const int s = s0 + b;
         cb[b] = s < kend ? a.ci[s] : INT_MAX;
-        ub[b] = s < kend ? __ldcg(&a.lu[s]) : 0.0;
+        ub[b] = 0.0;
+        if (s < kend) {
+          if (byval) {  // the diagonal was seen; the rest of the row follows at once
+            double v = ld_relaxed(a.pub + s);
+            while (__double2hiint(v) == sent_hi) v = ld_relaxed(a.pub + s);
+            ub[b] = v;
+          } else {
+            ub[b] = __ldcg(&a.lu[s]);
+          }
+        }
       }
     }
   }
   bool fin = true;
+  if (byval) {  // publish the diagonal and the upper part first (consumers wait on them)
+    for (int q = d - lo; q < len; ++q) {
+      const double v = vals[q];
+      const double w = __double2hiint(v) == sent_hi
+                           ? __longlong_as_double((long long)kQNaNBits) : v;
+      asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a.pub + lo + q), "d"(w)
+                   : "memory");
+    }
+  }
   for (int q = 0; q < len; ++q) {
     __stcg(&a.lu[lo + q], vals[q]);
     fin = fin && isfin(vals[q]);
   }
   if (vals[d - lo] == 0.0) atomicMin(a.bad_row, i);
   if (!fin) atomicOr(a.nonfinite, 1);
-  st_release_i(&a.rowflag[i], 1);
+  if (!byval) st_release_i(&a.rowflag[i], 1);
 }
 
 template <bool CX>
@@ -1648,6 +1684,20 @@ void launch_sweep_reset(double *y, double *z, int n, bool cx,
     sweep_reset_kernel<true><<<g, kBlock, 0, st>>>(y, z, n, done);
   else
     sweep_reset_kernel<false><<<g, kBlock, 0, st>>>(y, z, n, done);
+}
+
+__global__ void fill_sentinel_kernel(double *p, long long n) {
+  const double s = sent_val();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = s;
+}
+void launch_fill_sentinel(double *p, long long n, cudaStream_t st) {
+  ++tl_launches;
+  long long g = (n + 255) / 256;
+  if (g > sm_count() * 8) g = sm_count() * 8;
+  if (g < 1) g = 1;
+  fill_sentinel_kernel<<<(int)g, 256, 0, st>>>(p, n);
 }
 
 void launch_factor(const FactorArgs &a, bool cx, cudaStream_t st) {

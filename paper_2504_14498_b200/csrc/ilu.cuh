@@ -206,10 +206,17 @@ struct FactorArgs {
   // a warp claims always belong to ONE level and never wait on each other
   const int *ordp = nullptr;
   int nt = 0;      // padded ticket count
+  // Publication by value (real matrices whose rows all fit factor_row_local):
+  // a copy of the factors, sentinel-filled before the launch, into which a
+  // finished row writes its diagonal and upper part with plain relaxed
+  // stores; consumers poll the values they need (as the sweeps do), so no
+  // flag, no release fence and no separate fetch sit between two DAG levels.
+  double *pub = nullptr;
   int *tick;       // [0] ticket, [1] exit counter
   int *bad_row;    // atomicMin of zero-pivot rows (init INT_MAX)
   int *nonfinite;  // set if any factor is non-finite
 };
 void launch_factor(const FactorArgs &a, bool cx, cudaStream_t st);
+void launch_fill_sentinel(double *p, long long n, cudaStream_t st);
 
 }  // namespace mpk
