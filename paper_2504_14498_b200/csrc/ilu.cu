@@ -1731,6 +1731,8 @@ void launch_factor(const FactorArgs &a, bool cx, cudaStream_t st) {
   int per_sm = level ? 1 : 6;  // level order: fewer pollers, shorter hand-off (measured)
   if (const char *e = getenv("MPK_FACTOR_BLOCKS")) per_sm = atoi(e) > 0 ? atoi(e) : per_sm;
   if (blocks > (long long)sm_count() * per_sm) blocks = (long long)sm_count() * per_sm;
+  if (const char *e = getenv("MPK_FACTOR_GRID"))
+    if (atoi(e) > 0 && atoi(e) < blocks) blocks = atoi(e);
   if (cx)
     factor_kernel<true><<<(int)blocks, kBlock, 0, st>>>(b);
   else
