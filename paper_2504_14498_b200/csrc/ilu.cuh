@@ -51,6 +51,9 @@ struct SweepArgs {
 // kernel is released when the forward phase is done, next to the backward
 // launch).  Null: no event.  Only the shuffle-wavefront plan honours it.
 inline thread_local cudaEvent_t tl_sweep_mid = nullptr;
+// ... and makes its second launch wait for this event (work on a side stream
+// that must be done before the backward phase writes the output vector).
+inline thread_local cudaEvent_t tl_sweep_wait = nullptr;
 
 // Level-ordered copy of one sweep phase ("sweep matrix"): position r in
 // level order holds row row[r] whose entries are col/val[ptr[r]..ptr[r+1])

@@ -37,6 +37,10 @@ struct State {
   int done, converged, breakdown, half_exit, have_nrm, sweep_err;
   double eps_rel, eps_abs;
   double relres, true_relres;
+  // BiCGSTAB x update deferred beside the next sweep (krylov_impl.cuh
+  // xu_kernel): iteration whose update is pending / applied, block counter
+  long long xu_it, xu_done;
+  int xu_cnt, xu_pad;
 };
 
 // Cached per-(method, K, field) solver workspace + graph (krylov_impl.cuh)
@@ -162,6 +166,8 @@ constexpr int kPipeRow = 12;  // longest row a pipeline plan accepts
 // see units.cu.  Launches nothing and returns false when the matrix has no
 // pipeline plan.
 void launch_pipe_reset(DMat &A, cudaStream_t st);
+void launch_pipe_delay(cudaStream_t st);
+constexpr size_t kPipeSmem = 88 * 1024;  // keeps side kernels off the sweep CTAs' SMs
 bool launch_pspmv(DMat &A, int k, const double *z, double *y, const int *done,
                   cudaStream_t st);
 int unit_spmv_full(DMat &A, int k, bool adjoint, bool x_is_f, const double *d_x,

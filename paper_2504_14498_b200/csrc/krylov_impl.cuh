@@ -141,6 +141,41 @@ __global__ void true_res_kernel_impl(State *S_, const double *pt_, int G_) {
 }
 
 
+// BiCGSTAB: x = (x + alpha phat) + omega shat of the iteration recorded in
+// S->xu_it (solvers.py:318), applied at the start of the NEXT body beside
+// the forward phase of its first sweep, on the SMs the sweep leaves idle;
+// also resets phat to the sentinel for that sweep's backward phase (this
+// kernel is the last reader of the old phat).  Not skipped on the done flag:
+// the pending update belongs to a completed iteration.  The last block out
+// marks the update as applied.
+template <int K, bool CX>
+__global__ void __launch_bounds__(512, 2)
+    xu_kernel(State *S, MV<K, CX> X, FV<CX> PH, FV<CX> SH, long long n) {
+  const bool pend = S->xu_it != S->xu_done;
+  const Sc al = S->alpha, om = S->omega;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (pend) {
+      double xr[K], xi[K], fr[K], fi[K], tr[K], ti[K];
+      X.load(i, xr, xi);
+      PH.template load_mc<K>(i, fr, fi);
+      e_axpy<K, CX>(al, fr, fi, xr, xi, tr, ti);
+      SH.template load_mc<K>(i, fr, fi);
+      e_axpy<K, CX>(om, fr, fi, tr, ti, xr, xi);
+      X.store(i, xr, xi);
+    }
+    PH.set_sent(i);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&S->xu_cnt, 1) == (int)gridDim.x - 1) {
+      if (pend) S->xu_done = S->xu_it;
+      S->xu_cnt = 0;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------
 // solver object
 // ---------------------------------------------------------------------
@@ -193,6 +228,9 @@ struct Solver : PlanBase {
   DA dap;  // da + the pipeline's result buffer and chunk flags
   cudaEvent_t evp_mid = nullptr, evp_join = nullptr;
   int *cur_started = nullptr;
+  // deferred x update of BiCGSTAB (xu_kernel) beside the next forward phase
+  bool xu_on = false;
+  cudaEvent_t ev_xu0 = nullptr, ev_xu1 = nullptr;
   State *hp = nullptr;  // pinned host staging of the device State (x2)
   int *hpi = nullptr;
 
@@ -252,6 +290,14 @@ struct Solver : PlanBase {
       dap.pflag = A.pipe_flag;
       cudaEventCreateWithFlags(&evp_mid, cudaEventDisableTiming);
       cudaEventCreateWithFlags(&evp_join, cudaEventDisableTiming);
+      const char *e = getenv("MPK_XU");
+      xu_on = p.method == kBiCGSTAB && !(e && e[0] == '0');
+      if (xu_on) {
+        cudaEventCreateWithFlags(&ev_xu0, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_xu1, cudaEventDisableTiming);
+        cudaFuncSetAttribute(xu_kernel<K, CX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kPipeSmem);
+      }
     }
     S = (State *)dalloc(sizeof(State));
     part = (double *)dalloc(sizeof(double) * 6 * kMaxGrid * 8);
@@ -290,6 +336,8 @@ struct Solver : PlanBase {
     if (evj3) cudaEventDestroy(evj3);
     if (evp_mid) cudaEventDestroy(evp_mid);
     if (evp_join) cudaEventDestroy(evp_join);
+    if (ev_xu0) cudaEventDestroy(ev_xu0);
+    if (ev_xu1) cudaEventDestroy(ev_xu1);
     if (hp) cudaFreeHost(hp);
     if (hpi) cudaFreeHost(hpi);
     for (void *q : allocs) cudaFree(q);
@@ -351,21 +399,41 @@ struct Solver : PlanBase {
   // with a pipeline plan, A z is formed chunk by chunk beside the backward
   // phase (st3, released between the two phases of the sweep) into
   // `prebuf`; the row kernel then loads the flagged chunks (DA::pflag).
-  void sweep_spmv(const double *in_re, const double *in_im, double *y, double *z) {
+  void sweep_spmv(const double *in_re, const double *in_im, double *y, double *z,
+                  cudaEvent_t before_bwd = nullptr) {
     if (!pipe_on) {
       sweep(in_re, in_im, y, z, false, 0);
       return;
     }
     launch_pipe_reset(A, st);
     tl_sweep_mid = evp_mid;
+    tl_sweep_wait = before_bwd;
     cur_started = A.pipe_state + 1;
     sweep(in_re, in_im, y, z, false, 0);
     cur_started = nullptr;
     tl_sweep_mid = nullptr;
+    tl_sweep_wait = nullptr;
     cudaStreamWaitEvent(st3, evp_mid, 0);
     launch_pspmv(A, K, z, prebuf, done, st3);
     cudaEventRecord(evp_join, st3);
     cudaStreamWaitEvent(st, evp_join, 0);
+  }
+  // deferred x update + phat sentinel reset (xu_kernel) on st3, released
+  // when everything enqueued on st so far is done; ev_xu1 marks its end
+  void launch_xu(bool side) {
+    const MVt X = mv(x);
+    const FVt PH = fvv(phat), SH = fvv(shat);
+    ++tl_launches;
+    if (side) {
+      cudaEventRecord(ev_xu0, st);
+      cudaStreamWaitEvent(st3, ev_xu0, 0);
+      launch_pipe_delay(st3);  // the forward phase's clusters are placed first
+      const int grid = (sm_count() - ssweep_bwd_ctas(A.smat.ss)) * 2;
+      xu_kernel<K, CX><<<grid, 512, kPipeSmem, st3>>>(S, X, PH, SH, (long long)n);
+      cudaEventRecord(ev_xu1, st3);
+    } else {
+      xu_kernel<K, CX><<<sm_count() * 2, 512, 0, st>>>(S, X, PH, SH, (long long)n);
+    }
   }
   // z = U^-1 L^-1 in at working precision (real; planar K-component)
   void mc_sweep(const double *in, double *z, int which, bool after_loop,
@@ -505,6 +573,7 @@ struct Solver : PlanBase {
     const DA a = pipe_on ? dap : da;
     const long long L = ld;
     const int np_ = nopre;
+    const bool xu = xu_on;
     // F5+F1: [end of the previous iteration, deferred: rho_old = rho,
     // ||r|| record + tests, iteration count] then [this iteration: rho,
     // rho/omega zero tests, beta = (rho/rho_old)*(alpha/omega)].  The norm
@@ -569,9 +638,10 @@ struct Solver : PlanBase {
                           P.store(i, pr, pi);
                         }
                         Y.set_sent(i);
-                        PH.set_sent(i);
+                        if (!xu) PH.set_sent(i);
                       });
-    sweep_spmv(head_re(pp), head_im(pp), A.sw_y, phat);
+    if (xu) launch_xu(true);
+    sweep_spmv(head_re(pp), head_im(pp), A.sw_y, phat, xu ? ev_xu1 : nullptr);
     // K4: v = A phat ; sigma = hdot(rt0, v)
     const double *phc = phat;
     pre_spmv(phat, !nopre);
@@ -653,13 +723,18 @@ struct Solver : PlanBase {
     //     norm2(r) [slot 1], next rho = hdot(rt0, r) [slot 0]
     rows<K, CX, 1, 1>(n, done, part, st,
                       [=] __device__(long long i, Red<K, CX, 1, 1> &red) {
-                        double xr[K], xi[K], fr[K], fi[K], tr[K], ti[K];
-                        X.load(i, xr, xi);
-                        PH.template load_mc<K>(i, fr, fi);
-                        e_axpy<K, CX>(Sd->alpha, fr, fi, xr, xi, tr, ti);
-                        SH.template load_mc<K>(i, fr, fi);
-                        e_axpy<K, CX>(Sd->omega, fr, fi, tr, ti, xr, xi);
-                        X.store(i, xr, xi);
+                        double tr[K], ti[K];
+                        if (!xu) {
+                          double xr[K], xi[K], fr[K], fi[K];
+                          X.load(i, xr, xi);
+                          PH.template load_mc<K>(i, fr, fi);
+                          e_axpy<K, CX>(Sd->alpha, fr, fi, xr, xi, tr, ti);
+                          SH.template load_mc<K>(i, fr, fi);
+                          e_axpy<K, CX>(Sd->omega, fr, fi, tr, ti, xr, xi);
+                          X.store(i, xr, xi);
+                        } else if (i == 0) {
+                          Sd->xu_it = Sd->it;  // applied by xu_kernel in the next body
+                        }
                         double sr[K], si[K], rr[K], ri[K], qr[K], qi[K];
                         Sv.load(i, sr, si);
                         T.load(i, tr, ti);
@@ -675,6 +750,8 @@ struct Solver : PlanBase {
   }
 
   void bicgstab_finish(const State &hs) {
+    // x update of the last completed iteration, if no later body applied it
+    if (xu_on && hs.xu_it != hs.xu_done) launch_xu(false);
     if (hs.half_exit) {
       const MVt X = mv(x);
       const FVt PH = fvv(phat);

@@ -1197,6 +1197,7 @@ void launch_ssweep(const SweepArgs &a, const SSweep &w, cudaStream_t st) {
       grid = (Q.ngroups + Q.cl - 1) / Q.cl * Q.cl;
     else if (grid > sm_count())
       grid = sm_count();
+    if (P == &w.b && tl_sweep_wait) cudaStreamWaitEvent(st, tl_sweep_wait, 0);
     launch_phase(a, Q, w.W, grid, w.smem, st);
     if (P == &w.f && tl_sweep_mid) cudaEventRecord(tl_sweep_mid, st);
   }

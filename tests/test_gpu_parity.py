@@ -750,3 +750,38 @@ def test_device_sweep_pipelined_spmv_is_bit_identical(pkg, monkeypatch, method, 
         orep, _, _, ohist = orc.solve(n, rp, ci, vre, None, "bicgstab", 2, b0.re,
                                       eps_rel=1e-300, eps_abs=1e-300, max_iter=12)
         _hist_check(reps["1"][0].history, ohist, 2, n_iter=12)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("tol,max_iter", [(1e-22, None), (1e-8, None), (1e-300, 1), (1e-300, 7)])
+def test_device_pipelined_bicgstab_exits_match_plain_path(pkg, monkeypatch, tol, max_iter):
+    """BiCGSTAB with the sweep-pipelined SpMV and the deferred x update
+    (xu_kernel: x = (x + alpha phat) + omega shat of iteration k applied at
+    the start of body k+1, or by finish() when no later body runs) against
+    the plain path, on every way out of the loop: convergence at the end of
+    an iteration or at the half step, and the iteration cap.  Same iteration
+    count, history, x and true residual, bit for bit."""
+    from paper_2504_14498_b200 import problems
+
+    rp, ci, vre = problems.convdiff9(200, 5.0)[:3]
+    n = len(rp) - 1
+    P = pkg.Precision.DD
+    b0 = pkg.spmv_mixed(_csr(pkg, rp, ci, vre, None),
+                        pkg.DenseVector.from_float64(np.ones(n), P))
+    cfg = pkg.SolverConfig(method="bicgstab", precision=P, precond=pkg.PrecondMode.ILU0_MIXED,
+                           spmv_mode="mixed", eps_rel=tol, eps_abs=1e-300, max_iter=max_iter)
+    reps = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("MPK_SWEEP_PICK", "swf")
+        monkeypatch.setenv("MPK_PIPE", mode)
+        monkeypatch.setenv("MPK_PIPE_MIN_N", "1")
+        A = pkg.CsrMatrix.from_binary64(n, rp, ci, vre, None, P)
+        reps[mode] = [pkg.solve(A, b0, cfg) for _ in range(2)]
+    for off, on in zip(reps["0"], reps["1"]):
+        assert on.iterations == off.iterations and on.converged == off.converged
+        assert (on.breakdown or "") == (off.breakdown or "")
+        assert bits_equal(np.asarray(on.history), np.asarray(off.history))
+        assert bits_equal(on.x.re, off.x.re)
+        assert on.true_relres == off.true_relres
+    if max_iter is None:
+        assert reps["1"][0].converged
