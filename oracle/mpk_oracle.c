@@ -8,7 +8,7 @@
  * /root/reference/pkg/src/mpkrylov (file:line cited per function).  Build
  * with -O2 -ffp-contract=off (no FMA contraction, no fast-math) so every
  * binary64 operation rounds exactly as CPython / numba do.  Pinned against
- * reference-generated golden vectors (tests/golden/, tests/test_oracle.py).
+ * reference-generated golden vectors (tests/golden/, tests/test_oracle_golden.py).
  */
 #include "mpk_oracle.h"
 
