@@ -773,6 +773,14 @@ def roofline_blocks(res, args, hbm, peak_src, sm_mhz):
         "traffic": t.get("dram_bytes_per_launch"), "algorithmic_bytes": sb,
         "avg_ms": probe["spmv_ms"], "peak_source": peak_src,
         "fp64_pipe_pct": t.get("fp64_pipe_pct"), "traffic_source": t.get("source")}
+    if probe.get("sweep_info", [0] * 3)[2] == 5 and p.n >= (1 << 18) and c == 1 and args.precond == "ilu0-mixed":
+        # cfg4-class systems: inside a solve this SpMV does not run as a kernel of
+        # its own -- pspmv_kernel (csrc/units.cu) forms A z chunk by chunk beside the
+        # backward phase of the sweep that produces z
+        blocks["spmv"]["in_solve"] = (
+            "pipelined beside the backward sweep on the 84 SMs it leaves idle "
+            "(pspmv_kernel); exposed per SpMV site: the dot-product row kernel only "
+            "(profiles/r02_launch_summary_cfg4_pipelined.txt)")
     return blocks
 
 

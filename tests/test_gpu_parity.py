@@ -716,7 +716,7 @@ def test_device_repeated_solves_same_matrix(pkg):
 
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("method", ["bicgstab", "cgs", "gpbicg"])
-@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("k", [2, 3, 4])
 def test_device_sweep_pipelined_spmv_is_bit_identical(pkg, monkeypatch, method, k):
     """The sweep-pipelined SpMV (units.cu pspmv_kernel: A z formed chunk by
     chunk beside the backward phase of the shuffle-wavefront sweep) computes
