@@ -20,7 +20,7 @@ import os
 _SO = pathlib.Path(os.environ.get("MPK_B200_LIB") or
                    pathlib.Path(__file__).resolve().parent / "_lib" / "libmpkb200.so")
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()  # re-entrant: context() loads the library under it
 _ctx = {}
 
 MPK_OK = 0

@@ -1553,8 +1553,10 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   hs = *sv->hp;
   tl_phase[3] = host_ms();  // loop done (synchronised)
   if (use_cond && !sharded) tl_launches += sv->body_nodes * hs.body_runs;
-  if (!hs.done) {
-    // loop ran out without a device-side stop (max_iter reached)
+  const bool ran_out = !hs.done;
+  if (ran_out) {
+    // loop ran out without a device-side stop (max_iter reached; only the
+    // plain-graph replay mode, MPK_NO_COND_GRAPH, can end this way)
     hs.iterations = p.max_iter;
     hs.converged = 0;
     hs.breakdown = kBdNone;
@@ -1589,6 +1591,11 @@ int run_typed(DMat &A, const SolveParams &p, const double *d_b, double *d_x,
   CK(cudaMemcpyAsync(sv->hp, sv->S, sizeof(State), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   hs = *sv->hp;
+  if (ran_out) {  // the device State never recorded a stop
+    hs.iterations = p.max_iter;
+    hs.converged = 0;
+    hs.breakdown = kBdNone;
+  }
   tl_phase[4] = host_ms();  // finish + true residual done
   if (chk_after) e_after = *sv->hpi;
   CK(cudaGetLastError());

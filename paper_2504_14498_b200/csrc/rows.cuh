@@ -245,7 +245,8 @@ __global__ void seq_chain_kernel(long long n, const int *done,
 template <class KFn>
 inline void prefer_max_smem(KFn kfn) {
   static bool done_once = false;
-  if (!done_once) {
+  static const bool off = getenv("MPK_NO_MAX_SMEM") != nullptr;  // A/B knob
+  if (!done_once && !off) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
     done_once = true;

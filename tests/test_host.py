@@ -190,3 +190,20 @@ def test_integration_binding_signatures():
             else:
                 ctype = prm.replace("const ", "").split()[0]
                 assert scalar[ctype] == arg, (fn, prm, arg)
+
+
+def test_first_use_paths_do_not_self_deadlock():
+    """context() creates the device context under the module lock and loads
+    the library inside it; the lock must be re-entrant (a solve() as the very
+    first call of a process used to hang on itself).  Checked in a fresh
+    interpreter without a GPU: the call must come back (with the CUDA error
+    of a GPU-less box), not block."""
+    import subprocess
+    import sys
+
+    code = ("import paper_2504_14498_b200._lib as L\n"
+            "try:\n    L.context()\nexcept RuntimeError as e:\n    print('returned', type(e).__name__)\n"
+            "else:\n    print('returned ok')\n")
+    out = subprocess.run([sys.executable, "-c", code], cwd=str(ROOT), capture_output=True,
+                         text=True, timeout=120)
+    assert "returned" in out.stdout, (out.stdout, out.stderr)
