@@ -780,7 +780,7 @@ def roofline_blocks(res, args, hbm, peak_src, sm_mhz):
         blocks["spmv"]["in_solve"] = (
             "pipelined beside the backward sweep on the 84 SMs it leaves idle "
             "(pspmv_kernel); exposed per SpMV site: the dot-product row kernel only "
-            "(profiles/r02_launch_summary_cfg4_pipelined.txt)")
+            "(profiles/r02_launch_summary_cfg4_final.txt)")
     return blocks
 
 
