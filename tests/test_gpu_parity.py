@@ -785,3 +785,35 @@ def test_device_pipelined_bicgstab_exits_match_plain_path(pkg, monkeypatch, tol,
         assert on.true_relres == off.true_relres
     if max_iter is None:
         assert reps["1"][0].converged
+
+
+@pytest.mark.timeout(300)
+def test_device_pipelined_solve_with_nonfinite_data_ends(pkg, monkeypatch):
+    """A non-finite right-hand side on the pipelined path (the SpMV kernel
+    polls the sweep's output for the sentinel pattern): the NaN values the
+    sweep publishes are ordinary values to the pipeline, the solve stops with
+    the reference's breakdown report instead of waiting, and the same matrix
+    then solves a clean system bit-identically to the plain path."""
+    from paper_2504_14498_b200 import problems
+
+    rp, ci, vre = problems.convdiff9(200, 5.0)[:3]
+    n = len(rp) - 1
+    P = pkg.Precision.DD
+    monkeypatch.setenv("MPK_SWEEP_PICK", "swf")
+    monkeypatch.setenv("MPK_PIPE_MIN_N", "1")
+    cfg = pkg.SolverConfig(method="bicgstab", precision=P, precond=pkg.PrecondMode.ILU0_MIXED,
+                           spmv_mode="mixed", eps_rel=1e-20, eps_abs=1e-300, max_iter=50)
+    A = pkg.CsrMatrix.from_binary64(n, rp, ci, vre, None, P)
+    bad = np.ones(n)
+    bad[n // 2] = np.nan
+    bad[7] = np.array([0x7FF40000DEADBEEF], dtype=np.uint64).view(np.float64)[0]
+    rep = pkg.solve(A, pkg.DenseVector.from_float64(bad, P), cfg)
+    assert not rep.converged and rep.breakdown is not None
+    b0 = pkg.spmv_mixed(A.demoted(), pkg.DenseVector.from_float64(np.ones(n), P))
+    good = pkg.solve(A, b0, cfg)
+    monkeypatch.setenv("MPK_PIPE", "0")
+    A2 = pkg.CsrMatrix.from_binary64(n, rp, ci, vre, None, P)
+    plain = pkg.solve(A2, b0, cfg)
+    assert good.iterations == plain.iterations and good.converged == plain.converged
+    assert bits_equal(np.asarray(good.history), np.asarray(plain.history))
+    assert bits_equal(good.x.re, plain.x.re)
