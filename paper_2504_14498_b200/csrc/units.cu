@@ -310,7 +310,10 @@ bool launch_pspmv(DMat &A, int k, const double *z, double *y, const int *done,
   if (!A.pipe_order || A.cx || need <= 0 || need >= sm_count()) return false;
   PipeArgs a{};
   a.n = A.n;
-  a.nchunks = A.pipe_nchunks;
+  // the chunks that become ready last are left to the consumer kernel, which
+  // runs on all SMs right after the sweep (MPK_PIPE_FRAC: percent piped)
+  static const int frac = getenv("MPK_PIPE_FRAC") ? atoi(getenv("MPK_PIPE_FRAC")) : 100;
+  a.nchunks = (int)((long long)A.pipe_nchunks * (frac < 1 ? 1 : frac > 100 ? 100 : frac) / 100);
   a.need_started = need;
   a.rp = A.rp;
   a.ci = A.ci;
@@ -323,7 +326,8 @@ bool launch_pspmv(DMat &A, int k, const double *z, double *y, const int *done,
   a.state = A.pipe_state;
   a.flag = A.pipe_flag;
   a.done = done;
-  const int grid = (sm_count() - need) * 2;
+  static const int bps = getenv("MPK_PIPE_BPS") ? atoi(getenv("MPK_PIPE_BPS")) : 2;  // A/B knob
+  const int grid = (sm_count() - need) * (bps > 0 ? bps : 2);
   ++tl_launches;
   launch_pipe_delay(st);
   switch (k) {
