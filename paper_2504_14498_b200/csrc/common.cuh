@@ -422,6 +422,29 @@ __device__ __forceinline__ void acc_combine(Acc<K, CX> &a,
   if constexpr (CX) add<K>(a.im, b.im, a.im);
 }
 
+// The one-block finalize kernels run a few thousand instructions ONCE, on a
+// cold instruction cache: their time follows their code size (ncu: 4.4 k
+// instructions 17 us, 9.9 k instructions 41 us).  Their reduction trees
+// therefore call ONE copy of the MC addition instead of inlining it at each
+// of the ~9 tree levels (x2 for the complex variant).
+template <int K>
+__device__ __noinline__ void add_call(double *x, const double *y) {
+  double a[K], b[K], r[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    a[c] = x[c];
+    b[c] = y[c];
+  }
+  add<K>(a, b, r);
+#pragma unroll
+  for (int c = 0; c < K; ++c) x[c] = r[c];
+}
+template <int K, bool CX>
+__device__ __forceinline__ void acc_combine_call(Acc<K, CX> &a, const Acc<K, CX> &b) {
+  add_call<K>(a.re, b.re);
+  if constexpr (CX) add_call<K>(a.im, b.im);
+}
+
 template <int K, bool CX>
 __device__ __forceinline__ void acc_shfl_down(Acc<K, CX> &o,
                                               const Acc<K, CX> &a, int off) {
@@ -440,14 +463,19 @@ __device__ __forceinline__ void acc_shfl_down(Acc<K, CX> &o,
 // Block tree: lane tree (16,8,4,2,1) then warp leaders in smem, then warp 0
 // tree over kWarpsPerBlock entries.  Result valid in threadIdx.x == 0.
 // smem must hold kWarpsPerBlock * 2K doubles.  All threads must call.
-template <int K, bool CX>
+template <int K, bool CX, bool CALL = false>
 __device__ __forceinline__ void block_reduce(Acc<K, CX> &a, double *smem) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     Acc<K, CX> o;
     acc_shfl_down<K, CX>(o, a, off);
-    if (lane < off) acc_combine<K, CX>(a, o);
+    if (lane < off) {
+      if constexpr (CALL)
+        acc_combine_call<K, CX>(a, o);
+      else
+        acc_combine<K, CX>(a, o);
+    }
   }
   __syncthreads();
   if (lane == 0) {
@@ -473,7 +501,12 @@ __device__ __forceinline__ void block_reduce(Acc<K, CX> &a, double *smem) {
     for (int off = kWarpsPerBlock / 2; off >= 1; off >>= 1) {
       Acc<K, CX> o;
       acc_shfl_down<K, CX>(o, b, off);
-      if (lane < off) acc_combine<K, CX>(b, o);
+      if (lane < off) {
+        if constexpr (CALL)
+          acc_combine_call<K, CX>(b, o);
+        else
+          acc_combine<K, CX>(b, o);
+      }
     }
     a = b;
   }
@@ -508,9 +541,9 @@ __device__ __forceinline__ Sc finalize_slot(const double *part, int slot,
       v.re[c] = q[c];
       v.im[c] = q[4 + c];
     }
-    acc_combine<K, CX>(a, v);
+    acc_combine_call<K, CX>(a, v);
   }
-  block_reduce<K, CX>(a, smem);
+  block_reduce<K, CX, true>(a, smem);
   Sc s = sc_zero();
 #pragma unroll
   for (int c = 0; c < K; ++c) {
@@ -541,13 +574,13 @@ __device__ __forceinline__ void fin_slot_warp(const double *part, int slot, int 
       v.re[c] = q[c];
       v.im[c] = q[4 + c];
     }
-    acc_combine<K, C>(a, v);
+    acc_combine_call<K, C>(a, v);
   }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     Acc<K, C> o;
     acc_shfl_down<K, C>(o, a, off);
-    if (lane < off) acc_combine<K, C>(a, o);
+    if (lane < off) acc_combine_call<K, C>(a, o);
   }
   if (lane == 0) {
 #pragma unroll
@@ -574,7 +607,7 @@ __device__ __forceinline__ void fin_slot_cross(const double *wsm0, int W,
     if (off >= W) continue;  // uniform
     Acc<K, C> o;
     acc_shfl_down<K, C>(o, b, off);
-    if (lane < off) acc_combine<K, C>(b, o);
+    if (lane < off) acc_combine_call<K, C>(b, o);
   }
   if (lane == 0) {
 #pragma unroll
@@ -595,18 +628,33 @@ __device__ __forceinline__ void finalize_slots(const double *part, int G,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = warp / W, wi = warp % W;
   Sc *res = reinterpret_cast<Sc *>(smem + 8 * kWarpsPerBlock);
+  // only the variants the slot list needs are compiled (a real solve has no
+  // complex slot: half the code of this cold single-block kernel)
+  constexpr bool anyc = (CXS || ...), allc = (CXS && ...);
   if (s < NS) {
-    if (cxs[s])
-      fin_slot_warp<K, true>(part, s, G, wi, W, lane, smem + 8 * warp);
-    else
+    if constexpr (!anyc) {
       fin_slot_warp<K, false>(part, s, G, wi, W, lane, smem + 8 * warp);
+    } else if constexpr (allc) {
+      fin_slot_warp<K, true>(part, s, G, wi, W, lane, smem + 8 * warp);
+    } else {
+      if (cxs[s])
+        fin_slot_warp<K, true>(part, s, G, wi, W, lane, smem + 8 * warp);
+      else
+        fin_slot_warp<K, false>(part, s, G, wi, W, lane, smem + 8 * warp);
+    }
   }
   __syncthreads();
   if (s < NS && wi == 0) {
-    if (cxs[s])
-      fin_slot_cross<K, true>(smem + 8 * warp, W, lane, res + s);
-    else
+    if constexpr (!anyc) {
       fin_slot_cross<K, false>(smem + 8 * warp, W, lane, res + s);
+    } else if constexpr (allc) {
+      fin_slot_cross<K, true>(smem + 8 * warp, W, lane, res + s);
+    } else {
+      if (cxs[s])
+        fin_slot_cross<K, true>(smem + 8 * warp, W, lane, res + s);
+      else
+        fin_slot_cross<K, false>(smem + 8 * warp, W, lane, res + s);
+    }
   }
   __syncthreads();
 #pragma unroll

@@ -42,7 +42,7 @@ __device__ __forceinline__ void record(State *S, double *hist, const Sc &v) {
 }
 
 template <int K>
-__device__ __forceinline__ Sc sqrt_sc(const Sc &ss) {
+__device__ __noinline__ Sc sqrt_sc(const Sc &ss) {  // one copy per kernel (code size)
   Sc o = sc_zero();
   sqrt_mc<K>(R<K>(ss), R<K>(o));
   return o;
