@@ -278,7 +278,42 @@ MPK_HD void renorm_passes(double (&t)[M]) {
 }
 
 template <int M, int K>
+MPK_HD void renorm_body(double (&t)[M], double (&out)[K]);
+
+// TD / QD on the device: ONE copy of each renormalisation per kernel, called.
+// The TD / QD row kernels of the BASELINE configs run on small systems (one
+// element per thread: the body executes once per warp), where ncu attributes
+// a third of the stall cycles to instruction fetch (r02 cfg5 captures: 34 %
+// "no instruction") -- the inlined renormalisations are most of the code.
+// DD keeps the inlined form (cfg4: the loop body is reused 28 times).
+#if defined(__CUDACC__)
+template <int M, int K>
+__device__ __noinline__ void renorm_call(double *t, double *out) {
+  double a[M], o[K];
+#pragma unroll
+  for (int i = 0; i < M; ++i) a[i] = t[i];
+  renorm_body<M, K>(a, o);
+#pragma unroll
+  for (int i = 0; i < K; ++i) out[i] = o[i];
+}
+#endif
+
+template <int M, int K>
 MPK_HD void renorm(double (&t)[M], double (&out)[K]) {
+#ifndef MPK_RENORM_CALL_MIN_K
+#define MPK_RENORM_CALL_MIN_K 3  // DD measured slower when called (cfg1 --precond ilu0 455 -> 406 it/s)
+#endif
+#if defined(__CUDA_ARCH__) && !defined(MPK_INLINE_RENORM)
+  if constexpr (K >= MPK_RENORM_CALL_MIN_K) {
+    renorm_call<M, K>(t, out);
+    return;
+  }
+#endif
+  renorm_body<M, K>(t, out);
+}
+
+template <int M, int K>
+MPK_HD void renorm_body(double (&t)[M], double (&out)[K]) {
   MPK_RT(0);
   bool small = true;
 #pragma unroll
