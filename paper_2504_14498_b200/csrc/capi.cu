@@ -894,17 +894,6 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
     return fail(MPK_INVALID, "matrix too large for int32 indices");
   if (row_ptr[0] != 0 || row_ptr[n] != nnz)
     return fail(MPK_INVALID, "inconsistent CSR row_ptr");
-  for (int64_t i = 0; i < n; ++i) {
-    if (row_ptr[i + 1] < row_ptr[i])
-      return fail(MPK_INVALID, "row_ptr must be non-decreasing");
-    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
-      const int64_t c = col_idx[p];
-      if (c < 0 || c >= n || (p > row_ptr[i] && c <= col_idx[p - 1]))
-        return fail(MPK_INVALID,
-                    "row " + std::to_string(i) +
-                        ": columns must be strictly increasing and in range");
-    }
-  }
   CKR(cudaSetDevice(ctx->device));
   mpk_matrix *m = new mpk_matrix;
   m->ctx = ctx;
@@ -915,13 +904,55 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
   A.h_rp.resize(n + 1);
   A.h_ci.resize(nnz);
   A.h_dp.assign(n, -1);
-  for (int64_t i = 0; i <= n; ++i) A.h_rp[i] = (int)row_ptr[i];
-  for (int64_t p = 0; p < nnz; ++p) A.h_ci[p] = (int)col_idx[p];
-  // CsrMatrix._find_diagonals sparse.py:235-243
-  for (int64_t i = 0; i < n; ++i) {
-    m->max_row = std::max<int>(m->max_row, (int)(row_ptr[i + 1] - row_ptr[i]));
-    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
-      if (col_idx[p] == i) A.h_dp[i] = (int)p;
+  A.h_rp[n] = (int)nnz;
+  // validation (CsrMatrix._validate sparse.py:217-233), int32 copies and the
+  // diagonal positions (_find_diagonals :235-243) in one pass over the
+  // rows, on a few host threads for large matrices; the first offending row
+  // (lowest index) is the one reported
+  {
+    const int T = n >= (1 << 16) ? (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    std::vector<int64_t> bad(T, -1), badkind(T, 0);
+    std::vector<int> mrow(T, 0);
+    auto work = [&](int t) {
+      const int64_t per = (n + T - 1) / T, lo = std::min<int64_t>(n, per * t),
+                    hi = std::min<int64_t>(n, per * (t + 1));
+      for (int64_t i = lo; i < hi; ++i) {
+        A.h_rp[i] = (int)row_ptr[i];
+        if (row_ptr[i + 1] < row_ptr[i] || row_ptr[i] < 0 || row_ptr[i + 1] > nnz) {
+          bad[t] = i;
+          badkind[t] = 1;
+          return;
+        }
+        mrow[t] = std::max<int>(mrow[t], (int)(row_ptr[i + 1] - row_ptr[i]));
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+          const int64_t c = col_idx[p];
+          if (c < 0 || c >= n || (p > row_ptr[i] && c <= col_idx[p - 1])) {
+            bad[t] = i;
+            badkind[t] = 2;
+            return;
+          }
+          A.h_ci[p] = (int)c;
+          if (c == i) A.h_dp[i] = (int)p;
+        }
+      }
+    };
+    if (T == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; ++t) th.emplace_back(work, t);
+      for (auto &x : th) x.join();
+    }
+    for (int t = 0; t < T; ++t) {
+      if (bad[t] < 0) continue;
+      const int64_t i = bad[t];
+      const bool rp_bad = badkind[t] == 1;
+      delete m;
+      if (rp_bad) return fail(MPK_INVALID, "row_ptr must be non-decreasing");
+      return fail(MPK_INVALID, "row " + std::to_string(i) +
+                                   ": columns must be strictly increasing and in range");
+    }
+    for (int t = 0; t < T; ++t) m->max_row = std::max(m->max_row, mrow[t]);
   }
   cudaStream_t st = ctx->stream;
   const double t_up1 = host_ms();
@@ -930,13 +961,16 @@ int mpk_csr_upload(mpk_ctx *ctx, int64_t n, int64_t nnz,
   std::vector<int> of, ob, pf, pb;
   {
     const int *rp = A.h_rp.data(), *dp = A.h_dp.data();
+    std::thread tb([&] {  // the two DAGs are independent
+      A.levels_b = level_order(
+          (int)n, true, A.h_ci.data(),
+          [&](int i) { return dp[i] < 0 ? rp[i + 1] : dp[i] + 1; },
+          [&](int i) { return rp[i + 1]; }, ob, pb);
+    });
     A.levels_f = level_order(
         (int)n, false, A.h_ci.data(), [&](int i) { return rp[i]; },
         [&](int i) { return dp[i] < 0 ? rp[i] : dp[i]; }, of, pf);
-    A.levels_b = level_order(
-        (int)n, true, A.h_ci.data(),
-        [&](int i) { return dp[i] < 0 ? rp[i + 1] : dp[i] + 1; },
-        [&](int i) { return rp[i + 1]; }, ob, pb);
+    tb.join();
   }
   const double t_up2 = host_ms();
   // deep L DAG (grid stencils: thousands of levels): factorization tickets
